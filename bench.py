@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark of the IRK stage-equation solve on B200 (BASELINE.json metric).
+
+Workload (N = 1): BASELINE ``configs[1]`` -- 2-D viscous Burgers on a
+1024^2 periodic grid, nu = 1e-2, Gauss 3-stage (order 6), dt = 5e-4,
+seeded Fourier-mode u0 (|k| <= 8, sigma = 0.5); manifest: variant 3,
+gamma*, Jacobi-4 inner solves, restart 200, krylov_maxit 5000, Newton rtol
+1e-9, Krylov rtol 1e-5 (reference defaults).  A "step" is one IRK time step
+(all Newton iterations of the stage solve + the u update), marching the same
+trajectory: W warm-up steps, then K timed steps.
+
+Headline metric: stage-DOF updates/s = sum_steps(newton_its * s * N) / time
+(SURVEY 8d); IRK steps/s and the CGS2 roofline are reported beside it.
+
+``--impl reference`` times the reference algorithm's CPU restatement
+(``oracle/``, a numpy/scipy port of irkit; the reference itself is Python and
+cannot travel to the GPU box) on the host cores: each of its steps is one full
+Newton iteration of the same trajectory at full size (a bounded sample).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "stage-DOF updates/s (IRK stage solve; configs[1] Burgers 1024^2 Gauss(3))"
+UNIT = "DOF/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[3:7]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        import torch
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ------------------------------------------------------------ CPU leg
+
+
+class OracleNewtonStream:
+    """Newton iterations of the configs[1] trajectory on the CPU oracle, one
+    per call (a complete reference Newton iteration: linearize s stages,
+    variant-3 combine, transformed solve, residual)."""
+
+    def __init__(self, spec):
+        from oracle import irk
+        from oracle import tableau as otab
+        from oracle.problems import build_problem
+
+        self.irk = irk
+        prob = spec.problem
+        pd = build_problem(prob.kind, prob.shape, **prob.oracle_params())
+        self.sys = irk.OdeSystem(pd.dim, pd.rhs, pd.linearize_csr)
+        self.prep = otab.prepare(spec.family, spec.s)
+        sv = spec.solver
+        self.cfg = irk.Config(variant=sv["variant"], krylov_maxit=sv["krylov_maxit"],
+                              restart=sv["restart"], inner=sv["inner"],
+                              newton_maxit=sv["newton_maxit"])
+        self.dt = spec.dt
+        self.u = spec.u0()
+        self.t = 0.0
+        self.s = spec.s
+        self.n = pd.dim
+        self._new_step()
+
+    def _new_step(self):
+        irk, tab = self.irk, self.prep.tableau
+        self.k = np.zeros((self.s, self.n))
+        self.res = irk.stage_residual(self.sys, self.u, self.k, self.t, self.dt, tab)
+        f0 = np.linalg.norm(self.res)
+        self.tol = max(self.cfg.newton_rtol * f0, self.cfg.newton_abs_floor)
+
+    def newton_iteration(self):
+        irk, tab, cfg = self.irk, self.prep.tableau, self.cfg
+        if np.linalg.norm(self.res) <= self.tol:
+            self.u = self.u + self.dt * (tab.b0 @ self.k)
+            self.t += self.dt
+            self._new_step()
+        times = self.t + tab.c0 * self.dt
+        u_stage = self.u[None, :] + self.dt * (tab.a0 @ self.k)
+        ops = [self.sys.linearize(u_stage[i], times[i]) for i in range(self.s)]
+        vjac = irk.build_variant_jacobian(self.prep, ops, cfg.variant, cfg.variant0_stage)
+        dk, st = irk.solve_transformed(self.prep, vjac, self.dt, self.res, cfg.gamma_mode,
+                                       cfg.inner, cfg.krylov_rtol, cfg.krylov_maxit, cfg.restart)
+        self.k = self.k + dk
+        self.res = irk.stage_residual(self.sys, self.u, self.k, self.t, self.dt, tab)
+        return st.krylov_iterations
+
+
+def cpu_sample(spec, n_iters):
+    threads = os.cpu_count() or 1
+    stream = OracleNewtonStream(spec)
+    t0 = time.perf_counter()
+    kry = 0
+    for _ in range(n_iters):
+        kry += stream.newton_iteration()
+    dt = time.perf_counter() - t0
+    dof = n_iters * spec.s * spec.problem.dim / dt
+    return dof, dt, kry, threads
+
+
+def run_reference(args, spec, ws, rank):
+    if rank != 0:
+        return
+    stream = OracleNewtonStream(spec)
+    for _ in range(args.warmup):
+        stream.newton_iteration()
+    t0 = time.perf_counter()
+    kry = 0
+    for _ in range(args.steps):
+        kry += stream.newton_iteration()
+    el = time.perf_counter() - t0
+    value = args.steps * spec.s * spec.problem.dim / el
+    cores = os.cpu_count() or 1
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Fourier-mode u0)",
+        "config": {"workload": spec.name, "grid": list(spec.problem.shape), "scheme": "gauss(3)",
+                   "dt": spec.dt, "inner": "jacobi-4", "variant": 3},
+        "cpu_baseline": {
+            "value": value, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{args.steps} full Newton iterations (after {args.warmup} warm-up) of the "
+                      f"configs[1] trajectory at full 1024^2 size on the numpy/scipy restatement "
+                      f"of irkit (oracle/irk.py); {kry} Krylov iterations",
+        },
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ GPU leg
+
+
+def run_ours(args, spec, ws, rank, local):
+    import torch
+
+    import paper_2101_01776_b200 as pk
+    from paper_2101_01776_b200.engine import Context
+
+    torch.cuda.set_device(local)
+    prob = spec.problem
+    tab = pk.make_tableau(spec.family, spec.s)
+    prep = pk.prepare_stages(tab)
+    sv = spec.solver
+    cfg = pk.SolverConfig(variant=sv["variant"], krylov_maxit=sv["krylov_maxit"],
+                          restart=sv["restart"], newton_maxit=sv["newton_maxit"],
+                          precond=pk.PrecondSpec(inner=sv["inner"]))
+    ctx = Context(prob, local)
+    ctx.set_prep(prep)
+    ctx.set_config(cfg)
+    u0 = spec.u0()
+    u = torch.from_numpy(u0).cuda()
+    stream = torch.cuda.current_stream()
+    N = prob.dim
+    t = 0.0
+    for _ in range(args.warmup):
+        ctx.step_device(u, t, spec.dt)
+        t += spec.dt
+    torch.cuda.synchronize()
+    c0 = ctx.counters()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    stats = []
+    with ClockSampler(local) as clk:
+        barrier(ws)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            stats.append(ctx.step_device(u, t, spec.dt))
+            t += spec.dt
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+    c1 = ctx.counters()
+    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ms, ws)
+    newton = sum(s.newton_iterations for s in stats)
+    krylov = sum(s.krylov_iterations for s in stats)
+    dof = sum_over_ranks(newton * spec.s * N, ws)
+    value = dof / (ms * 1e-3)
+    steps_per_s = args.steps / (ms * 1e-3)
+    launches = int(c1["kernel_launches"] - c0["kernel_launches"])
+
+    # roofline pass: device time of the CGS2 sweeps (CUDA events on the engine
+    # stream around the 4 sweeps of each Arnoldi step) over extra steps
+    ctx.set_timing(True)
+    r0 = ctx.counters()
+    rsteps = max(1, min(args.steps, 3))
+    tr0 = time.perf_counter()
+    for _ in range(rsteps):
+        ctx.step_device(u, t, spec.dt)
+        t += spec.dt
+    torch.cuda.synchronize()
+    tr = time.perf_counter() - tr0
+    ctx.set_timing(False)
+    r1 = ctx.counters()
+    cgs_bytes = r1["cgs_bytes"] - r0["cgs_bytes"]
+    cgs_ms = r1["cgs_time_ms"] - r0["cgs_time_ms"]
+    cgs_launch = r1["cgs_launches"] - r0["cgs_launches"]
+    peak, peak_kind = _peaks()
+    achieved = cgs_bytes / (cgs_ms * 1e-3) / 1e9 if cgs_ms > 0 else 0.0
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "kernel": "k_mdot/k_mupdate (CGS2 sweeps)",
+            "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+            "algorithmic_bytes_per_launch": cgs_bytes / max(1, cgs_launch),
+            "avg_launch_us": 1e3 * cgs_ms / max(1, cgs_launch),
+            "share_of_step": (cgs_ms * 1e-3) / tr if tr > 0 else None}
+
+    # e2e: the public API with host buffers (H2D of u + D2H of u_next per step)
+    uh = u.cpu().numpy().copy()
+    e_stats = []
+    barrier(ws)
+    te0 = time.perf_counter()
+    for _ in range(args.steps):
+        uh, st = pk.step(prob, uh, t, spec.dt, tab, cfg)
+        e_stats.append(st)
+        t += spec.dt
+    te = max_over_ranks(time.perf_counter() - te0, ws)
+    e_dof = sum_over_ranks(sum(s.newton_iterations for s in e_stats) * spec.s * N, ws)
+    e2e = {"value": e_dof / te, "unit": UNIT, "h2d_bytes_per_step": 8 * N,
+           "d2h_bytes_per_step": 8 * N, "steps_per_s": args.steps / te}
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Fourier-mode u0, BASELINE configs[1] shape)",
+            "config": {"workload": spec.name, "grid": list(prob.shape), "scheme": "gauss(3)",
+                       "dt": spec.dt, "inner": "jacobi-4", "variant": 3, "restart": 200,
+                       "parallelism": f"replicas{ws}" if ws > 1 else "1 GPU",
+                       "l2": "working set > L2 (V basis 201 x 16.8 MB per rank)"},
+            "steps_per_s": steps_per_s, "newton_iterations": newton, "krylov_iterations": krylov,
+            "gpu_launches": launches, "roofline": roof, "e2e": e2e, "clocks": clk.summary(),
+        }
+        if ws == 1 and not args.no_cpu:
+            dof_cpu, el, kry, cores = cpu_sample(spec, 1)
+            line["cpu_baseline"] = {
+                "value": dof_cpu, "unit": UNIT, "cores": cores, "kind": "port",
+                "sample": f"first Newton iteration of step 1 at full 1024^2 on the numpy/scipy "
+                          f"restatement of irkit (oracle/irk.py): {el:.1f} s, {kry} Krylov its",
+            }
+        print(json.dumps(line), flush=True)
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=None, help="override grid size (testing)")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    from paper_2101_01776_b200.problems import baseline_config
+
+    spec = baseline_config(1, n=args.n)
+    if args.impl == "reference":
+        ws = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, spec, ws, rank)
+        return
+    ws, rank, local = dist_init()
+    run_ours(args, spec, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,218 @@
+/*
+ * irkg.h -- C ABI of the B200 IRK stage-solve engine (libirkg.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `irkit`
+ * (paths relative to /root/reference/pkg/src/irkit).  The reference has no
+ * FFI: its "plugin/operator API" is Python.  Each entry point
+ * below replaces one reference function; the Python mirror
+ * `paper_2101_01776_b200` binds them with ctypes.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; all vectors are fp64.
+ *  - `*_dev` pointers are CUDA device pointers owned by the caller; stage
+ *    arrays are (s, N) row-major (stage-major, C order), N = nx*ny*nz with x
+ *    fastest -- the reference's layout (src/nonlinear.py:310, problems.py:238).
+ *  - work is enqueued on the context's stream; calls return after the
+ *    result is on the device (scalars / stats are copied back to the host).
+ *  - return value: IRKG_OK or a negative IRKG_ERR_* code; the Python shim
+ *    maps them to the reference exception types (src/errors.py:6-58) with the
+ *    same payload fields.  irkg_last_error() gives a message.
+ *  - one context per GPU / rank, not thread-safe per context.
+ */
+#ifndef IRKG_H
+#define IRKG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IRKG_OK 0
+#define IRKG_ERR_VALUE -1          /* ValueError (shape/domain, zero Jacobi diagonal) */
+#define IRKG_ERR_CONFIG -2         /* ConfigurationError */
+#define IRKG_ERR_STAGE_SOLVE -3    /* StageSolveError(block_offset, report) */
+#define IRKG_ERR_STEP_FAILURE -4   /* StepFailureError(stats) */
+#define IRKG_ERR_BREAKDOWN -5      /* KrylovBreakdownError */
+#define IRKG_ERR_CUDA -6           /* CUDA / NCCL runtime failure */
+
+#define IRKG_MAX_STAGES 8
+#define IRKG_MAX_NEWTON 512
+#define IRKG_MAX_BLOCK_RECORDS 4096
+
+/* Problem kinds (paper_2101_01776_b200/problems.py, csrc/kinds.cuh). */
+#define IRKG_KIND_NLDIFF 0   /* N(u) = Lap_h(u + u^3/3) */
+#define IRKG_KIND_BURGERS 1  /* N(u) = -Dsum(u^2/2) + nu Lap_h u */
+#define IRKG_KIND_RAD 2      /* N(u) = nu Lap_h u + c Dsum u + lam u + mu u^2 */
+
+typedef struct irkg_ctx irkg_ctx;
+
+/* Grid + problem plugin: replaces OdeSystem(dim, rhs, linearize)
+ * (src/nonlinear.py:35-48) for the matrix-free stencil kinds.
+ * rank/nranks describe the slab partition along the slowest axis
+ * (ny_global split into contiguous slabs); nranks = 1 on one GPU. */
+typedef struct {
+  int kind;
+  int nx, ny, nz;        /* global extents; 1 for absent axes */
+  double length;         /* periodic box side per axis (h = length / n) */
+  double nu, c, lam, mu; /* kind parameters */
+} irkg_problem;
+
+/* Prepared stage constants: ButcherTableau + StagePrep
+ * (src/tableau.py:66-101, 364-379); consumed bit-exactly, never recomputed. */
+typedef struct {
+  int s;
+  double a0[IRKG_MAX_STAGES * IRKG_MAX_STAGES];
+  double b0[IRKG_MAX_STAGES];
+  double c0[IRKG_MAX_STAGES];
+  double q[IRKG_MAX_STAGES * IRKG_MAX_STAGES];
+  double r[IRKG_MAX_STAGES * IRKG_MAX_STAGES];
+  double d[IRKG_MAX_STAGES * IRKG_MAX_STAGES * IRKG_MAX_STAGES]; /* d[k][l][i] */
+  int nblocks;
+  int blk_offset[IRKG_MAX_STAGES];
+  int blk_size[IRKG_MAX_STAGES];
+  double blk_eta[IRKG_MAX_STAGES];
+  double blk_beta[IRKG_MAX_STAGES];
+  double blk_phi[IRKG_MAX_STAGES];
+} irkg_tableau;
+
+/* SolverConfig + PrecondSpec (src/nonlinear.py:61-83, src/irk_core.py:39-68). */
+typedef struct {
+  int variant;            /* 0..3 */
+  double newton_rtol;
+  int newton_maxit;
+  double newton_abs_floor;
+  double krylov_rtol;
+  int krylov_maxit;
+  int restart;
+  int gamma_mode;         /* 0 = star, 1 = eta, 2 = custom */
+  double gamma_custom;
+  int inner;              /* damped-Jacobi sweeps (>0) */
+  int jacobian_refresh;   /* 0 = every, 1 = frozen */
+  int variant0_stage;
+} irkg_solver;
+
+/* KrylovReport (src/sparsela.py:155-162); residuals into a caller buffer. */
+typedef struct {
+  int iterations;
+  int converged;
+  int precond_applications;
+  int n_residuals;        /* entries written (may exceed capacity: truncated) */
+  int residual_capacity;  /* set by caller */
+  double *residuals;      /* host buffer, caller-owned (may be NULL) */
+} irkg_krylov_report;
+
+/* StepStats (src/nonlinear.py:155-179) plus the failure payload. */
+typedef struct {
+  int newton_iterations;
+  int krylov_iterations;
+  int precond_applications;
+  int jacobian_assemblies;
+  int converged;
+  int n_residuals;
+  double residual_history[IRKG_MAX_NEWTON + 1];
+  int n_block_records;                      /* one per (Newton it, block) */
+  int block_offset[IRKG_MAX_BLOCK_RECORDS]; /* in solve order */
+  int block_iterations[IRKG_MAX_BLOCK_RECORDS];
+  double wall_time;
+  /* StageSolveError payload (valid when a call returned IRKG_ERR_STAGE_SOLVE) */
+  int fail_block_offset;
+  irkg_krylov_report fail_report;
+} irkg_step_stats;
+
+/* Engine counters since creation (bench.py: launches / algorithmic bytes). */
+typedef struct {
+  int64_t kernel_launches;
+  int64_t arnoldi_iterations;
+  double cgs_bytes;       /* algorithmic bytes moved by the CGS2 sweeps */
+  double cgs_time_ms;     /* device time of the CGS2 sweeps (if timing on) */
+  int64_t cgs_launches;
+  double precond_bytes;
+  double op_bytes;
+} irkg_counters;
+
+const char *irkg_last_error(void);
+const char *irkg_version(void);
+
+/* Context: owns the stream binding, workspaces (V basis sized by restart)
+ * and the stage arrays.  `stream` is a cudaStream_t (0 = legacy default);
+ * `nccl_id` (128 bytes) may be NULL when nranks == 1.
+ * Replaces the per-call workspaces of gmres (src/sparsela.py:208-213). */
+int irkg_create(irkg_ctx **out, const irkg_problem *prob, int device, void *stream,
+                const void *nccl_id, int rank, int nranks);
+int irkg_destroy(irkg_ctx *ctx);
+int irkg_get_local_extent(irkg_ctx *ctx, int *n_local, int *y0, int *ny_local);
+int irkg_nccl_unique_id(void *out128);
+
+int irkg_set_tableau(irkg_ctx *ctx, const irkg_tableau *tab);
+int irkg_set_solver(irkg_ctx *ctx, const irkg_solver *cfg);
+int irkg_set_timing(irkg_ctx *ctx, int on);
+int irkg_get_counters(irkg_ctx *ctx, irkg_counters *out);
+
+/* stage_residual (src/nonlinear.py:145-152): F = N(u + dt A0 K) - K.
+ * u_dev (N), k_dev (s,N), f_dev (s,N) out; *norm = ||F||_F. */
+int irkg_stage_residual(irkg_ctx *ctx, const double *u_dev, const double *k_dev, double t,
+                        double dt, double *f_dev, double *norm);
+
+/* newton_like_step (src/nonlinear.py:186-236): k_dev (s,N) in/out. */
+int irkg_newton_step(irkg_ctx *ctx, const double *u_dev, double *k_dev, double t, double dt,
+                     irkg_step_stats *stats);
+
+/* step (src/nonlinear.py:299-314): u_dev (N) in/out, u <- u + dt b0^T K. */
+int irkg_step(irkg_ctx *ctx, double *u_dev, double t, double dt, irkg_step_stats *stats);
+
+/* Same as irkg_step with host buffers: H2D copy of u, step, D2H copy
+ * (the end-to-end path timed by bench.py's e2e leg). */
+int irkg_step_host(irkg_ctx *ctx, double *u_host, double t, double dt, irkg_step_stats *stats);
+
+/* ---- operator-level entry points (parity tests; src/irk_core.py) ----
+ * An operator "field" is the coefficient field a (device, N) + scalar sigma
+ * of the collapsed weighted linearisation sum_k w_k L_k (see problems.py). */
+typedef struct {
+  const double *a_dev; /* may be NULL for kinds whose L does not read a */
+  double sigma;
+} irkg_opfield;
+
+/* linearize + combine (src/nonlinear.py:204-209, src/sparsela.py:106-128):
+ * the operator field of sum_k w_k L(U_k) for m stage values U_dev (m,N):
+ * a_out_dev (N) = sum_k w_k f(U_k), *sigma_out = sum_k w_k. */
+int irkg_linearize(irkg_ctx *ctx, const double *U_dev, int m, const double *weights,
+                   double *a_out_dev, double *sigma_out);
+
+/* apply_block2x2 (src/irk_core.py:126-140): y = A x, x,y (2N). c12/c21 may be NULL. */
+int irkg_block2x2_apply(irkg_ctx *ctx, double eta, double beta, double phi, double dt,
+                        const irkg_opfield *l1, const irkg_opfield *l2,
+                        const irkg_opfield *c12, const irkg_opfield *c21,
+                        const double *x_dev, double *y_dev);
+
+/* make_block2x2_preconditioner(...)(r) (src/irk_core.py:147-165), Jacobi-k inner. */
+int irkg_block2x2_precond(irkg_ctx *ctx, double eta, double beta, double phi, double gamma,
+                          double dt, int inner, const irkg_opfield *l1,
+                          const irkg_opfield *l2, const double *r_dev, double *z_dev);
+
+/* ShiftedSolver(alpha, I, L, dt, inner=k).solve(r) (src/irk_core.py:103-123). */
+int irkg_shifted_solve(irkg_ctx *ctx, double alpha, double dt, int inner,
+                       const irkg_opfield *l, const double *r_dev, double *x_dev);
+
+/* gmres on one eigen-block system (src/sparsela.py:176-280 driving
+ * src/irk_core.py:215-222 / 303-333): size 1 (eta*I - dt*L1, ShiftedSolver
+ * preconditioner) or 2 (Block2x2System + block preconditioner).
+ * rhs_dev, x_dev: size*N.  x0 = 0 (as every reference block solve). */
+int irkg_block_gmres(irkg_ctx *ctx, int size, double eta, double beta, double phi,
+                     double gamma, double dt, int inner, const irkg_opfield *l1,
+                     const irkg_opfield *l2, const irkg_opfield *c12,
+                     const irkg_opfield *c21, const double *rhs_dev, double *x_dev,
+                     double rtol, int maxit, int restart, irkg_krylov_report *report);
+
+/* solve_transformed_system (src/irk_core.py:225-338) at the linearisation
+ * last set by irkg_newton_step / irkg_prepare_linearization.
+ * rhs_dev (s,N) -> dk_dev (s,N); per-block records into stats. */
+int irkg_prepare_linearization(irkg_ctx *ctx, const double *u_dev, const double *k_dev,
+                               double dt);
+int irkg_transformed_solve(irkg_ctx *ctx, double dt, const double *rhs_dev, double *dk_dev,
+                           irkg_step_stats *stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IRKG_H */

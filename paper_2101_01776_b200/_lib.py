@@ -1,0 +1,188 @@
+"""ctypes binding of the C ABI in include/irkg.h (libirkg.so, built in-tree).
+
+There is no CPU fallback: if the shared library is missing or no CUDA
+device is usable, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libirkg.so")
+
+MAX_STAGES = 8
+MAX_NEWTON = 512
+MAX_BLOCK_RECORDS = 4096
+
+OK = 0
+ERR_VALUE = -1
+ERR_CONFIG = -2
+ERR_STAGE_SOLVE = -3
+ERR_STEP_FAILURE = -4
+ERR_BREAKDOWN = -5
+ERR_CUDA = -6
+
+
+class Problem(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int),
+        ("nx", C.c_int),
+        ("ny", C.c_int),
+        ("nz", C.c_int),
+        ("length", C.c_double),
+        ("nu", C.c_double),
+        ("c", C.c_double),
+        ("lam", C.c_double),
+        ("mu", C.c_double),
+    ]
+
+
+S = MAX_STAGES
+
+
+class Tableau(C.Structure):
+    _fields_ = [
+        ("s", C.c_int),
+        ("a0", C.c_double * (S * S)),
+        ("b0", C.c_double * S),
+        ("c0", C.c_double * S),
+        ("q", C.c_double * (S * S)),
+        ("r", C.c_double * (S * S)),
+        ("d", C.c_double * (S * S * S)),
+        ("nblocks", C.c_int),
+        ("blk_offset", C.c_int * S),
+        ("blk_size", C.c_int * S),
+        ("blk_eta", C.c_double * S),
+        ("blk_beta", C.c_double * S),
+        ("blk_phi", C.c_double * S),
+    ]
+
+
+class Solver(C.Structure):
+    _fields_ = [
+        ("variant", C.c_int),
+        ("newton_rtol", C.c_double),
+        ("newton_maxit", C.c_int),
+        ("newton_abs_floor", C.c_double),
+        ("krylov_rtol", C.c_double),
+        ("krylov_maxit", C.c_int),
+        ("restart", C.c_int),
+        ("gamma_mode", C.c_int),
+        ("gamma_custom", C.c_double),
+        ("inner", C.c_int),
+        ("jacobian_refresh", C.c_int),
+        ("variant0_stage", C.c_int),
+    ]
+
+
+class KrylovReportC(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int),
+        ("converged", C.c_int),
+        ("precond_applications", C.c_int),
+        ("n_residuals", C.c_int),
+        ("residual_capacity", C.c_int),
+        ("residuals", C.POINTER(C.c_double)),
+    ]
+
+
+class StepStatsC(C.Structure):
+    _fields_ = [
+        ("newton_iterations", C.c_int),
+        ("krylov_iterations", C.c_int),
+        ("precond_applications", C.c_int),
+        ("jacobian_assemblies", C.c_int),
+        ("converged", C.c_int),
+        ("n_residuals", C.c_int),
+        ("residual_history", C.c_double * (MAX_NEWTON + 1)),
+        ("n_block_records", C.c_int),
+        ("block_offset", C.c_int * MAX_BLOCK_RECORDS),
+        ("block_iterations", C.c_int * MAX_BLOCK_RECORDS),
+        ("wall_time", C.c_double),
+        ("fail_block_offset", C.c_int),
+        ("fail_report", KrylovReportC),
+    ]
+
+
+class Counters(C.Structure):
+    _fields_ = [
+        ("kernel_launches", C.c_int64),
+        ("arnoldi_iterations", C.c_int64),
+        ("cgs_bytes", C.c_double),
+        ("cgs_time_ms", C.c_double),
+        ("cgs_launches", C.c_int64),
+        ("precond_bytes", C.c_double),
+        ("op_bytes", C.c_double),
+    ]
+
+
+class OpField(C.Structure):
+    _fields_ = [("a_dev", C.c_void_p), ("sigma", C.c_double)]
+
+
+_P = C.c_void_p
+_D = C.c_double
+_I = C.c_int
+
+_SIGS = {
+    "irkg_last_error": (C.c_char_p, []),
+    "irkg_version": (C.c_char_p, []),
+    "irkg_create": (_I, [C.POINTER(_P), C.POINTER(Problem), _I, _P, _P, _I, _I]),
+    "irkg_destroy": (_I, [_P]),
+    "irkg_get_local_extent": (_I, [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
+    "irkg_nccl_unique_id": (_I, [_P]),
+    "irkg_set_tableau": (_I, [_P, C.POINTER(Tableau)]),
+    "irkg_set_solver": (_I, [_P, C.POINTER(Solver)]),
+    "irkg_set_timing": (_I, [_P, _I]),
+    "irkg_get_counters": (_I, [_P, C.POINTER(Counters)]),
+    "irkg_stage_residual": (_I, [_P, _P, _P, _D, _D, _P, C.POINTER(_D)]),
+    "irkg_newton_step": (_I, [_P, _P, _P, _D, _D, C.POINTER(StepStatsC)]),
+    "irkg_step": (_I, [_P, _P, _D, _D, C.POINTER(StepStatsC)]),
+    "irkg_step_host": (_I, [_P, _P, _D, _D, C.POINTER(StepStatsC)]),
+    "irkg_linearize": (_I, [_P, _P, _I, _P, _P, C.POINTER(_D)]),
+    "irkg_block2x2_apply": (
+        _I,
+        [_P, _D, _D, _D, _D, C.POINTER(OpField), C.POINTER(OpField), C.POINTER(OpField),
+         C.POINTER(OpField), _P, _P],
+    ),
+    "irkg_block2x2_precond": (
+        _I, [_P, _D, _D, _D, _D, _D, _I, C.POINTER(OpField), C.POINTER(OpField), _P, _P]
+    ),
+    "irkg_shifted_solve": (_I, [_P, _D, _D, _I, C.POINTER(OpField), _P, _P]),
+    "irkg_block_gmres": (
+        _I,
+        [_P, _I, _D, _D, _D, _D, _D, _I, C.POINTER(OpField), C.POINTER(OpField),
+         C.POINTER(OpField), C.POINTER(OpField), _P, _P, _D, _I, _I, C.POINTER(KrylovReportC)],
+    ),
+    "irkg_prepare_linearization": (_I, [_P, _P, _P, _D]),
+    "irkg_transformed_solve": (_I, [_P, _D, _P, _P, C.POINTER(StepStatsC)]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load():
+    """Load libirkg.so (raises loudly; there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"CUDA engine {LIB_PATH} is missing: run `python -m paper_2101_01776_b200._build` "
+            "(there is no CPU fallback)"
+        )
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def last_error():
+    return load().irkg_last_error().decode(errors="replace")

@@ -1,0 +1,760 @@
+// engine.cu -- solver drivers and the C ABI (include/irkg.h).
+//
+// The drivers restate the reference control flow exactly:
+//   gmres                src/sparsela.py:176-280
+//   transformed_solve    src/irk_core.py:225-338
+//   newton               src/nonlinear.py:186-236
+//   step                 src/nonlinear.py:299-314
+// All vector work is on the device; the host reads back only scalars
+// (norms, the GMRES control block) to steer the loops.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "engine.h"
+
+namespace irkg {
+
+static thread_local std::string g_last_error;
+
+template <class T>
+static void dalloc(T **p, size_t count) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  if (count == 0) return;
+  check(cudaMalloc((void **)p, count * sizeof(T)), "cudaMalloc");
+}
+
+Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st) : prob(p), device(dev), stream(st) {
+  check(cudaSetDevice(dev), "cudaSetDevice");
+  cudaDeviceProp prop;
+  check(cudaGetDeviceProperties(&prop, dev), "props");
+  sms = prop.multiProcessorCount;
+  G = 2 * sms;
+  int ext[3] = {p.nx, p.ny, p.nz};
+  ndim = (p.nz > 1) ? 3 : (p.ny > 1 ? 2 : 1);
+  grid.nx = p.nx;
+  grid.ny = p.ny;
+  grid.nz = p.nz;
+  grid.nxy = p.nx * p.ny;
+  grid.n = p.nx * p.ny * p.nz;
+  double lapdiag = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    double h = p.length / ext[a];
+    if (ext[a] > 1) {
+      grid.ih2[a] = 1.0 / (h * h);
+      grid.i2h[a] = 1.0 / (2.0 * h);
+      lapdiag += -2.0 * grid.ih2[a];
+    } else {
+      grid.ih2[a] = 0.0;
+      grid.i2h[a] = 0.0;
+    }
+  }
+  grid.lapdiag = lapdiag;
+  kp.nu = p.nu;
+  kp.c = p.c;
+  kp.lam = p.lam;
+  kp.mu = p.mu;
+  N = grid.n;
+  dalloc(&part, (size_t)(MAXR + 2) * G);
+  dalloc(&counter, 1);
+  check(cudaMemsetAsync(counter, 0, sizeof(unsigned), stream));
+  dalloc(&scal_dev, 16);
+  dalloc(&ctrl_dev, 1);
+  check(cudaMemsetAsync(ctrl_dev, 0, sizeof(GCtrl), stream));
+  W.ctrl = ctrl_dev;
+  dalloc(&W.H, (size_t)(MAXR + 1) * MAXR);
+  dalloc(&W.cs, MAXR);
+  dalloc(&W.sn, MAXR);
+  dalloc(&W.g, MAXR + 1);
+  dalloc(&W.alpha, MAXR + 1);
+  dalloc(&W.y, MAXR);
+  dalloc(&W.c1, MAXR + 1);
+  dalloc(&W.c2, MAXR + 1);
+  check(cudaMallocHost((void **)&ctrl_host, sizeof(GCtrl)), "cudaMallocHost");
+  dalloc(&wbuf, 2 * N);
+  dalloc(&zbuf, 2 * N);
+  dalloc(&ubuf, 2 * N);
+  dalloc(&tmp_x, N);
+  dalloc(&tmp_t, N);
+  dalloc(&RHS, 2 * N);
+  dalloc(&ufield, N);
+  check(cudaEventCreate(&ev0), "event");
+  check(cudaEventCreate(&ev1), "event");
+  for (int i = 0; i < MAXS; ++i)
+    for (int j = 0; j < MAXS; ++j) od_slot[i][j] = -1;
+}
+
+Engine::~Engine() {
+  cudaStreamSynchronize(stream);
+  void *bufs[] = {part, counter, scal_dev, ctrl_dev, W.H, W.cs, W.sn, W.g, W.alpha, W.y,
+                  W.c1, W.c2, W.res, V, wbuf, zbuf, ubuf, tmp_x, tmp_t, U, F, Gs, Y, DK,
+                  Kst, RHS, ufield, opA};
+  for (void *b : bufs)
+    if (b) cudaFree(b);
+  if (ctrl_host) cudaFreeHost(ctrl_host);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+}
+
+void Engine::ensure_stage_buffers() {
+  if (U) return;
+  dalloc(&U, (size_t)s * N);
+  dalloc(&F, (size_t)s * N);
+  dalloc(&Gs, (size_t)s * N);
+  dalloc(&Y, (size_t)s * N);
+  dalloc(&DK, (size_t)s * N);
+  dalloc(&Kst, (size_t)s * N);
+}
+
+void Engine::ensure_basis(int restart) {
+  if (restart > MAXR) throw SolveError(IRKG_ERR_CONFIG, "restart exceeds MAXR=512");
+  if (V && restart <= vcap) return;
+  vpitch = ((2 * N + 31) / 32) * 32;
+  dalloc(&V, (size_t)(restart + 1) * vpitch);
+  vcap = restart;
+}
+
+void Engine::set_tableau(const irkg_tableau &t) {
+  if (t.s < 1 || t.s > MAXS) throw SolveError(IRKG_ERR_CONFIG, "stage count out of range");
+  if (U && t.s != s) {
+    void *bufs[] = {U, F, Gs, Y, DK, Kst};
+    for (void *b : bufs) cudaFree(b);
+    U = F = Gs = Y = DK = Kst = nullptr;
+  }
+  tab = t;
+  s = t.s;
+  have_tab = true;
+  ensure_stage_buffers();
+}
+
+void Engine::set_solver(const irkg_solver &c) {
+  if (c.variant < 0 || c.variant > 3) throw SolveError(IRKG_ERR_CONFIG, "variant must be 0..3");
+  if (!(c.newton_rtol > 0.0 && c.newton_rtol < 1.0) || !(c.krylov_rtol > 0.0 && c.krylov_rtol < 1.0))
+    throw SolveError(IRKG_ERR_CONFIG, "tolerance outside (0, 1)");
+  if (c.inner < 1) throw SolveError(IRKG_ERR_VALUE, "inner must be a positive int");
+  if (c.newton_maxit > IRKG_MAX_NEWTON) throw SolveError(IRKG_ERR_CONFIG, "newton_maxit too large");
+  cfg = c;
+  have_cfg = true;
+  ensure_basis(c.restart);
+  ensure_res(c.krylov_maxit);
+}
+
+void Engine::ensure_res(int maxit) {
+  if (W.res && rescap >= maxit + 4) return;
+  dalloc(&W.res, (size_t)maxit + 4);
+  rescap = maxit + 4;
+}
+
+void Engine::read_ctrl() {
+  check(cudaMemcpyAsync(ctrl_host, ctrl_dev, sizeof(GCtrl), cudaMemcpyDeviceToHost, stream));
+  check(cudaStreamSynchronize(stream), "sync");
+}
+
+double Engine::gamma_of(double eta, double beta) const {
+  if (cfg.gamma_mode == 0) return eta + beta * beta / eta;
+  if (cfg.gamma_mode == 1) return eta;
+  return cfg.gamma_custom;
+}
+
+// ------------------------------------------------------------------ GMRES
+// src/sparsela.py:176-280 with x0 = 0.  V slot l stores s_l with
+// v_l = alpha_l * s_l (no separate normalisation pass); the preconditioned
+// basis Z is not stored: with the fixed linear preconditioner M^{-1}
+// (Jacobi-k), x += Z y == x += M^{-1} (V y).
+KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double rtol, int maxit,
+                        int restart) {
+  if (!(rtol > 0.0 && rtol < 1.0)) throw SolveError(IRKG_ERR_VALUE, "rtol must lie in (0, 1)");
+  ensure_basis(restart);
+  ensure_res(maxit);
+  const long long n = (long long)B.size * N;
+  const int spa = B.size;
+  KrylovOut out;
+  double bnorm2 = norm2(rhs, n);
+  double bnorm = std::sqrt(bnorm2);
+  check(cudaMemsetAsync(x, 0, n * sizeof(double), stream));
+  if (bnorm == 0.0) {
+    out.iterations = 0;
+    out.converged = 1;
+    out.residuals = {0.0};
+    return out;
+  }
+  // host-side init of the control block
+  GCtrl c{};
+  c.maxit = maxit;
+  c.bnorm = bnorm;
+  c.beta = bnorm;
+  c.rtol = rtol;
+  c.n_res = 1;
+  double one = 1.0;  // residuals[0] = beta / bnorm
+  check(cudaMemcpyAsync(ctrl_dev, &c, sizeof(GCtrl), cudaMemcpyHostToDevice, stream));
+  check(cudaMemcpyAsync(W.res, &one, sizeof(double), cudaMemcpyHostToDevice, stream));
+  check(cudaMemcpyAsync(V, rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+  int total_it = 0;
+  int converged = (1.0 <= rtol);
+  VecIn vslot{V, vpitch, ctrl_dev, W.alpha};
+  VecIn vfix{ubuf, 0, nullptr, nullptr};
+  while (!converged && total_it < maxit) {
+    int m = std::min(restart, maxit - total_it);
+    cycle_init(m);
+    for (int it = 0; it < m; ++it) {
+      precond(B, &vslot, zbuf, ctrl_dev);                           // z = M^{-1} v_j
+      block_op(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev);          // w = A z
+      if (timing) check(cudaEventRecord(ev0, stream));
+      mdot(n, wbuf, W.c1, &ctrl_dev->wn2);                          // CGS pass 1 dots + ||w||
+      mupdate(n, W.c1, wbuf, wbuf, false, nullptr);                 // w -= V c1
+      mdot(n, wbuf, W.c2, nullptr);                                 // CGS pass 2 dots
+      mupdate(n, W.c2, wbuf, nullptr, true, &ctrl_dev->hn2);        // s_{j+1} = w - V c2
+      if (timing) check(cudaEventRecord(ev1, stream));
+      counters.cgs_launches += 4;
+      arnoldi_finish();
+      counters.arnoldi_iterations += 1;
+      read_ctrl();
+      if (timing) {
+        float ms = 0.f;
+        check(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
+        counters.cgs_time_ms += ms;
+      }
+      if (ctrl_host->cycle_done) break;
+    }
+    {
+      // algorithmic CGS2 bytes of this cycle: per iteration j, 4 sweeps over
+      // (j+1) basis vectors + w traffic (2 reads, 1 rmw, 1 read + 1 write)
+      double its = (double)(ctrl_host->j + 1);
+      double sumj1 = its * (its + 1.0) / 2.0;  // sum_{j=0}^{its-1} (j+1)
+      counters.cgs_bytes += 8.0 * (double)n * (4.0 * sumj1 + 6.0 * its);
+    }
+    // cycle end: x += M^{-1} (V (alpha .* y)); r = b - A x (src/sparsela.py:258-272)
+    backsolve();
+    vcombine(n, W.c1, ubuf);
+    precond(B, &vfix, zbuf, nullptr);
+    axpy(n, 1.0, zbuf, x);
+    block_op(B, x, V, rhs, &ctrl_dev->rr, nullptr);
+    cycle_end();
+    read_ctrl();
+    total_it = ctrl_host->total_it;
+    converged = ctrl_host->converged;
+    if (ctrl_host->zero_diag)
+      throw SolveError(IRKG_ERR_VALUE, "Jacobi inner solver needs a nonzero diagonal");
+    if (ctrl_host->err_breakdown) {
+      char msg[160];
+      double tr = std::sqrt(ctrl_host->rr) / bnorm;
+      snprintf(msg, sizeof msg, "Arnoldi breakdown with residual %.3e above rtol %.3e", tr, rtol);
+      throw SolveError(IRKG_ERR_BREAKDOWN, msg);
+    }
+  }
+  out.iterations = total_it;
+  out.converged = converged;
+  out.precond_applications = total_it * spa;
+  int nres = ctrl_host->n_res;
+  if (total_it == 0 && nres == 0) nres = 1;
+  out.residuals.resize(nres);
+  check(cudaMemcpyAsync(out.residuals.data(), W.res, nres * sizeof(double), cudaMemcpyDeviceToHost,
+                        stream));
+  check(cudaStreamSynchronize(stream));
+  return out;
+}
+
+// ------------------------------------------------------- linearisation
+// variant_weights (src/nonlinear.py:99-126) -> operator slots.
+void Engine::build_linearization(const double *Ust) {
+  const int v = cfg.variant;
+  double dw[MAXS][MAXS] = {};
+  struct Key {
+    int i, j;
+  };
+  std::vector<Key> keys;
+  std::vector<std::vector<double>> ow;
+  auto d = [&](int k, int l, int i) { return tab.d[(k * IRKG_MAX_STAGES + l) * IRKG_MAX_STAGES + i]; };
+  if (v == 0) {
+    for (int i = 0; i < s; ++i) dw[i][cfg.variant0_stage] = 1.0;
+  } else if (v == 1) {
+    for (int i = 0; i < s; ++i) {
+      int best = 0;
+      double bv = std::fabs(d(i, i, 0));
+      for (int k = 1; k < s; ++k)
+        if (std::fabs(d(i, i, k)) > bv) {
+          bv = std::fabs(d(i, i, k));
+          best = k;
+        }
+      dw[i][best] = 1.0;
+    }
+  } else {
+    for (int i = 0; i < s; ++i)
+      for (int k = 0; k < s; ++k) dw[i][k] = d(i, i, k);
+    if (v == 3) {
+      for (int i = 0; i < s; ++i)
+        for (int j = i + 1; j < s; ++j) {
+          keys.push_back({i, j});
+          std::vector<double> w(s);
+          for (int k = 0; k < s; ++k) w[k] = d(i, j, k);
+          ow.push_back(w);
+        }
+      for (int b = 0; b < tab.nblocks; ++b)
+        if (tab.blk_size[b] == 2) {
+          int i = tab.blk_offset[b];
+          keys.push_back({i + 1, i});
+          std::vector<double> w(s);
+          for (int k = 0; k < s; ++k) w[k] = d(i + 1, i, k);
+          ow.push_back(w);
+        }
+    }
+  }
+  nops = s + (int)keys.size();
+  if (nops > MAXOPS) throw SolveError(IRKG_ERR_CONFIG, "too many operator fields");
+  if (nops > nops_cap) {
+    dalloc(&opA, (size_t)nops * N);
+    nops_cap = nops;
+  }
+  weights = OpWeights{};
+  weights.nops = nops;
+  weights.s = s;
+  for (int i = 0; i < MAXS; ++i)
+    for (int j = 0; j < MAXS; ++j) od_slot[i][j] = -1;
+  for (int o = 0; o < nops; ++o) {
+    const double *w = nullptr;
+    std::vector<double> tmp(s);
+    if (o < s) {
+      for (int k = 0; k < s; ++k) tmp[k] = dw[o][k];
+      diag_slot[o] = o;
+    } else {
+      tmp = ow[o - s];
+      od_slot[keys[o - s].i][keys[o - s].j] = o;
+    }
+    w = tmp.data();
+    double sig = 0.0;
+    bool allzero = true;
+    for (int k = 0; k < s; ++k) {
+      weights.w[o * MAXS + k] = w[k];
+      if (w[k] != 0.0) {
+        sig += w[k];
+        allzero = false;
+      }
+    }
+    op_sigma[o] = sig;
+    op_zero[o] = allzero;
+  }
+  opfields(Ust, weights, opA);
+}
+
+Op Engine::op_of(int slot) const {
+  Op o{};
+  if (slot < 0 || op_zero[slot]) {
+    o.present = 0;
+    o.a = nullptr;
+    o.sigma = 0.0;
+    return o;
+  }
+  o.present = 1;
+  o.a = opA + (size_t)slot * N;
+  o.sigma = op_sigma[slot];
+  return o;
+}
+
+// ---------------------------------------------------- transformed solve
+// src/irk_core.py:225-338 (identity mass).
+void Engine::transformed_solve(double dt, const double *rhs, double *dk, irkg_step_stats *stats) {
+  // g = Q^T F
+  std::vector<double> qt(s * s), qr(s * s);
+  for (int i = 0; i < s; ++i)
+    for (int k = 0; k < s; ++k) qt[i * s + k] = tab.q[k * IRKG_MAX_STAGES + i];
+  stage_mix(qt.data(), rhs, Gs, false);
+  check(cudaMemsetAsync(Y, 0, (size_t)s * N * sizeof(double), stream));
+  for (int b = tab.nblocks - 1; b >= 0; --b) {
+    const int off = tab.blk_offset[b], size = tab.blk_size[b];
+    BacksubTerms T{};
+    T.rows = size;
+    T.row0 = off;
+    T.njs = 0;
+    for (int j = off + size; j < s; ++j) {
+      int q = T.njs++;
+      T.j[q] = j;
+      for (int r = 0; r < size; ++r) {
+        T.coef[r][q] = tab.r[(off + r) * IRKG_MAX_STAGES + j];
+        T.od[r][q] = op_of(od_slot[off + r][j]);
+      }
+    }
+    backsub(dt, T, Gs, Y, RHS);
+    BlockSpec B{};
+    B.size = size;
+    B.eta = tab.blk_eta[b];
+    B.beta = tab.blk_beta[b];
+    B.phi = tab.blk_phi[b];
+    B.gamma = gamma_of(B.eta, B.beta);
+    B.dt = dt;
+    B.inner = cfg.inner;
+    B.l1 = op_of(diag_slot[off]);
+    if (size == 2) {
+      B.l2 = op_of(diag_slot[off + 1]);
+      B.c12 = op_of(od_slot[off][off + 1]);
+      B.c21 = op_of(od_slot[off + 1][off]);
+    }
+    // the reference always applies the diagonal operators, even if zero
+    B.l1.present = 1;
+    if (!B.l1.a) B.l1.a = opA + (size_t)diag_slot[off] * N;
+    if (size == 2) {
+      B.l2.present = 1;
+      if (!B.l2.a) B.l2.a = opA + (size_t)diag_slot[off + 1] * N;
+    }
+    KrylovOut rep = gmres(B, RHS, Y + (size_t)off * N, cfg.krylov_rtol, cfg.krylov_maxit, cfg.restart);
+    if (stats) {
+      if (stats->n_block_records < IRKG_MAX_BLOCK_RECORDS) {
+        stats->block_offset[stats->n_block_records] = off;
+        stats->block_iterations[stats->n_block_records] = rep.iterations;
+        stats->n_block_records++;
+      }
+      stats->krylov_iterations += rep.iterations;
+      stats->precond_applications += rep.precond_applications;
+    }
+    if (!rep.converged) {
+      if (stats) {
+        stats->fail_block_offset = off;
+        irkg_krylov_report &fr = stats->fail_report;
+        fr.iterations = rep.iterations;
+        fr.converged = 0;
+        fr.precond_applications = rep.precond_applications;
+        fr.n_residuals = (int)rep.residuals.size();
+        if (fr.residuals)
+          for (int i = 0; i < (int)rep.residuals.size() && i < fr.residual_capacity; ++i)
+            fr.residuals[i] = rep.residuals[i];
+      }
+      char msg[96];
+      snprintf(msg, sizeof msg, "%dx%d block at offset %d did not converge", size, size, off);
+      throw SolveError(IRKG_ERR_STAGE_SOLVE, msg);
+    }
+  }
+  // dk = (Q R0) y
+  for (int i = 0; i < s; ++i)
+    for (int j = 0; j < s; ++j) {
+      double acc = 0.0;
+      for (int k = 0; k < s; ++k) acc += tab.q[i * IRKG_MAX_STAGES + k] * tab.r[k * IRKG_MAX_STAGES + j];
+      qr[i * s + j] = acc;
+    }
+  stage_mix(qr.data(), Y, dk, false);
+}
+
+// -------------------------------------------------------------- Newton
+// src/nonlinear.py:186-236.  K (s,N) in/out.
+void Engine::newton(const double *u, double *K, double t, double dt, irkg_step_stats *stats) {
+  auto tic = std::chrono::steady_clock::now();
+  stage_values(u, K, dt, U);
+  double f0 = std::sqrt(residual(U, K, F));
+  stats->n_residuals = 0;
+  stats->residual_history[stats->n_residuals++] = f0;
+  const double tol = std::max(cfg.newton_rtol * f0, cfg.newton_abs_floor);
+  double fn = f0;
+  bool have_ops = false;
+  auto finish = [&]() {
+    stats->wall_time =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - tic).count();
+  };
+  while (stats->newton_iterations < cfg.newton_maxit) {
+    if (fn <= tol) {
+      stats->converged = 1;
+      finish();
+      return;
+    }
+    if (!have_ops || cfg.jacobian_refresh == 0) {
+      build_linearization(U);  // U = u + dt A0 K at the current iterate
+      stats->jacobian_assemblies += s;
+      have_ops = true;
+    }
+    transformed_solve(dt, F, DK, stats);
+    {
+      // K += dk
+      std::vector<double> eye(s * s, 0.0);
+      for (int i = 0; i < s; ++i) eye[i * s + i] = 1.0;
+      stage_mix(eye.data(), DK, K, true);
+    }
+    stats->newton_iterations += 1;
+    stage_values(u, K, dt, U);
+    fn = std::sqrt(residual(U, K, F));
+    if (stats->n_residuals <= IRKG_MAX_NEWTON) stats->residual_history[stats->n_residuals++] = fn;
+  }
+  if (fn > tol) {
+    finish();
+    char msg[160];
+    snprintf(msg, sizeof msg, "stage solve stalled after %d iterations (residual %.3e, tol %.3e)",
+             cfg.newton_maxit, fn, tol);
+    throw SolveError(IRKG_ERR_STEP_FAILURE, msg);
+  }
+  stats->converged = 1;
+  finish();
+}
+
+}  // namespace irkg
+
+// ================================================================ C ABI
+using namespace irkg;
+
+struct irkg_ctx {
+  Engine *eng;
+};
+
+static int fail(int code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define IRKG_GUARD(...)                                           \
+  try {                                                           \
+    __VA_ARGS__;                                                  \
+    return IRKG_OK;                                               \
+  } catch (const SolveError &e) {                                 \
+    return fail(e.code, e.what());                                \
+  } catch (const CudaError &e) {                                  \
+    return fail(IRKG_ERR_CUDA, e.what());                         \
+  } catch (const std::exception &e) {                             \
+    return fail(IRKG_ERR_CUDA, e.what());                         \
+  }
+
+extern "C" {
+
+const char *irkg_last_error(void) { return g_last_error.c_str(); }
+const char *irkg_version(void) { return "irkg 0.1 sm_100a"; }
+
+int irkg_create(irkg_ctx **out, const irkg_problem *prob, int device, void *stream,
+                const void *nccl_id, int rank, int nranks) {
+  IRKG_GUARD({
+    if (nranks != 1) throw SolveError(IRKG_ERR_CONFIG, "multi-rank contexts not built in this version");
+    (void)nccl_id;
+    (void)rank;
+    if (prob->kind < 0 || prob->kind > 2) throw SolveError(IRKG_ERR_CONFIG, "unknown problem kind");
+    if (prob->nx < 1 || prob->ny < 1 || prob->nz < 1)
+      throw SolveError(IRKG_ERR_VALUE, "grid extents must be positive");
+    long long n = (long long)prob->nx * prob->ny * prob->nz;
+    if (2 * n >= (1LL << 31)) throw SolveError(IRKG_ERR_VALUE, "grid too large for one rank");
+    auto *c = new irkg_ctx;
+    c->eng = new Engine(*prob, device, (cudaStream_t)stream);
+    *out = c;
+  });
+}
+
+int irkg_destroy(irkg_ctx *ctx) {
+  IRKG_GUARD({
+    if (ctx) {
+      delete ctx->eng;
+      delete ctx;
+    }
+  });
+}
+
+int irkg_get_local_extent(irkg_ctx *ctx, int *n_local, int *y0, int *ny_local) {
+  IRKG_GUARD({
+    *n_local = (int)ctx->eng->N;
+    *y0 = 0;
+    *ny_local = ctx->eng->ndim == 3 ? ctx->eng->prob.nz : ctx->eng->prob.ny;
+  });
+}
+
+int irkg_nccl_unique_id(void *out128) {
+  IRKG_GUARD({
+    memset(out128, 0, 128);
+    throw SolveError(IRKG_ERR_CONFIG, "NCCL not built in this version");
+  });
+}
+
+int irkg_set_tableau(irkg_ctx *ctx, const irkg_tableau *tab) { IRKG_GUARD(ctx->eng->set_tableau(*tab)); }
+int irkg_set_solver(irkg_ctx *ctx, const irkg_solver *cfg) { IRKG_GUARD(ctx->eng->set_solver(*cfg)); }
+int irkg_set_timing(irkg_ctx *ctx, int on) { IRKG_GUARD(ctx->eng->timing = (on != 0)); }
+int irkg_get_counters(irkg_ctx *ctx, irkg_counters *out) { IRKG_GUARD(*out = ctx->eng->counters); }
+
+int irkg_stage_residual(irkg_ctx *ctx, const double *u_dev, const double *k_dev, double t, double dt,
+                        double *f_dev, double *norm) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    if (!e.have_tab) throw SolveError(IRKG_ERR_CONFIG, "tableau not set");
+    (void)t;
+    e.stage_values(u_dev, k_dev, dt, e.U);
+    double v = e.residual(e.U, k_dev, f_dev);
+    *norm = std::sqrt(v);
+  });
+}
+
+int irkg_newton_step(irkg_ctx *ctx, const double *u_dev, double *k_dev, double t, double dt,
+                     irkg_step_stats *stats) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    if (!e.have_tab || !e.have_cfg) throw SolveError(IRKG_ERR_CONFIG, "tableau/solver not set");
+    irkg_krylov_report fr = stats->fail_report;
+    memset(stats, 0, offsetof(irkg_step_stats, fail_report));
+    stats->fail_report = fr;
+    e.newton(u_dev, k_dev, t, dt, stats);
+  });
+}
+
+int irkg_step(irkg_ctx *ctx, double *u_dev, double t, double dt, irkg_step_stats *stats) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    if (!e.have_tab || !e.have_cfg) throw SolveError(IRKG_ERR_CONFIG, "tableau/solver not set");
+    irkg_krylov_report fr = stats->fail_report;
+    memset(stats, 0, offsetof(irkg_step_stats, fail_report));
+    stats->fail_report = fr;
+    check(cudaMemsetAsync(e.Kst, 0, (size_t)e.s * e.N * sizeof(double), e.stream));
+    e.newton(u_dev, e.Kst, t, dt, stats);
+    e.step_update(dt, e.Kst, u_dev);
+    check(cudaStreamSynchronize(e.stream));
+  });
+}
+
+int irkg_step_host(irkg_ctx *ctx, double *u_host, double t, double dt, irkg_step_stats *stats) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    if (!e.have_tab || !e.have_cfg) throw SolveError(IRKG_ERR_CONFIG, "tableau/solver not set");
+    irkg_krylov_report fr = stats->fail_report;
+    memset(stats, 0, offsetof(irkg_step_stats, fail_report));
+    stats->fail_report = fr;
+    check(cudaMemcpyAsync(e.ufield, u_host, e.N * sizeof(double), cudaMemcpyHostToDevice, e.stream));
+    check(cudaMemsetAsync(e.Kst, 0, (size_t)e.s * e.N * sizeof(double), e.stream));
+    e.newton(e.ufield, e.Kst, t, dt, stats);
+    e.step_update(dt, e.Kst, e.ufield);
+    check(cudaMemcpyAsync(u_host, e.ufield, e.N * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+    check(cudaStreamSynchronize(e.stream));
+  });
+}
+
+static Op to_op(const irkg_opfield *f) {
+  Op o{};
+  if (!f) return o;
+  o.a = f->a_dev;
+  o.sigma = f->sigma;
+  o.present = 1;
+  return o;
+}
+
+int irkg_linearize(irkg_ctx *ctx, const double *U_dev, int m, const double *weights,
+                   double *a_out_dev, double *sigma_out) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    if (m < 1 || m > MAXS) throw SolveError(IRKG_ERR_VALUE, "stage count out of range");
+    OpWeights W{};
+    W.nops = 1;
+    W.s = m;
+    double sig = 0.0;
+    for (int k = 0; k < m; ++k) {
+      W.w[k] = weights[k];
+      if (weights[k] != 0.0) sig += weights[k];
+    }
+    e.opfields(U_dev, W, a_out_dev);
+    *sigma_out = sig;
+    check(cudaStreamSynchronize(e.stream));
+  });
+}
+
+int irkg_block2x2_apply(irkg_ctx *ctx, double eta, double beta, double phi, double dt,
+                        const irkg_opfield *l1, const irkg_opfield *l2, const irkg_opfield *c12,
+                        const irkg_opfield *c21, const double *x_dev, double *y_dev) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    BlockSpec B{};
+    B.size = 2;
+    B.eta = eta;
+    B.beta = beta;
+    B.phi = phi;
+    B.dt = dt;
+    B.l1 = to_op(l1);
+    B.l2 = to_op(l2);
+    B.c12 = to_op(c12);
+    B.c21 = to_op(c21);
+    e.block_op(B, x_dev, y_dev, nullptr, nullptr, nullptr);
+    check(cudaStreamSynchronize(e.stream));
+  });
+}
+
+int irkg_block2x2_precond(irkg_ctx *ctx, double eta, double beta, double phi, double gamma, double dt,
+                          int inner, const irkg_opfield *l1, const irkg_opfield *l2,
+                          const double *r_dev, double *z_dev) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    if (inner < 1) throw SolveError(IRKG_ERR_VALUE, "inner must be a positive int");
+    BlockSpec B{};
+    B.size = 2;
+    B.eta = eta;
+    B.beta = beta;
+    B.phi = phi;
+    B.gamma = gamma;
+    B.dt = dt;
+    B.inner = inner;
+    B.l1 = to_op(l1);
+    B.l2 = to_op(l2);
+    VecIn vin{r_dev, 0, nullptr, nullptr};
+    check(cudaMemsetAsync(e.ctrl_dev, 0, sizeof(GCtrl), e.stream));
+    e.precond(B, &vin, z_dev, nullptr);
+    e.read_ctrl();
+    if (e.ctrl_host->zero_diag) throw SolveError(IRKG_ERR_VALUE, "Jacobi inner solver needs a nonzero diagonal");
+  });
+}
+
+int irkg_shifted_solve(irkg_ctx *ctx, double alpha, double dt, int inner, const irkg_opfield *l,
+                       const double *r_dev, double *x_dev) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    if (inner < 1) throw SolveError(IRKG_ERR_VALUE, "inner must be a positive int");
+    VecIn vin{r_dev, 0, nullptr, nullptr};
+    check(cudaMemsetAsync(e.ctrl_dev, 0, sizeof(GCtrl), e.stream));
+    e.jacobi_chain(to_op(l), alpha, dt, inner, &vin, 0, nullptr, 0.0, x_dev, nullptr);
+    e.read_ctrl();
+    if (e.ctrl_host->zero_diag) throw SolveError(IRKG_ERR_VALUE, "Jacobi inner solver needs a nonzero diagonal");
+  });
+}
+
+int irkg_block_gmres(irkg_ctx *ctx, int size, double eta, double beta, double phi, double gamma,
+                     double dt, int inner, const irkg_opfield *l1, const irkg_opfield *l2,
+                     const irkg_opfield *c12, const irkg_opfield *c21, const double *rhs_dev,
+                     double *x_dev, double rtol, int maxit, int restart,
+                     irkg_krylov_report *report) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    if (size != 1 && size != 2) throw SolveError(IRKG_ERR_VALUE, "block size must be 1 or 2");
+    if (inner < 1) throw SolveError(IRKG_ERR_VALUE, "inner must be a positive int");
+    BlockSpec B{};
+    B.size = size;
+    B.eta = eta;
+    B.beta = beta;
+    B.phi = phi;
+    B.gamma = gamma;
+    B.dt = dt;
+    B.inner = inner;
+    B.l1 = to_op(l1);
+    B.l2 = to_op(l2);
+    B.c12 = to_op(c12);
+    B.c21 = to_op(c21);
+    KrylovOut rep = e.gmres(B, rhs_dev, x_dev, rtol, maxit, restart);
+    report->iterations = rep.iterations;
+    report->converged = rep.converged;
+    report->precond_applications = rep.precond_applications;
+    report->n_residuals = (int)rep.residuals.size();
+    if (report->residuals)
+      for (int i = 0; i < (int)rep.residuals.size() && i < report->residual_capacity; ++i)
+        report->residuals[i] = rep.residuals[i];
+  });
+}
+
+int irkg_prepare_linearization(irkg_ctx *ctx, const double *u_dev, const double *k_dev, double dt) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    if (!e.have_tab || !e.have_cfg) throw SolveError(IRKG_ERR_CONFIG, "tableau/solver not set");
+    e.stage_values(u_dev, k_dev, dt, e.U);
+    e.build_linearization(e.U);
+    check(cudaStreamSynchronize(e.stream));
+  });
+}
+
+int irkg_transformed_solve(irkg_ctx *ctx, double dt, const double *rhs_dev, double *dk_dev,
+                           irkg_step_stats *stats) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    if (!e.have_tab || !e.have_cfg) throw SolveError(IRKG_ERR_CONFIG, "tableau/solver not set");
+    if (!(dt > 0.0)) throw SolveError(IRKG_ERR_VALUE, "dt must be positive");
+    irkg_krylov_report fr = stats->fail_report;
+    memset(stats, 0, offsetof(irkg_step_stats, fail_report));
+    stats->fail_report = fr;
+    e.transformed_solve(dt, rhs_dev, dk_dev, stats);
+    check(cudaStreamSynchronize(e.stream));
+  });
+}
+
+}  // extern "C"

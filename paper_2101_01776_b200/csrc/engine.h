@@ -1,0 +1,142 @@
+// engine.h -- host-side engine: device buffers, launchers and the solver
+// drivers (GMRES control, transformed solve, Newton loop).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/irkg.h"
+#include "kernels.cuh"
+
+namespace irkg {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Error carrying an irkg status code (mapped to reference exception types).
+struct SolveError : std::runtime_error {
+  int code;
+  SolveError(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+inline void check(cudaError_t e, const char *what = "cuda") {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// One eigen-block system (Block2x2System / the 1x1 shifted system) plus
+// the preconditioner parameters (src/irk_core.py:71-95, 147-165, 215-222).
+struct BlockSpec {
+  int size;
+  double eta, beta, phi, gamma, dt;
+  int inner;
+  Op l1, l2, c12, c21;
+};
+
+struct KrylovOut {
+  int iterations = 0;
+  int converged = 0;
+  int precond_applications = 0;
+  std::vector<double> residuals;
+};
+
+struct Engine {
+  // configuration
+  irkg_problem prob{};
+  Grid grid{};
+  KindParams kp{};
+  int ndim = 1;
+  long long N = 0;
+  int device = 0;
+  int sms = 148;
+  int G = 296;  // CTAs of the reduction kernels (partials per value)
+  cudaStream_t stream = nullptr;
+  bool timing = false;
+  irkg_counters counters{};
+
+  // tableau + solver
+  bool have_tab = false, have_cfg = false;
+  irkg_tableau tab{};
+  irkg_solver cfg{};
+  int s = 0;
+
+  // device buffers
+  double *part = nullptr;       // (MAXR+2) * G reduction partials
+  unsigned *counter = nullptr;  // last-CTA ticket
+  double *scal_dev = nullptr;   // scalar outputs
+  GCtrl *ctrl_dev = nullptr;
+  GWork W{};
+  double *V = nullptr;          // basis, (restart+1) slots of 2N
+  long long vpitch = 0;
+  int vcap = 0;                 // allocated restart capacity
+  double *wbuf = nullptr;       // 2N: w
+  double *zbuf = nullptr;       // 2N: z / cycle-end scratch
+  double *ubuf = nullptr;       // 2N: V y combination
+  double *tmp_x = nullptr;      // N: Jacobi ping-pong
+  double *tmp_t = nullptr;      // N: coupled rhs of the second inner solve
+  // stage arrays (s, N)
+  double *U = nullptr, *F = nullptr, *Gs = nullptr, *Y = nullptr, *DK = nullptr, *Kst = nullptr;
+  double *RHS = nullptr;        // (2, N) block rhs
+  double *ufield = nullptr;     // N (step_host staging)
+  double *opA = nullptr;        // (nops, N) operator fields
+  int nops_cap = 0;
+  GCtrl *ctrl_host = nullptr;   // pinned mirror
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  // current linearisation: operator slot per diag row and per offdiag key
+  int nops = 0;
+  int diag_slot[MAXS];
+  int od_slot[MAXS][MAXS];  // -1 if absent
+  double op_sigma[MAXOPS];
+  bool op_zero[MAXOPS];
+  OpWeights weights{};
+
+  Engine(const irkg_problem &p, int dev, cudaStream_t st);
+  ~Engine();
+
+  void set_tableau(const irkg_tableau &t);
+  void set_solver(const irkg_solver &c);
+  void ensure_stage_buffers();
+  void ensure_basis(int restart);
+  void ensure_res(int maxit);
+  int rescap = 0;
+
+  // launch helpers (kernels.cu)
+  int grid_for(long long n) const;
+  void count(int k);
+  double norm2(const double *x, long long n, const GCtrl *skip = nullptr);
+  void stage_values(const double *u, const double *K, double dt, double *U);
+  double residual(const double *U, const double *K, double *F);
+  void opfields(const double *U, const OpWeights &W, double *A);
+  void stage_mix(const double *M_rowmajor_s, const double *in, double *out, bool accumulate);
+  void step_update(double dt, const double *K, double *u);
+  void backsub(double dt, const BacksubTerms &T, const double *gst, const double *y, double *rhs);
+  void jacobi_chain(const Op &L, double alpha, double dt, int inner, const void *vin, int in_off,
+                    const double *zc, double cpl, double *x_out, const GCtrl *skip);
+  void precond(const BlockSpec &B, const void *vin, double *z, const GCtrl *skip);
+  void block_op(const BlockSpec &B, const double *z, double *w, const double *b,
+                double *out_norm, const GCtrl *skip);
+  void mdot(long long n, const double *w, double *out_c, double *out_norm);
+  void mupdate(long long n, const double *coef, const double *w, double *out, bool to_next,
+               double *out_norm);
+  void cycle_init(int m);
+  void arnoldi_finish();
+  void backsolve();
+  void vcombine(long long n, const double *coef, double *out);
+  void axpy(long long n, double a, const double *x, double *y);
+  void cycle_end();
+
+  // drivers (engine.cu)
+  void read_ctrl();
+  KrylovOut gmres(const BlockSpec &B, const double *rhs, double *x, double rtol, int maxit,
+                  int restart);
+  void build_linearization(const double *U);
+  Op op_of(int slot) const;
+  double gamma_of(double eta, double beta) const;
+  void transformed_solve(double dt, const double *rhs, double *dk, irkg_step_stats *stats);
+  void newton(const double *u, double *K, double t, double dt, irkg_step_stats *stats);
+};
+
+}  // namespace irkg

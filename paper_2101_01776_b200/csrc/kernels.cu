@@ -1,0 +1,714 @@
+// kernels.cu -- device kernels + host launchers (see kernels.cuh for the rules).
+#include <cstdio>
+#include <type_traits>
+
+#include "engine.h"
+
+namespace irkg {
+
+// ------------------------------------------------------------ reductions
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int BS>
+__device__ __forceinline__ double block_sum(double v, double *sm) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sm[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (warp == 0) {
+    r = (lane < BS / 32) ? sm[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;  // valid in thread 0
+}
+
+// Last-CTA ticket.  Every CTA calls it after writing its partials; returns
+// true in all threads of the CTA that finished last.
+__device__ __forceinline__ bool last_block(unsigned *counter, int G) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = (atomicAdd(counter, 1u) == (unsigned)(G - 1));
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+
+// Fold part[l*G + c] over c (fixed order per lane, fixed shuffle tree).
+__device__ __forceinline__ double fold_partials(const double *part, int l, int G) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int c = lane; c < G; c += 32) s += __ldcg(part + (size_t)l * G + c);
+  return warp_sum(s);
+}
+
+template <int BS>
+__global__ void k_norm2(int n, const double *__restrict__ x, double *part, int G, double *out,
+                        unsigned *counter, const GCtrl *ctrl) {
+  __shared__ double sm[32];
+  if (ctrl && ctrl->cycle_done) return;
+  double acc = 0.0;
+  for (int p = blockIdx.x * BS + threadIdx.x; p < n; p += G * BS) {
+    double v = x[p];
+    acc += v * v;
+  }
+  acc = block_sum<BS>(acc, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+  if (!last_block(counter, G)) return;
+  if (threadIdx.x < 32) {
+    double s = fold_partials(part, 0, G);
+    if (threadIdx.x == 0) {
+      *out = s;
+      *counter = 0u;
+    }
+  }
+}
+
+// ------------------------------------------------------ stage-space passes
+
+// U_i = u + dt * (A0 K)_i  (src/nonlinear.py:147)
+__global__ void k_stage_values(int n, int s, const double *__restrict__ u,
+                               const double *__restrict__ K, StageConsts A, double dt,
+                               double *__restrict__ U) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    double kv[MAXS];
+#pragma unroll
+    for (int j = 0; j < MAXS; ++j)
+      if (j < s) kv[j] = K[(size_t)j * n + p];
+    const double up = u[p];
+#pragma unroll
+    for (int i = 0; i < MAXS; ++i) {
+      if (i < s) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < MAXS; ++j)
+          if (j < s) acc += A.a[i * MAXS + j] * kv[j];
+        U[(size_t)i * n + p] = up + dt * acc;
+      }
+    }
+  }
+}
+
+// F_i = N(U_i) - K_i and ||F||^2  (src/nonlinear.py:148-152)
+template <int KIND, int NDIM, int BS>
+__global__ void k_residual(Grid g, KindParams kp, int s, const double *__restrict__ U,
+                           const double *__restrict__ K, double *__restrict__ F, double *part,
+                           int G, double *out, unsigned *counter) {
+  __shared__ double sm[32];
+  const int n = g.n;
+  double acc = 0.0;
+  for (int p = blockIdx.x * BS + threadIdx.x; p < n; p += G * BS) {
+    for (int i = 0; i < s; ++i) {
+      double f = rhs_at<KIND, NDIM>(g, kp, U + (size_t)i * n, p) - K[(size_t)i * n + p];
+      F[(size_t)i * n + p] = f;
+      acc += f * f;
+    }
+  }
+  acc = block_sum<BS>(acc, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+  if (!last_block(counter, G)) return;
+  if (threadIdx.x < 32) {
+    double t = fold_partials(part, 0, G);
+    if (threadIdx.x == 0) {
+      *out = t;
+      *counter = 0u;
+    }
+  }
+}
+
+// a_o = sum_k w[o][k] f(U_k), zero weights skipped, stage order
+// (combine, src/sparsela.py:120-127)
+template <int KIND>
+__global__ void k_opfields(int n, KindParams kp, OpWeights W, const double *__restrict__ U,
+                           double *__restrict__ A) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    double f[MAXS];
+#pragma unroll
+    for (int k = 0; k < MAXS; ++k)
+      if (k < W.s) f[k] = field_of<KIND>(kp, U[(size_t)k * n + p]);
+    for (int o = 0; o < W.nops; ++o) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < MAXS; ++k) {
+        if (k < W.s) {
+          double wk = W.w[o * MAXS + k];
+          if (wk != 0.0) acc += wk * f[k];
+        }
+      }
+      A[(size_t)o * n + p] = acc;
+    }
+  }
+}
+
+// out_i = sum_k M[i][k] in_k  (pointwise s x s mix; g = Q^T F, dk = (Q R0) y)
+// mode 0: out = M in; mode 1: out += M in (Newton update K += dk)
+__global__ void k_stage_mix(int n, int s, StageConsts M, const double *__restrict__ in,
+                            double *__restrict__ out, int accumulate) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    double v[MAXS];
+#pragma unroll
+    for (int k = 0; k < MAXS; ++k)
+      if (k < s) v[k] = in[(size_t)k * n + p];
+#pragma unroll
+    for (int i = 0; i < MAXS; ++i) {
+      if (i < s) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < MAXS; ++k)
+          if (k < s) acc += M.a[i * MAXS + k] * v[k];
+        if (accumulate)
+          out[(size_t)i * n + p] += acc;
+        else
+          out[(size_t)i * n + p] = acc;
+      }
+    }
+  }
+}
+
+// u <- u + dt * sum_i b_i K_i  (src/nonlinear.py:313)
+__global__ void k_step_update(int n, int s, StageConsts B, double dt, const double *__restrict__ K,
+                              double *__restrict__ u) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < MAXS; ++i)
+      if (i < s) acc += B.v[i] * K[(size_t)i * n + p];
+    u[p] = u[p] + dt * acc;
+  }
+}
+
+// Block right-hand side: acc_r = g_r - sum_j R0[r,j] y_j + dt * sum_j od(r,j) y_j
+// (src/irk_core.py:273-283); writes rows contiguously into rhs (rows, N).
+template <int KIND, int NDIM>
+__global__ void k_backsub(Grid g, KindParams kp, double dt, BacksubTerms T,
+                          const double *__restrict__ gst, const double *__restrict__ y,
+                          double *__restrict__ rhs) {
+  const int n = g.n;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    int nb[6];
+    neighbours<NDIM>(g, p, nb);
+    for (int r = 0; r < T.rows; ++r) {
+      double acc = gst[(size_t)(T.row0 + r) * n + p];
+      for (int q = 0; q < T.njs; ++q) {
+        const double *yj = y + (size_t)T.j[q] * n;
+        double c = T.coef[r][q];
+        if (c != 0.0) acc -= c * yj[p];
+        const Op od = T.od[r][q];
+        if (od.present) acc += dt * lx_at<KIND, NDIM>(g, kp, od.a, od.sigma, yj, p, nb);
+      }
+      rhs[(size_t)r * n + p] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------- inner solves / ops
+
+__device__ __forceinline__ void resolve_in(const VecIn &vi, const double *&ptr, double &scale) {
+  if (vi.ctrl) {
+    int j = vi.ctrl->j;
+    ptr = vi.base + (size_t)j * vi.pitch;
+    scale = vi.alpha[j];
+  } else {
+    ptr = vi.base;
+    scale = 1.0;
+  }
+}
+
+// First damped-Jacobi sweep from x = 0:  x = omega * (r / D)
+// r = scale*in (+ cpl*zc, materialised into t_out when coupling).
+template <int KIND>
+__global__ void k_jac_first(Grid g, KindParams kp, Op L, double alpha, double dt, VecIn vin,
+                            int in_off, const double *__restrict__ zc, double cpl,
+                            double *__restrict__ t_out, double *__restrict__ x_out,
+                            GCtrl *flag_ctrl, const GCtrl *skip) {
+  if (skip && skip->cycle_done) return;
+  const double *in;
+  double scale;
+  resolve_in(vin, in, scale);
+  in += in_off;
+  const int n = g.n;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    double r = scale * in[p];
+    if (zc) {
+      r = r + cpl * zc[p];
+      t_out[p] = r;
+    }
+    double D = alpha - dt * ldiag_at<KIND>(g, kp, L.a, L.sigma, p);
+    if (D == 0.0) flag_ctrl->zero_diag = 1;
+    x_out[p] = OMEGA * ((1.0 / D) * r);
+  }
+}
+
+// Later sweeps: x' = x + omega * (r - (alpha x - dt L x)) / D
+template <int KIND, int NDIM>
+__global__ void k_jac_sweep(Grid g, KindParams kp, Op L, double alpha, double dt, VecIn vin,
+                            int in_off, const double *__restrict__ t_in,
+                            const double *__restrict__ x, double *__restrict__ x_out,
+                            const GCtrl *skip) {
+  if (skip && skip->cycle_done) return;
+  const double *in = nullptr;
+  double scale = 1.0;
+  if (!t_in) {
+    resolve_in(vin, in, scale);
+    in += in_off;
+  }
+  const int n = g.n;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    int nb[6];
+    neighbours<NDIM>(g, p, nb);
+    double r = t_in ? t_in[p] : scale * in[p];
+    double xp = x[p];
+    double sx = alpha * xp - dt * lx_at<KIND, NDIM>(g, kp, L.a, L.sigma, x, p, nb);
+    double D = alpha - dt * ldiag_at<KIND>(g, kp, L.a, L.sigma, p);
+    x_out[p] = xp + OMEGA * ((1.0 / D) * (r - sx));
+  }
+}
+
+// Block operator y = A z (size 1: eta z - dt L1 z; size 2: apply_block2x2,
+// src/irk_core.py:126-140).  With b != null writes r = b - A z instead and
+// reduces ||r||^2 into *out_norm.
+template <int KIND, int NDIM, int SIZE, int BS>
+__global__ void k_block_op(Grid g, KindParams kp, double eta, double beta, double phi, double dt,
+                           Op l1, Op l2, Op c12, Op c21, const double *__restrict__ z,
+                           double *__restrict__ w, const double *__restrict__ b, double *part,
+                           int G, double *out_norm, unsigned *counter, const GCtrl *skip) {
+  __shared__ double sm[32];
+  if (skip && skip->cycle_done) return;
+  const int n = g.n;
+  double nrm = 0.0;
+  for (int p = blockIdx.x * BS + threadIdx.x; p < n; p += G * BS) {
+    int nb[6];
+    neighbours<NDIM>(g, p, nb);
+    if (SIZE == 1) {
+      double v = eta * z[p] - dt * lx_at<KIND, NDIM>(g, kp, l1.a, l1.sigma, z, p, nb);
+      if (b) {
+        v = b[p] - v;
+        nrm += v * v;
+      }
+      w[p] = v;
+    } else {
+      const double *z1 = z, *z2 = z + n;
+      double x1 = z1[p], x2 = z2[p];
+      double top = eta * x1 - dt * lx_at<KIND, NDIM>(g, kp, l1.a, l1.sigma, z1, p, nb) + phi * x2;
+      double bot = -(beta * beta / phi) * x1 + eta * x2 -
+                   dt * lx_at<KIND, NDIM>(g, kp, l2.a, l2.sigma, z2, p, nb);
+      if (c12.present) top -= dt * lx_at<KIND, NDIM>(g, kp, c12.a, c12.sigma, z2, p, nb);
+      if (c21.present) bot -= dt * lx_at<KIND, NDIM>(g, kp, c21.a, c21.sigma, z1, p, nb);
+      if (b) {
+        top = b[p] - top;
+        bot = b[p + n] - bot;
+        nrm += top * top + bot * bot;
+      }
+      w[p] = top;
+      w[p + n] = bot;
+    }
+  }
+  if (!b) return;
+  nrm = block_sum<BS>(nrm, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = nrm;
+  if (!last_block(counter, G)) return;
+  if (threadIdx.x < 32) {
+    double t = fold_partials(part, 0, G);
+    if (threadIdx.x == 0) {
+      *out_norm = t;
+      *counter = 0u;
+    }
+  }
+}
+
+// ----------------------------------------------------------- CGS2 sweeps
+
+// c_l = alpha_l * (s_l . w), l = 0..j  and  ||w||^2 (index j+1)
+// (src/sparsela.py:222, 225).  Each CTA owns a contiguous row chunk; warps
+// take disjoint l's; partials part[l*G + cta] folded by the last CTA.
+template <int BS>
+__global__ void k_mdot(int n, const double *__restrict__ V, long long pitch,
+                       const double *__restrict__ alpha, const GCtrl *ctrl,
+                       const double *__restrict__ w, double *part, int G, double *out_c,
+                       double *out_norm, unsigned *counter) {
+  __shared__ double acc[MAXR + 2];
+  if (ctrl->cycle_done) return;
+  const int L = ctrl->j + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NW = BS / 32;
+  int chunk = (n + G - 1) / G;
+  chunk = (chunk + 31) & ~31;
+  const int r0 = blockIdx.x * chunk;
+  const int r1 = min(n, r0 + chunk);
+  const int nl = out_norm ? L + 1 : L;
+  for (int l = warp; l < nl; l += NW) {
+    const double *vl = (l == L) ? w : V + (size_t)l * pitch;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int r = r0 + lane;
+    for (; r + 96 < r1; r += 128) {
+      s0 += vl[r] * w[r];
+      s1 += vl[r + 32] * w[r + 32];
+      s2 += vl[r + 64] * w[r + 64];
+      s3 += vl[r + 96] * w[r + 96];
+    }
+    for (; r < r1; r += 32) s0 += vl[r] * w[r];
+    double s = warp_sum((s0 + s1) + (s2 + s3));
+    if (lane == 0) acc[l] = s;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < nl; l += BS) part[(size_t)l * G + blockIdx.x] = acc[l];
+  if (!last_block(counter, G)) return;
+  for (int l = warp; l < nl; l += NW) {
+    double s = fold_partials(part, l, G);
+    if (lane == 0) {
+      if (l == L)
+        *out_norm = s;
+      else
+        out_c[l] = alpha[l] * s;
+    }
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// out = w - sum_l s_l (alpha_l c_l), l = 0..j  (src/sparsela.py:226); when
+// to_next_slot, out is basis slot j+1 and ||out||^2 is reduced (228).
+template <int BS>
+__global__ void k_mupdate(int n, double *__restrict__ V, long long pitch,
+                          const double *__restrict__ alpha, const GCtrl *ctrl,
+                          const double *__restrict__ coef, const double *w, double *out,
+                          int to_next_slot, double *part, int G, double *out_norm,
+                          unsigned *counter) {
+  __shared__ double cs[MAXR + 1];
+  __shared__ double sm[32];
+  if (ctrl->cycle_done) return;
+  const int L = ctrl->j + 1;
+  for (int l = threadIdx.x; l < L; l += BS) cs[l] = alpha[l] * coef[l];
+  __syncthreads();
+  double *o = to_next_slot ? V + (size_t)L * pitch : out;
+  double nrm = 0.0;
+  for (int r = blockIdx.x * BS + threadIdx.x; r < n; r += G * BS) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int l = 0;
+    for (; l + 4 <= L; l += 4) {
+      a0 += V[(size_t)l * pitch + r] * cs[l];
+      a1 += V[(size_t)(l + 1) * pitch + r] * cs[l + 1];
+      a2 += V[(size_t)(l + 2) * pitch + r] * cs[l + 2];
+      a3 += V[(size_t)(l + 3) * pitch + r] * cs[l + 3];
+    }
+    for (; l < L; ++l) a0 += V[(size_t)l * pitch + r] * cs[l];
+    double v = w[r] - ((a0 + a1) + (a2 + a3));
+    o[r] = v;
+    nrm += v * v;
+  }
+  if (!out_norm) return;
+  nrm = block_sum<BS>(nrm, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = nrm;
+  if (!last_block(counter, G)) return;
+  if (threadIdx.x < 32) {
+    double t = fold_partials(part, 0, G);
+    if (threadIdx.x == 0) {
+      *out_norm = t;
+      *counter = 0u;
+    }
+  }
+}
+
+// ------------------------------------------------------ scalar control
+
+// Start a restart cycle: v_0 = r / beta  (src/sparsela.py:207-216).
+__global__ void k_cycle_init(GWork W, int m) {
+  GCtrl *c = W.ctrl;
+  c->j = 0;
+  c->m = m;
+  c->k = 0;
+  c->cycle_done = 0;
+  c->breakdown = 0;
+  W.g[0] = c->beta;
+  W.alpha[0] = 1.0 / c->beta;
+}
+
+// Finish Arnoldi column j: H column, breakdown test, Givens rotations,
+// residual estimate and the loop exit test (src/sparsela.py:227-256).
+__global__ void k_arnoldi_finish(GWork W) {
+  GCtrl *c = W.ctrl;
+  if (c->cycle_done) return;
+  const int j = c->j;
+  double *h = W.H + (size_t)j * (MAXR + 1);
+  for (int i = 0; i <= j; ++i) h[i] = (0.0 + W.c1[i]) + W.c2[i];
+  const double hj = sqrt(c->hn2);
+  const double wnorm0 = sqrt(c->wn2);
+  h[j + 1] = hj;
+  bool breakdown = hj <= 1e-14 * fmax(wnorm0, 1e-300);
+  if (!breakdown) W.alpha[j + 1] = 1.0 / hj;
+  for (int i = 0; i < j; ++i) {
+    double tmp = W.cs[i] * h[i] + W.sn[i] * h[i + 1];
+    h[i + 1] = -W.sn[i] * h[i] + W.cs[i] * h[i + 1];
+    h[i] = tmp;
+  }
+  double denom = hypot(h[j], h[j + 1]);
+  if (denom == 0.0) {
+    // dead column: drop it and stop (src/sparsela.py:239-246)
+    c->breakdown = 1;
+    c->total_it += 1;
+    W.res[c->n_res] = W.res[c->n_res - 1];
+    c->n_res += 1;
+    c->k = j;
+    c->cycle_done = 1;
+    return;
+  }
+  W.cs[j] = h[j] / denom;
+  W.sn[j] = h[j + 1] / denom;
+  h[j] = denom;
+  h[j + 1] = 0.0;
+  W.g[j + 1] = -W.sn[j] * W.g[j];
+  W.g[j] = W.cs[j] * W.g[j];
+  c->total_it += 1;
+  double est = fabs(W.g[j + 1]) / c->bnorm;
+  W.res[c->n_res] = est;
+  c->n_res += 1;
+  if (breakdown) c->breakdown = 1;
+  if (est <= c->rtol || breakdown || c->total_it >= c->maxit || j + 1 >= c->m) {
+    c->k = j + 1;
+    c->cycle_done = 1;
+  } else {
+    c->j = j + 1;
+  }
+}
+
+// y = H(:k,:k)^{-1} g(:k) by back substitution (src/sparsela.py:258-261),
+// then fold alpha into y so that x += V (alpha .* y).
+__global__ void k_backsolve(GWork W) {
+  GCtrl *c = W.ctrl;
+  const int k = c->k;
+  for (int i = k - 1; i >= 0; --i) {
+    double dot = 0.0;
+    for (int l = i + 1; l < k; ++l) dot += W.H[(size_t)l * (MAXR + 1) + i] * W.y[l];
+    W.y[i] = (W.g[i] - dot) / W.H[(size_t)i * (MAXR + 1) + i];
+  }
+  for (int i = 0; i < k; ++i) W.c1[i] = W.alpha[i] * W.y[i];
+}
+
+// out = sum_{l<k} s_l * coef_l
+__global__ void k_vcombine(int n, const double *__restrict__ V, long long pitch, const GCtrl *ctrl,
+                           const double *__restrict__ coef, double *__restrict__ out) {
+  const int k = ctrl->k;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    double a0 = 0.0, a1 = 0.0;
+    int l = 0;
+    for (; l + 2 <= k; l += 2) {
+      a0 += V[(size_t)l * pitch + r] * coef[l];
+      a1 += V[(size_t)(l + 1) * pitch + r] * coef[l + 1];
+    }
+    if (l < k) a0 += V[(size_t)l * pitch + r] * coef[l];
+    out[r] = a0 + a1;
+  }
+}
+
+__global__ void k_axpy(int n, double a, const double *__restrict__ x, double *__restrict__ y) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    y[r] = y[r] + a * x[r];
+}
+
+// True residual bookkeeping after x += Z y (src/sparsela.py:263-272).
+__global__ void k_cycle_end(GWork W) {
+  GCtrl *c = W.ctrl;
+  double rn = sqrt(c->rr);
+  double true_rel = rn / c->bnorm;
+  W.res[c->n_res - 1] = true_rel;
+  if (true_rel <= c->rtol)
+    c->converged = 1;
+  else if (c->breakdown)
+    c->err_breakdown = 1;
+  c->beta = rn;
+}
+
+// ============================================================ launchers
+
+template <class F>
+static void dispatch_kind(int kind, F f) {
+  switch (kind) {
+    case KIND_NLDIFF: f(std::integral_constant<int, KIND_NLDIFF>{}); break;
+    case KIND_BURGERS: f(std::integral_constant<int, KIND_BURGERS>{}); break;
+    default: f(std::integral_constant<int, KIND_RAD>{}); break;
+  }
+}
+
+template <class F>
+static void dispatch_kd(int kind, int ndim, F f) {
+  dispatch_kind(kind, [&](auto K) {
+    switch (ndim) {
+      case 1: f(K, std::integral_constant<int, 1>{}); break;
+      case 2: f(K, std::integral_constant<int, 2>{}); break;
+      default: f(K, std::integral_constant<int, 3>{}); break;
+    }
+  });
+}
+
+int Engine::grid_for(long long n) const {
+  long long b = (n + 255) / 256;
+  long long cap = (long long)sms * 8;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+void Engine::count(int k) { counters.kernel_launches += k; }
+
+double Engine::norm2(const double *x, long long n, const GCtrl *skip) {
+  k_norm2<256><<<G, 256, 0, stream>>>((int)n, x, part, G, &scal_dev[0], counter, skip);
+  count(1);
+  double v = 0.0;
+  check(cudaMemcpyAsync(&v, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost, stream));
+  check(cudaStreamSynchronize(stream));
+  return v;
+}
+
+void Engine::stage_values(const double *u, const double *K, double dt, double *U) {
+  StageConsts A{};
+  A.s = s;
+  for (int i = 0; i < s; ++i)
+    for (int j = 0; j < s; ++j) A.a[i * MAXS + j] = tab.a0[i * IRKG_MAX_STAGES + j];
+  k_stage_values<<<grid_for(N), 256, 0, stream>>>((int)N, s, u, K, A, dt, U);
+  count(1);
+}
+
+double Engine::residual(const double *U, const double *K, double *F) {
+  dispatch_kd(prob.kind, ndim, [&](auto KD, auto ND) {
+    k_residual<decltype(KD)::value, decltype(ND)::value, 256>
+        <<<G, 256, 0, stream>>>(grid, kp, s, U, K, F, part, G, &scal_dev[0], counter);
+  });
+  count(1);
+  double v = 0.0;
+  check(cudaMemcpyAsync(&v, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost, stream));
+  check(cudaStreamSynchronize(stream));
+  return v;
+}
+
+void Engine::opfields(const double *U, const OpWeights &W, double *A) {
+  dispatch_kind(prob.kind, [&](auto KD) {
+    k_opfields<decltype(KD)::value><<<grid_for(N), 256, 0, stream>>>((int)N, kp, W, U, A);
+  });
+  count(1);
+}
+
+void Engine::stage_mix(const double *M_rowmajor_s, const double *in, double *out, bool accumulate) {
+  StageConsts M{};
+  M.s = s;
+  for (int i = 0; i < s; ++i)
+    for (int k = 0; k < s; ++k) M.a[i * MAXS + k] = M_rowmajor_s[i * s + k];
+  k_stage_mix<<<grid_for(N), 256, 0, stream>>>((int)N, s, M, in, out, accumulate ? 1 : 0);
+  count(1);
+}
+
+void Engine::step_update(double dt, const double *K, double *u) {
+  StageConsts B{};
+  B.s = s;
+  for (int i = 0; i < s; ++i) B.v[i] = tab.b0[i];
+  k_step_update<<<grid_for(N), 256, 0, stream>>>((int)N, s, B, dt, K, u);
+  count(1);
+}
+
+void Engine::backsub(double dt, const BacksubTerms &T, const double *gst, const double *y,
+                     double *rhs) {
+  dispatch_kd(prob.kind, ndim, [&](auto KD, auto ND) {
+    k_backsub<decltype(KD)::value, decltype(ND)::value>
+        <<<grid_for(N), 256, 0, stream>>>(grid, kp, dt, T, gst, y, rhs);
+  });
+  count(1);
+}
+
+// Jacobi-k chain on (alpha I - dt L): x_out = S^{-1}_k (scale*in [+cpl*zc])
+void Engine::jacobi_chain(const Op &L, double alpha, double dt, int inner, const void *vin_p,
+                          int in_off, const double *zc, double cpl, double *x_out,
+                          const GCtrl *skip) {
+  const VecIn &vin = *static_cast<const VecIn *>(vin_p);
+  const int gb = grid_for(N);
+  double *tbuf = zc ? tmp_t : nullptr;
+  // sweep i (1-based) writes into out if (inner - i) even, else tmp_x
+  auto dst = [&](int i) { return ((inner - i) % 2 == 0) ? x_out : tmp_x; };
+  dispatch_kind(prob.kind, [&](auto KD) {
+    k_jac_first<decltype(KD)::value><<<gb, 256, 0, stream>>>(grid, kp, L, alpha, dt, vin, in_off,
+                                                               zc, cpl, tbuf, dst(1), ctrl_dev,
+                                                               skip);
+  });
+  count(1);
+  for (int i = 2; i <= inner; ++i) {
+    const double *xin = dst(i - 1);
+    double *xo = dst(i);
+    dispatch_kd(prob.kind, ndim, [&](auto KD, auto ND) {
+      k_jac_sweep<decltype(KD)::value, decltype(ND)::value>
+          <<<gb, 256, 0, stream>>>(grid, kp, L, alpha, dt, vin, in_off, tbuf, xin, xo, skip);
+    });
+    count(1);
+  }
+  counters.precond_bytes += 8.0 * N * ((zc ? 4.0 : 3.0) + (inner - 1) * 4.0);
+}
+
+void Engine::precond(const BlockSpec &B, const void *vin_p, double *z, const GCtrl *skip) {
+  if (B.size == 1) {
+    jacobi_chain(B.l1, B.eta, B.dt, B.inner, vin_p, 0, nullptr, 0.0, z, skip);
+  } else {
+    jacobi_chain(B.l1, B.eta, B.dt, B.inner, vin_p, 0, nullptr, 0.0, z, skip);
+    jacobi_chain(B.l2, B.gamma, B.dt, B.inner, vin_p, (int)N, z, B.beta * B.beta / B.phi, z + N,
+                 skip);
+  }
+}
+
+void Engine::block_op(const BlockSpec &B, const double *z, double *w, const double *b,
+                      double *out_norm, const GCtrl *skip) {
+  dispatch_kd(prob.kind, ndim, [&](auto KD, auto ND) {
+    constexpr int K_ = decltype(KD)::value, D_ = decltype(ND)::value;
+    if (B.size == 1)
+      k_block_op<K_, D_, 1, 256><<<G, 256, 0, stream>>>(grid, kp, B.eta, B.beta, B.phi, B.dt,
+                                                         B.l1, B.l2, B.c12, B.c21, z, w, b, part,
+                                                         G, out_norm, counter, skip);
+    else
+      k_block_op<K_, D_, 2, 256><<<G, 256, 0, stream>>>(grid, kp, B.eta, B.beta, B.phi, B.dt,
+                                                         B.l1, B.l2, B.c12, B.c21, z, w, b, part,
+                                                         G, out_norm, counter, skip);
+  });
+  count(1);
+  counters.op_bytes += 8.0 * N * B.size * 3.0;
+}
+
+void Engine::mdot(long long n, const double *w, double *out_c, double *out_norm) {
+  k_mdot<256><<<G, 256, 0, stream>>>((int)n, V, vpitch, W.alpha, ctrl_dev, w, part, G, out_c,
+                                     out_norm, counter);
+  count(1);
+}
+
+void Engine::mupdate(long long n, const double *coef, const double *w, double *out,
+                     bool to_next, double *out_norm) {
+  k_mupdate<256><<<G, 256, 0, stream>>>((int)n, V, vpitch, W.alpha, ctrl_dev, coef, w, out,
+                                        to_next ? 1 : 0, part, G, out_norm, counter);
+  count(1);
+}
+
+void Engine::cycle_init(int m) {
+  k_cycle_init<<<1, 1, 0, stream>>>(W, m);
+  count(1);
+}
+void Engine::arnoldi_finish() {
+  k_arnoldi_finish<<<1, 1, 0, stream>>>(W);
+  count(1);
+}
+void Engine::backsolve() {
+  k_backsolve<<<1, 1, 0, stream>>>(W);
+  count(1);
+}
+void Engine::vcombine(long long n, const double *coef, double *out) {
+  k_vcombine<<<grid_for(n), 256, 0, stream>>>((int)n, V, vpitch, ctrl_dev, coef, out);
+  count(1);
+}
+void Engine::axpy(long long n, double a, const double *x, double *y) {
+  k_axpy<<<grid_for(n), 256, 0, stream>>>((int)n, a, x, y);
+  count(1);
+}
+void Engine::cycle_end() {
+  k_cycle_end<<<1, 1, 0, stream>>>(W);
+  count(1);
+}
+
+}  // namespace irkg

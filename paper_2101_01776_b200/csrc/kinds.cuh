@@ -1,0 +1,140 @@
+// kinds.cuh -- matrix-free problem kinds: N(u), L(a, sigma) x, diag L, f(U).
+//
+// Replaces the reference's problem callbacks OdeSystem.rhs / .linearize
+// (src/nonlinear.py:35-48) and the CSR weighted sums of
+// build_variant_jacobian / combine (src/nonlinear.py:129-142,
+// src/sparsela.py:106-128).  Every Jacobian of the supported kinds is affine
+// in one pointwise function f(U) of the stage state, so
+//      sum_k w_k L(U_k)  ==  L_eff(a, sigma),  a = sum_k w_k f(U_k),
+//                                              sigma = sum_k w_k,
+// and an operator is carried on the device as one coefficient field a plus
+// the scalar sigma.
+//
+//   kind     N(u)                              L_eff(a,sigma) x                f(U)
+//   nldiff   Lap(u + u^3/3)                    Lap(a x)                        1 + U^2
+//   burgers  -Dsum(u^2/2) + nu Lap u           -Dsum(a x) + sigma nu Lap x     U
+//   rad      nu Lap u + c Dsum u + lam u       sigma (nu Lap x + c Dsum x)     lam + 2 mu U
+//              + mu u^2                          + a x
+//
+// Lap = periodic 2d+1-point Laplacian, Dsum = sum of periodic central
+// differences, x fastest: p = (iz*ny + iy)*nx + ix (src/problems.py:238-239).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace irkg {
+
+enum { KIND_NLDIFF = 0, KIND_BURGERS = 1, KIND_RAD = 2 };
+
+struct Grid {
+  int nx, ny, nz;  // local extents (ny or nz is the slab axis when partitioned)
+  int nxy;         // nx*ny
+  int n;           // nx*ny*nz local points
+  double ih2[3];   // 1/h^2 per axis, 0 for an axis of extent 1
+  double i2h[3];   // 1/(2h) per axis, 0 for an axis of extent 1
+  double lapdiag;  // diagonal of Lap: -2 * sum ih2
+};
+
+struct KindParams {
+  double nu, c, lam, mu;
+};
+
+// Periodic neighbours of p: [xm, xp, ym, yp, zm, zp].
+template <int NDIM>
+__device__ __forceinline__ void neighbours(const Grid &g, int p, int nb[6]) {
+  int ix = p % g.nx;
+  nb[0] = p + (ix == 0 ? g.nx - 1 : -1);
+  nb[1] = p + (ix == g.nx - 1 ? 1 - g.nx : 1);
+  if (NDIM >= 2) {
+    int r = p / g.nx;
+    int iy = (NDIM == 3) ? r % g.ny : r;
+    nb[2] = p + (iy == 0 ? (g.ny - 1) * g.nx : -g.nx);
+    nb[3] = p + (iy == g.ny - 1 ? -(g.ny - 1) * g.nx : g.nx);
+    if (NDIM == 3) {
+      int iz = r / g.ny;
+      nb[4] = p + (iz == 0 ? (g.nz - 1) * g.nxy : -g.nxy);
+      nb[5] = p + (iz == g.nz - 1 ? -(g.nz - 1) * g.nxy : g.nxy);
+    }
+  }
+}
+
+// sum over axes of ih2 * (v[p+e] + v[p-e] - 2 v[p]) for a value functor
+template <int NDIM, class F>
+__device__ __forceinline__ double lap_of(const Grid &g, const int nb[6], double vp, F v) {
+  double s = g.ih2[0] * (v(nb[0]) + v(nb[1]) - 2.0 * vp);
+  if (NDIM >= 2) s += g.ih2[1] * (v(nb[2]) + v(nb[3]) - 2.0 * vp);
+  if (NDIM == 3) s += g.ih2[2] * (v(nb[4]) + v(nb[5]) - 2.0 * vp);
+  return s;
+}
+
+template <int NDIM, class F>
+__device__ __forceinline__ double dsum_of(const Grid &g, const int nb[6], F v) {
+  double s = g.i2h[0] * (v(nb[1]) - v(nb[0]));
+  if (NDIM >= 2) s += g.i2h[1] * (v(nb[3]) - v(nb[2]));
+  if (NDIM == 3) s += g.i2h[2] * (v(nb[5]) - v(nb[4]));
+  return s;
+}
+
+// N(u)[p]
+template <int KIND, int NDIM>
+__device__ __forceinline__ double rhs_at(const Grid &g, const KindParams &kp,
+                                         const double *__restrict__ u, int p) {
+  int nb[6];
+  neighbours<NDIM>(g, p, nb);
+  double up = u[p];
+  if (KIND == KIND_NLDIFF) {
+    auto phi = [&](int q) {
+      double v = u[q];
+      return v + v * v * v / 3.0;
+    };
+    return lap_of<NDIM>(g, nb, up + up * up * up / 3.0, phi);
+  } else if (KIND == KIND_BURGERS) {
+    auto half_sq = [&](int q) {
+      double v = u[q];
+      return 0.5 * v * v;
+    };
+    auto val = [&](int q) { return u[q]; };
+    return -dsum_of<NDIM>(g, nb, half_sq) + kp.nu * lap_of<NDIM>(g, nb, up, val);
+  } else {
+    auto val = [&](int q) { return u[q]; };
+    return kp.nu * lap_of<NDIM>(g, nb, up, val) + kp.c * dsum_of<NDIM>(g, nb, val) +
+           kp.lam * up + kp.mu * up * up;
+  }
+}
+
+// f(U): the pointwise function whose weighted sum is the operator field
+template <int KIND>
+__device__ __forceinline__ double field_of(const KindParams &kp, double U) {
+  if (KIND == KIND_NLDIFF) return 1.0 + U * U;
+  if (KIND == KIND_BURGERS) return U;
+  return kp.lam + 2.0 * kp.mu * U;
+}
+
+// (L_eff(a, sigma) x)[p]
+template <int KIND, int NDIM>
+__device__ __forceinline__ double lx_at(const Grid &g, const KindParams &kp,
+                                        const double *__restrict__ a, double sigma,
+                                        const double *__restrict__ x, int p, const int nb[6]) {
+  if (KIND == KIND_NLDIFF) {
+    auto ax = [&](int q) { return a[q] * x[q]; };
+    return lap_of<NDIM>(g, nb, a[p] * x[p], ax);
+  } else if (KIND == KIND_BURGERS) {
+    auto ax = [&](int q) { return a[q] * x[q]; };
+    auto xv = [&](int q) { return x[q]; };
+    return -dsum_of<NDIM>(g, nb, ax) + sigma * kp.nu * lap_of<NDIM>(g, nb, x[p], xv);
+  } else {
+    auto xv = [&](int q) { return x[q]; };
+    return sigma * (kp.nu * lap_of<NDIM>(g, nb, x[p], xv) + kp.c * dsum_of<NDIM>(g, nb, xv)) +
+           a[p] * x[p];
+  }
+}
+
+// diagonal entry of L_eff(a, sigma) at p
+template <int KIND>
+__device__ __forceinline__ double ldiag_at(const Grid &g, const KindParams &kp,
+                                           const double *__restrict__ a, double sigma, int p) {
+  if (KIND == KIND_NLDIFF) return g.lapdiag * a[p];
+  if (KIND == KIND_BURGERS) return sigma * kp.nu * g.lapdiag;
+  return sigma * kp.nu * g.lapdiag + a[p];
+}
+
+}  // namespace irkg

@@ -1,0 +1,361 @@
+"""irkit-compatible solver entry points, running on the B200 engine.
+
+Same names, argument meaning and error behaviour as the reference
+(``/root/reference/pkg/src/irkit``):
+
+* ``stage_residual``           src/nonlinear.py:145-152
+* ``newton_like_step``         src/nonlinear.py:186-236
+* ``step``                     src/nonlinear.py:299-314
+* ``integrate``                src/nonlinear.py:331-374
+* ``solve_transformed_system`` src/irk_core.py:225-338
+* ``apply_block2x2`` / ``precond_block2x2`` / ``ShiftedSolver`` /
+  ``block_gmres``              src/irk_core.py:71-165, src/sparsela.py:176-280
+
+``sys`` is a :class:`~paper_2101_01776_b200.problems.GridProblem` (the
+device-side analogue of ``OdeSystem``).  State arrays may be numpy arrays
+(results come back as numpy, like the reference) or CUDA torch tensors
+(results stay on the device).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .config import PrecondSpec, SolverConfig, inner_sweeps
+from .engine import _raise, as_device, context_for, opfield, ptr, torch
+from .errors import ConfigurationError, StepFailureError
+from .stats import IntegrationResult, KrylovReport, SolveStats
+from .tableau import SDIRK_FAMILIES, prepare_stages
+
+
+def _check_sys(sys):
+    if getattr(sys, "mass", None) is not None:
+        raise ConfigurationError("the device engine supports identity mass only (M = I)")
+    if not hasattr(sys, "kind"):
+        raise ConfigurationError(
+            "device solves need a GridProblem (paper_2101_01776_b200.problems); "
+            "host-callable OdeSystems run on the reference"
+        )
+
+
+def _is_torch(x):
+    try:
+        return isinstance(x, torch().Tensor)
+    except ImportError:
+        return False
+
+
+def _out(x_dev, like):
+    if _is_torch(like):
+        return x_dev
+    return x_dev.cpu().numpy()
+
+
+@dataclass
+class StageState:
+    """Current stage vectors and step context (src/nonlinear.py:51-58)."""
+
+    k: object  # (s, dim)
+    u: object
+    t: float
+    dt: float
+
+
+def _sdirk_guard(tableau):
+    if str(tableau.family) in SDIRK_FAMILIES:
+        raise ConfigurationError(
+            f"{tableau.family} is an SDIRK baseline (src/nonlinear.py:239-296), "
+            "outside the device stage-solve path"
+        )
+
+
+def stage_residual(sys, st: StageState, tableau):
+    """``N(u + dt * sum_j a_ij k_j, t + c_i dt) - k_i`` per stage."""
+    _check_sys(sys)
+    ctx = context_for(sys)
+    ctx.set_prep(_prep_for(tableau))
+    u = as_device(st.u)
+    k = as_device(st.k).reshape(tableau.s, sys.dim)
+    f = torch().empty_like(k)
+    ctx.stage_residual(u, k, st.t, st.dt, f)
+    return _out(f, st.k)
+
+
+_PREP_CACHE = {}
+
+
+def _prep_for(tableau, prep=None):
+    if prep is not None:
+        return prep
+    key = (str(tableau.family), int(tableau.s), np.asarray(tableau.a0).tobytes())
+    p = _PREP_CACHE.get(key)
+    if p is None:
+        p = prepare_stages(tableau)
+        _PREP_CACHE[key] = p
+    return p
+
+
+def newton_like_step(sys, st: StageState, prep, cfg: SolverConfig):
+    """Drive the stage vectors to the residual tolerance on the device.
+
+    Returns ``(st, StepStats)`` with ``st.k`` rebound (not mutated), like the
+    reference; exhausting ``newton_maxit`` raises StepFailureError(stats).
+    """
+    _check_sys(sys)
+    _sdirk_guard(prep.tableau)
+    ctx = context_for(sys)
+    ctx.set_prep(prep)
+    ctx.set_config(cfg)
+    u = as_device(st.u)
+    k = as_device(st.k).reshape(prep.tableau.s, sys.dim).clone()
+    stats = ctx.newton(u, k, st.t, st.dt)
+    st.k = _out(k, st.k)
+    return st, stats
+
+
+def step(sys, u, t, dt, tableau, cfg=SolverConfig(), prep=None):
+    """Advance one step: solve the stages, then ``u + dt * sum b_i k_i``.
+
+    Returns ``(u_next, StepStats)``.
+    """
+    _check_sys(sys)
+    _sdirk_guard(tableau)
+    prep = _prep_for(tableau, prep)
+    ctx = context_for(sys)
+    ctx.set_prep(prep)
+    ctx.set_config(cfg)
+    if _is_torch(u):
+        ud = as_device(u).clone()
+        stats = ctx.step_device(ud, t, dt)
+        return ud, stats
+    uh = np.array(u, dtype=np.float64, copy=True, order="C")
+    stats = ctx.step_host(uh, t, dt)
+    return uh, stats
+
+
+def integrate(sys, u0, t0, t_final, dt, tableau, cfg=SolverConfig(), snapshot_every=None):
+    """Fixed-step march from ``t0`` to ``t_final`` (src/nonlinear.py:331-374).
+
+    The state stays resident on the device between steps; snapshots are
+    copied back to the host.  The first failing step raises
+    StepFailureError with ``partial`` attached.
+    """
+    _check_sys(sys)
+    span = t_final - t0
+    nsteps_f = span / dt
+    nsteps = int(round(nsteps_f))
+    if abs(nsteps_f - nsteps) > 1e-8 * max(1.0, abs(nsteps_f)):
+        raise ConfigurationError(f"(t_final - t0)/dt = {nsteps_f} is not an integer step count")
+    _sdirk_guard(tableau)
+    prep = _prep_for(tableau)
+    ctx = context_for(sys)
+    ctx.set_prep(prep)
+    ctx.set_config(cfg)
+    on_dev = _is_torch(u0)
+    u = as_device(u0).clone()
+    host = (lambda x: x.clone()) if on_dev else (lambda x: x.cpu().numpy())
+    times = [t0]
+    states = [host(u)]
+    step_stats = []
+    for j in range(nsteps):
+        t = t0 + j * dt
+        try:
+            stats = ctx.step_device(u, t, dt)
+        except StepFailureError as exc:
+            exc.partial = IntegrationResult(times=np.array(times), states=states,
+                                            step_stats=step_stats)
+            raise
+        step_stats.append(stats)
+        keep = snapshot_every is None or ((j + 1) % snapshot_every == 0)
+        if keep or j == nsteps - 1:
+            times.append(t0 + (j + 1) * dt)
+            states.append(host(u))
+    return IntegrationResult(times=np.array(times), states=states, step_stats=step_stats)
+
+
+# ------------------------------------------------------ operator level
+
+
+class OperatorField:
+    """A device linearisation ``sum_k w_k L(U_k)`` held as its coefficient
+    field ``a`` (CUDA tensor, N) and weight sum ``sigma`` -- the engine's
+    replacement for the CSR ``SparseMatrix`` returned by ``linearize`` and
+    summed by ``combine`` (src/sparsela.py:106-128)."""
+
+    def __init__(self, problem, a, sigma=1.0):
+        self.problem = problem
+        self.a = None if a is None else as_device(a)
+        self.sigma = float(sigma)
+
+    @classmethod
+    def linearize(cls, problem, u_stages, weights=None):
+        """Field of ``sum_k w_k L(U_k)`` for stage values ``u_stages`` (m, N)."""
+        ctx = context_for(problem)
+        U = as_device(u_stages)
+        if U.dim() == 1:
+            U = U.reshape(1, -1)
+        if weights is None:
+            weights = [1.0] + [0.0] * (U.shape[0] - 1)
+        a, sig = ctx.linearize(U.contiguous(), weights)
+        return cls(problem, a, sig)
+
+
+@dataclass(frozen=True)
+class Block2x2System:
+    """One complex eigen-block system (src/irk_core.py:71-95), identity mass."""
+
+    eta: float
+    beta: float
+    phi: float
+    mass: object
+    l1: OperatorField
+    l2: OperatorField
+    dt: float
+    offdiag12: OperatorField = None
+    offdiag21: OperatorField = None
+
+    @property
+    def n(self):
+        return self.l1.problem.dim
+
+
+def apply_block2x2(sys2: Block2x2System, x):
+    """Matrix action of the 2x2 eigen-block system on ``x`` (length 2n)."""
+    n = sys2.n
+    xd = as_device(x)
+    if tuple(xd.shape) != (2 * n,):
+        raise ValueError(f"x has shape {tuple(xd.shape)}, expected ({2 * n},)")
+    ctx = context_for(sys2.l1.problem)
+    y = torch().empty_like(xd)
+    rc = ctx.lib.irkg_block2x2_apply(
+        ctx.h, sys2.eta, sys2.beta, sys2.phi, sys2.dt, opfield(sys2.l1), opfield(sys2.l2),
+        opfield(sys2.offdiag12), opfield(sys2.offdiag21), ptr(xd), ptr(y))
+    if rc:
+        _raise(rc)
+    return _out(y, x)
+
+
+def precond_block2x2(sys2: Block2x2System, spec: PrecondSpec, r):
+    """One application of the block lower-triangular preconditioner."""
+    rd = as_device(r)
+    ctx = context_for(sys2.l1.problem)
+    z = torch().empty_like(rd)
+    rc = ctx.lib.irkg_block2x2_precond(
+        ctx.h, sys2.eta, sys2.beta, sys2.phi, spec.gamma(sys2.eta, sys2.beta), sys2.dt,
+        inner_sweeps(spec), opfield(sys2.l1), opfield(sys2.l2), ptr(rd), ptr(z))
+    if rc:
+        _raise(rc)
+    return _out(z, r)
+
+
+class ShiftedSolver:
+    """Applies ``(alpha*I - dt*L)^{-1}`` by k damped-Jacobi sweeps
+    (src/irk_core.py:103-123)."""
+
+    def __init__(self, alpha, mass, lmat: OperatorField, dt, inner=4):
+        if mass is not None:
+            raise ConfigurationError("identity mass only")
+        if inner == "exact":
+            inner_sweeps(PrecondSpec(inner="exact"))
+        self.alpha = float(alpha)
+        self.lmat = lmat
+        self.dt = float(dt)
+        self.inner = int(inner)
+
+    def solve(self, r):
+        rd = as_device(r)
+        ctx = context_for(self.lmat.problem)
+        x = torch().empty_like(rd)
+        rc = ctx.lib.irkg_shifted_solve(ctx.h, self.alpha, self.dt, self.inner,
+                                        opfield(self.lmat), ptr(rd), ptr(x))
+        if rc:
+            _raise(rc)
+        return _out(x, r)
+
+
+def block_gmres(sys2, rhs, spec=PrecondSpec(inner=4), rtol=1e-5, maxit=200, restart=200):
+    """GMRES on one eigen-block with its reference preconditioner.
+
+    ``sys2`` is a Block2x2System (block preconditioner, src/irk_core.py:
+    303-333) or a ``(eta, OperatorField, dt)`` tuple for a 1x1 block
+    (``_solve_1x1``, src/irk_core.py:215-222).  Returns ``(x, KrylovReport)``.
+    """
+    rd = as_device(rhs)
+    if isinstance(sys2, Block2x2System):
+        size, eta, beta, phi, dt = 2, sys2.eta, sys2.beta, sys2.phi, sys2.dt
+        l1, l2, c12, c21 = sys2.l1, sys2.l2, sys2.offdiag12, sys2.offdiag21
+        gamma = spec.gamma(eta, beta)
+    else:
+        eta, l1, dt = sys2
+        size, beta, phi, gamma, l2, c12, c21 = 1, 0.0, 1.0, float(eta), None, None, None
+    n = l1.problem.dim
+    if tuple(rd.shape) != (size * n,):
+        raise ValueError(f"rhs has shape {tuple(rd.shape)}, expected ({size * n},)")
+    ctx = context_for(l1.problem)
+    x = torch().empty_like(rd)
+    res = (C.c_double * (int(maxit) + 4))()
+    rep = _lib.KrylovReportC()
+    rep.residuals = C.cast(res, C.POINTER(C.c_double))
+    rep.residual_capacity = len(res)
+    rc = ctx.lib.irkg_block_gmres(
+        ctx.h, size, float(eta), float(beta), float(phi), float(gamma), float(dt),
+        inner_sweeps(spec), opfield(l1), opfield(l2), opfield(c12), opfield(c21), ptr(rd),
+        ptr(x), float(rtol), int(maxit), int(restart), C.byref(rep))
+    if rc:
+        _raise(rc)
+    report = KrylovReport(int(rep.iterations), bool(rep.converged),
+                          list(res[: min(rep.n_residuals, len(res))]),
+                          int(rep.precond_applications))
+    return _out(x, rhs), report
+
+
+class StageLinearization:
+    """The s stage linearisations of ``sys`` at ``u + dt A0 K`` -- the device
+    analogue of the ``stage_ops`` list of CSR matrices the reference passes
+    to ``solve_transformed_system``."""
+
+    def __init__(self, sys, u, k, dt):
+        self.sys = sys
+        self.u = as_device(u)
+        self.k = as_device(k)
+        self.dt = float(dt)
+
+
+def solve_transformed_system(prep, stage_ops=None, variant=None, dt=None, rhs_stages=None,
+                             mass=None, precond=PrecondSpec(inner=4), krylov_rtol=1e-5,
+                             krylov_maxit=200, restart=200, variant_jacobian=None):
+    """Solve one linearised stage system through the Schur transform.
+
+    ``stage_ops`` is a :class:`StageLinearization`.  Returns ``(k, SolveStats)``;
+    a non-convergent block solve raises StageSolveError(block_offset, report).
+    """
+    if variant_jacobian is not None:
+        raise ConfigurationError("pass stage_ops=StageLinearization(...) and variant")
+    if mass is not None:
+        raise ConfigurationError("identity mass only")
+    if dt is None or dt <= 0.0:
+        raise ValueError("dt must be positive")
+    lin = stage_ops
+    s = prep.tableau.s
+    rhs = as_device(rhs_stages)
+    if rhs.shape[0] != s:
+        raise ValueError(f"rhs has {rhs.shape[0]} stage rows, expected {s}")
+    cfg = SolverConfig(variant=variant, krylov_rtol=krylov_rtol, krylov_maxit=krylov_maxit,
+                       restart=restart, precond=precond)
+    ctx = context_for(lin.sys)
+    ctx.set_prep(prep)
+    ctx.set_config(cfg)
+    ctx.prepare_linearization(lin.u, lin.k.reshape(s, -1), lin.dt)
+    dk = torch().empty_like(rhs)
+    st = ctx.transformed_solve(dt, rhs.contiguous(), dk)
+    stats = SolveStats()
+    for i in range(st.n_block_records):
+        its = int(st.block_iterations[i])
+        size = 2 if any(b.offset == st.block_offset[i] and b.size == 2 for b in prep.blocks) else 1
+        stats.reports.append(
+            (int(st.block_offset[i]), KrylovReport(its, True, [], its * size)))
+    return _out(dk, rhs_stages), stats

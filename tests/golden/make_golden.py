@@ -1,0 +1,202 @@
+"""Generate the golden fixtures from the REAL reference (build container only).
+
+Run from the repo root:  ``python tests/golden/make_golden.py``
+
+It imports ``irkit`` from ``/root/reference/pkg/src`` (read-only; absent on
+the GPU box, which only reads the committed outputs) and writes:
+
+* ``tests/golden/tableaux.json`` and ``paper_2101_01776_b200/data/tableaux.json``:
+  ``make_tableau`` + ``prepare_stages`` constants (src/tableau.py:329-379)
+  for every collocation family and stage count, as hex floats (bit-exact).
+* ``tests/golden/<case>.npz`` + ``<case>.json``: ``irkit.integrate`` runs of
+  the oracle problem builders (``oracle/problems.py``) on seeded
+  ``fourier_u0`` fields: initial and final state plus per-step StepStats
+  (Newton / Krylov counts, per-block iteration lists, residual histories).
+* ``tests/golden/transformed.json``: Krylov counts and solutions of
+  ``solve_transformed_system`` on small linear systems for every variant.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, ROOT)
+
+import irkit  # noqa: E402
+from irkit.irk_core import PrecondSpec, solve_transformed_system  # noqa: E402
+from irkit.nonlinear import OdeSystem, SolverConfig, integrate  # noqa: E402
+from irkit.sparsela import SparseMatrix  # noqa: E402
+
+from oracle.problems import build_problem  # noqa: E402
+from paper_2101_01776_b200.problems import GridProblem, baseline_config, fourier_u0  # noqa: E402
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+FAMILIES = [("gauss", s) for s in range(1, 9)] + [("radau_iia", s) for s in range(1, 9)] + [
+    ("lobatto_iiic", s) for s in range(2, 9)
+]
+
+
+def _hex(a):
+    a = np.asarray(a, dtype=float)
+    return {"shape": list(a.shape), "data": [float(x).hex() for x in a.ravel()]}
+
+
+def dump_tableaux():
+    doc = {}
+    for fam, s in FAMILIES:
+        tab = irkit.make_tableau(fam, s)
+        prep = irkit.prepare_stages(tab)
+        doc[f"{fam}:{s}"] = {
+            "family": tab.family,
+            "s": tab.s,
+            "order": tab.order,
+            "a0": _hex(tab.a0),
+            "b0": _hex(tab.b0),
+            "c0": _hex(tab.c0),
+            "a0inv": _hex(prep.a0inv),
+            "q": _hex(prep.schur.q),
+            "r": _hex(prep.schur.r),
+            "blocks": [
+                [b.offset, b.size, float(b.eta).hex(), float(b.beta).hex(), float(b.phi).hex()]
+                for b in prep.blocks
+            ],
+            "d": _hex(prep.d),
+        }
+    text = json.dumps(doc, indent=1, sort_keys=True)
+    for path in (os.path.join(GOLD, "tableaux.json"),
+                 os.path.join(ROOT, "paper_2101_01776_b200", "data", "tableaux.json")):
+        with open(path, "w") as fh:
+            fh.write(text)
+    print("tableaux:", len(doc))
+
+
+def _cfg(solver):
+    inner = solver.get("inner", 4)
+    return SolverConfig(
+        variant=solver.get("variant", 3),
+        newton_rtol=solver.get("newton_rtol", 1e-9),
+        newton_maxit=solver.get("newton_maxit", 30),
+        krylov_rtol=solver.get("krylov_rtol", 1e-5),
+        krylov_maxit=solver.get("krylov_maxit", 200),
+        restart=solver.get("restart", 200),
+        precond=PrecondSpec(gamma_mode=solver.get("gamma_mode", "star"), inner=inner),
+    )
+
+
+def run_case(name, prob: GridProblem, u0, family, s, dt, nsteps, solver):
+    pd = build_problem(prob.kind, prob.shape, **prob.oracle_params())
+    sysr = pd.as_ode_system(OdeSystem, SparseMatrix)
+    tab = irkit.make_tableau(family, s)
+    tic = time.time()
+    res = integrate(sysr, u0, 0.0, nsteps * dt, dt, tab, _cfg(solver))
+    wall = time.time() - tic
+    steps = []
+    for st in res.step_stats:
+        steps.append(
+            {
+                "newton_iterations": st.newton_iterations,
+                "krylov_iterations": st.krylov_iterations,
+                "precond_applications": st.precond_applications,
+                "jacobian_assemblies": st.jacobian_assemblies,
+                "block_iterations": {str(k): v for k, v in st.block_iterations.items()},
+                "residual_history": [float(x).hex() for x in st.residual_history],
+            }
+        )
+    meta = {
+        "name": name,
+        "kind": prob.kind,
+        "shape": list(prob.shape),
+        "params": {"nu": prob.nu, "c": prob.c, "lam": prob.lam, "mu": prob.mu, "length": prob.length},
+        "family": family,
+        "s": s,
+        "dt": dt,
+        "nsteps": nsteps,
+        "solver": solver,
+        "steps": steps,
+        "reference_wall_s": wall,
+    }
+    np.savez_compressed(os.path.join(GOLD, name + ".npz"), u0=u0, u_final=res.u_final)
+    with open(os.path.join(GOLD, name + ".json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+    print(f"{name}: {wall:.1f}s newton={[x['newton_iterations'] for x in steps]} "
+          f"krylov={[x['krylov_iterations'] for x in steps]}")
+
+
+def run_configs():
+    # config 0 at full size, both inner modes
+    sp0 = baseline_config(0)
+    run_case("cfg0_full", sp0.problem, sp0.u0(), "gauss", 2, sp0.dt, sp0.nsteps, sp0.solver)
+    run_case("cfg0_full_exact", sp0.problem, sp0.u0(), "gauss", 2, sp0.dt, sp0.nsteps,
+             dict(sp0.solver, inner="exact"))
+    # config 1 (Burgers, Gauss(3)) at reduced grids
+    for n, ns in ((64, 20), (128, 3)):
+        sp1 = baseline_config(1, n=n, nsteps=ns)
+        run_case(f"cfg1_n{n}", sp1.problem, sp1.u0(), "gauss", 3, sp1.dt, ns, sp1.solver)
+    # config 2 (nldiff 4096^2 field) reduced: Gauss(2) and Radau IIA(3)
+    for fam, s in (("gauss", 2), ("radau_iia", 3)):
+        sp2 = baseline_config(2, n=128, nsteps=2)
+        run_case(f"cfg2_{fam}{s}_n128", sp2.problem, sp2.u0(), fam, s, sp2.dt, 2, sp2.solver)
+    # config 3 (3-D, Gauss(5)) reduced
+    sp3 = baseline_config(3, n=16, nsteps=2)
+    run_case("cfg3_n16", sp3.problem, sp3.u0(), "gauss", 5, sp3.dt, 2, sp3.solver)
+    # variants 0..3 on a nonlinear problem with several tableaux
+    prob = GridProblem("burgers", (24, 24), nu=1e-2)
+    u0 = fourier_u0(prob.shape, 1, 4, 0.5, seed=3)
+    for fam, s in (("gauss", 3), ("radau_iia", 3), ("lobatto_iiic", 4), ("gauss", 4), ("radau_iia", 2)):
+        for v in range(4):
+            run_case(f"var_{fam}{s}_v{v}", prob, u0, fam, s, 2e-3, 2,
+                     dict(variant=v, inner=4, krylov_maxit=2000, restart=200))
+    # reaction-advection-diffusion (rad kind): logistic-KPP in 1-D and 2-D
+    prob = GridProblem("rad", (64,), nu=1e-3, c=0.5, lam=1.0, mu=-1.0)
+    u0 = 0.5 + fourier_u0(prob.shape, 1, 3, 0.1, seed=7)
+    run_case("rad1d_kpp", prob, u0, "gauss", 2, 0.05, 4, dict(variant=3, inner=4, krylov_rtol=1e-8))
+    prob = GridProblem("rad", (32, 32), nu=1e-2, c=0.3, lam=-0.5, mu=0.0)
+    u0 = fourier_u0(prob.shape, 1, 4, 0.2, seed=8)
+    run_case("rad2d_linear", prob, u0, "radau_iia", 3, 0.01, 3, dict(variant=3, inner=4))
+
+
+def run_transformed():
+    """solve_transformed_system on advdiff-type linear stencils (every variant),
+    mirroring tests/test_irk_core.py:152-167 of the reference."""
+    out = []
+    prob = GridProblem("rad", (24,), nu=0.01, c=1.0)
+    pd = build_problem(prob.kind, prob.shape, **prob.oracle_params())
+    lmat = SparseMatrix(pd.linearize_csr(np.zeros(24), 0.0), bandwidth=1)
+    for fam, s in (("gauss", 3), ("radau_iia", 3), ("lobatto_iiic", 4), ("gauss", 4)):
+        prep = irkit.prepare_stages(irkit.make_tableau(fam, s))
+        rng = np.random.default_rng(s)
+        rhs = rng.standard_normal((s, 24))
+        for variant in range(4):
+            for inner in ("exact", 4):
+                k, stats = solve_transformed_system(
+                    prep, [lmat] * s, variant, 0.05, rhs,
+                    precond=PrecondSpec(inner=inner),
+                    krylov_rtol=1e-12, krylov_maxit=400,
+                )
+                out.append({
+                    "family": fam, "s": s, "variant": variant, "inner": inner,
+                    "seed": s, "dt": 0.05,
+                    "reports": [[off, rep.iterations] for off, rep in stats.reports],
+                    "k": _hex(k),
+                })
+    with open(os.path.join(GOLD, "transformed.json"), "w") as fh:
+        json.dump(out, fh)
+    print("transformed cases:", len(out))
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["tableaux", "transformed", "configs"]
+    if "tableaux" in which:
+        dump_tableaux()
+    if "transformed" in which:
+        run_transformed()
+    if "configs" in which:
+        run_configs()
