@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libirkg.so")
-SOURCES = ["kernels.cu", "engine.cu"]
+SOURCES = ["kernels.cu", "cgs.cu", "stencil.cu", "engine.cu"]
 HEADERS = ["kinds.cuh", "kernels.cuh", "engine.h", os.path.join("..", "..", "include", "irkg.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -23,14 +23,31 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-re
          "-Xptxas", "-v"]
 
 
-def _stale():
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
+HASH_FILE = LIB + ".srchash"
+
+
+def source_hash():
+    """Content hash of the CUDA sources + build flags (mtime-free, so it
+    survives the repo snapshot to the GPU box)."""
+    import hashlib
+
+    h = hashlib.sha256()
     for f in SOURCES + HEADERS:
-        if os.path.getmtime(os.path.join(CSRC, f)) > t:
-            return True
-    return False
+        with open(os.path.join(CSRC, f), "rb") as fh:
+            h.update(fh.read())
+    h.update(" ".join(ARCH + FLAGS).encode())
+    return h.hexdigest()
+
+
+def is_fresh():
+    if not os.path.exists(LIB) or not os.path.exists(HASH_FILE):
+        return False
+    with open(HASH_FILE) as fh:
+        return fh.read().strip() == source_hash()
+
+
+def _stale():
+    return not is_fresh()
 
 
 def build(force=False, verbose=False):
@@ -54,6 +71,8 @@ def build(force=False, verbose=False):
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed")
     os.replace(tmp, LIB)
+    with open(HASH_FILE, "w") as fh:
+        fh.write(source_hash())
     return LIB
 
 

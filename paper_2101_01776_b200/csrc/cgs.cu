@@ -1,0 +1,338 @@
+// cgs.cu -- fused classical Gram-Schmidt sweeps (CGS2) + Arnoldi finish.
+//
+// Replaces the reference's orthogonalisation (src/sparsela.py:222-233):
+//     wnorm0 = ||w||; 2x { coef = V^T w ; w -= V coef ; h += coef }; h_{j+1,j} = ||w||
+// as three sweeps over the basis instead of four:
+//     DOT       c1 = V^T w, ||w||^2
+//     UPD_DOT   w1 = w - V c1 (written back), c2 = V^T w1      (V tile read once)
+//     UPD_NORM  s_{j+1} = w1 - V c2, ||s_{j+1}||^2; last CTA finishes the column
+// Each CTA streams row tiles of all (j+1) basis slots + w into shared memory
+// with 1-D TMA bulk copies (cp.async.bulk + mbarrier, 2-stage pipeline): one
+// thread issues the copies, HBM sees long contiguous bursts, and the tile is
+// read once from HBM for both the update and the dots.  Per-CTA partials are
+// folded by the last CTA in fixed order (deterministic, no fp atomics).
+#include <cstdint>
+
+#include "engine.h"
+
+namespace irkg {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace
+
+// Finish Arnoldi column j (src/sparsela.py:227-256); single thread.
+__device__ void arnoldi_finish_dev(GWork W) {
+  GCtrl *c = W.ctrl;
+  const int j = c->j;
+  double *h = W.H + (size_t)j * (MAXR + 1);
+  for (int i = 0; i <= j; ++i) h[i] = (0.0 + W.c1[i]) + W.c2[i];
+  const double hj = sqrt(c->hn2);
+  const double wnorm0 = sqrt(c->wn2);
+  h[j + 1] = hj;
+  const bool breakdown = hj <= 1e-14 * fmax(wnorm0, 1e-300);
+  if (!breakdown) W.alpha[j + 1] = 1.0 / hj;
+  for (int i = 0; i < j; ++i) {
+    double tmp = W.cs[i] * h[i] + W.sn[i] * h[i + 1];
+    h[i + 1] = -W.sn[i] * h[i] + W.cs[i] * h[i + 1];
+    h[i] = tmp;
+  }
+  const double denom = hypot(h[j], h[j + 1]);
+  if (denom == 0.0) {  // dead column (src/sparsela.py:239-246)
+    c->breakdown = 1;
+    c->total_it += 1;
+    W.res[c->n_res] = W.res[c->n_res - 1];
+    c->n_res += 1;
+    c->k = j;
+    c->cycle_done = 1;
+    return;
+  }
+  W.cs[j] = h[j] / denom;
+  W.sn[j] = h[j + 1] / denom;
+  h[j] = denom;
+  h[j + 1] = 0.0;
+  W.g[j + 1] = -W.sn[j] * W.g[j];
+  W.g[j] = W.cs[j] * W.g[j];
+  c->total_it += 1;
+  const double est = fabs(W.g[j + 1]) / c->bnorm;
+  W.res[c->n_res] = est;
+  c->n_res += 1;
+  if (breakdown) c->breakdown = 1;
+  if (est <= c->rtol || breakdown || c->total_it >= c->maxit || j + 1 >= c->m) {
+    c->k = j + 1;
+    c->cycle_done = 1;
+  } else {
+    c->j = j + 1;
+  }
+}
+
+constexpr int CGS_BS = 256;
+constexpr int CGS_NW = CGS_BS / 32;
+
+enum { CGS_DOT = 0, CGS_UPD_DOT = 1, CGS_UPD_NORM = 2 };
+
+// Stage layout: (L+1) x TR doubles; rows [0, L) are basis slots, row L is w.
+template <int MODE>
+__global__ void __launch_bounds__(CGS_BS, 2)
+    k_cgs(int n, double *__restrict__ V, long long pitch, GWork W, const double *cin,
+          const double *win, double *wout, double *part, int G, unsigned *counter,
+          int stage_doubles, int use_cond, cudaGraphConditionalHandle cond) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ double cs[MAXR + 1];
+  __shared__ double dacc[MAXR + 2];
+  __shared__ double red[CGS_BS];
+  __shared__ bool is_last;
+
+  GCtrl *ctrl = W.ctrl;
+  if (ctrl->cycle_done) {
+    // inside the graph WHILE body: make sure the loop terminates
+    if (MODE == CGS_UPD_NORM && use_cond && blockIdx.x == 0 && threadIdx.x == 0)
+      cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const int L = ctrl->j + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double *out = (MODE == CGS_UPD_NORM) ? V + (size_t)L * pitch : wout;
+  // tile rows: largest power of two with (L+1)*TR <= stage, within [32, 1024]
+  int TR = 1024;
+  while (TR > 32 && (L + 1) * TR > stage_doubles) TR >>= 1;
+  const int ntiles = (n + TR - 1) / TR;
+  double *stage0 = sm, *stage1 = sm + stage_doubles;
+  const int nd = (MODE == CGS_DOT) ? L + 1 : L;  // dot entries (DOT: + ||w||^2)
+
+  for (int l = tid; l < L; l += CGS_BS) {
+    if (MODE != CGS_DOT) cs[l] = W.alpha[l] * cin[l];
+  }
+  for (int l = tid; l < nd; l += CGS_BS) dacc[l] = 0.0;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto tile_full = [&](int t) { return (long long)(t + 1) * TR <= (long long)n; };
+  auto issue = [&](int t, int s) {  // single thread
+    const int r0 = t * TR;
+    const uint32_t bytes = TR * 8u;
+    uint64_t *bar = &bars[s];
+    mbar_expect_tx(bar, bytes * (uint32_t)(L + 1));
+    double *dst = s ? stage1 : stage0;
+    for (int l = 0; l < L; ++l) tma_load_1d(dst + l * TR, V + (size_t)l * pitch + r0, bytes, bar);
+    tma_load_1d(dst + L * TR, win + r0, bytes, bar);
+  };
+
+  const int t0 = blockIdx.x;
+  if (tid == 0) {
+    if (t0 < ntiles && tile_full(t0)) issue(t0, 0);
+    if (t0 + G < ntiles && tile_full(t0 + G)) issue(t0 + G, 1);
+  }
+
+  double nrm = 0.0;
+  const int rpp = TR < CGS_BS ? TR : CGS_BS;  // rows per pass in phase A
+  const int parts = CGS_BS / rpp;
+
+  int it = 0;
+  for (int t = t0; t < ntiles; t += G, ++it) {
+    const int s = it & 1;
+    const int r0 = t * TR;
+    const int rows = min(TR, n - r0);
+    double *buf = s ? stage1 : stage0;
+    if (tile_full(t)) {
+      while (!mbar_try_wait(&bars[s], (uint32_t)((it >> 1) & 1))) {
+      }
+    } else {  // partial tail tile (only the globally last one): generic loads
+      for (int l = 0; l <= L; ++l) {
+        const double *src = (l < L) ? V + (size_t)l * pitch + r0 : win + r0;
+        for (int r = tid; r < TR; r += CGS_BS) buf[l * TR + r] = (r < rows) ? src[r] : 0.0;
+      }
+      __syncthreads();
+    }
+    double *wt = buf + L * TR;
+    if (MODE != CGS_DOT) {
+      // phase A: w1 = w - sum_l s_l cs_l on this tile
+      const int pid = tid / rpp, rl = tid % rpp;
+      for (int rb = 0; rb < TR; rb += rpp) {
+        const int r = rb + rl;
+        double sum = 0.0;
+        for (int l = pid; l < L; l += parts) sum += buf[l * TR + r] * cs[l];
+        if (parts > 1) {
+          red[tid] = sum;
+          __syncthreads();
+          if (pid == 0) {
+            double tot = 0.0;
+            for (int p = 0; p < parts; ++p) tot += red[p * rpp + rl];
+            sum = tot;
+          }
+        }
+        if (pid == 0) {
+          double v = wt[r] - sum;
+          if (r < rows) {
+            if (MODE == CGS_UPD_NORM) nrm += v * v;
+            out[r0 + r] = v;
+          } else {
+            v = 0.0;
+          }
+          wt[r] = v;
+        }
+        if (parts > 1) __syncthreads();
+      }
+      __syncthreads();
+    }
+    if (MODE != CGS_UPD_NORM) {
+      // phase B: one warp per basis slot, lanes over rows, per-CTA sums in smem
+      for (int l = warp; l < nd; l += CGS_NW) {
+        const double *vl = buf + l * TR;
+        double a0 = 0.0, a1 = 0.0;
+        int r = lane;
+        for (; r + 32 < TR; r += 64) {
+          a0 += vl[r] * wt[r];
+          a1 += vl[r + 32] * wt[r + 32];
+        }
+        if (r < TR) a0 += vl[r] * wt[r];
+        double a = wsum(a0 + a1);
+        if (lane == 0) dacc[l] += a;
+      }
+    }
+    __syncthreads();  // stage s consumed
+    if (tid == 0) {
+      const int tn = t + 2 * G;
+      if (tn < ntiles && tile_full(tn)) {
+        fence_proxy_async();
+        issue(tn, s);
+      }
+    }
+  }
+
+  // per-CTA partials -> part[l * G + cta]
+  if (MODE != CGS_UPD_NORM) {
+    for (int l = tid; l < nd; l += CGS_BS) part[(size_t)l * G + blockIdx.x] = dacc[l];
+  } else {
+    double v = wsum(nrm);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < CGS_NW; ++w) tot += red[w];
+      part[blockIdx.x] = tot;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) is_last = (atomicAdd(counter, 1u) == (unsigned)(G - 1));
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  const int nfold = (MODE == CGS_UPD_NORM) ? 1 : nd;
+  for (int l = warp; l < nfold; l += CGS_NW) {
+    const double *pl = part + (size_t)l * G;
+    double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;
+    int c = lane;
+    for (; c + 96 < G; c += 128) {
+      f0 += __ldcg(pl + c);
+      f1 += __ldcg(pl + c + 32);
+      f2 += __ldcg(pl + c + 64);
+      f3 += __ldcg(pl + c + 96);
+    }
+    for (; c < G; c += 32) f0 += __ldcg(pl + c);
+    double v = wsum((f0 + f1) + (f2 + f3));
+    if (lane == 0) {
+      if (MODE == CGS_DOT) {
+        if (l == L)
+          ctrl->wn2 = v;
+        else
+          W.c1[l] = W.alpha[l] * v;
+      } else if (MODE == CGS_UPD_DOT) {
+        W.c2[l] = W.alpha[l] * v;
+      } else {
+        ctrl->hn2 = v;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (MODE == CGS_UPD_NORM) {
+      __threadfence();
+      arnoldi_finish_dev(W);
+      if (use_cond) cudaGraphSetConditional(cond, ctrl->cycle_done ? 0u : 1u);
+    }
+    *counter = 0u;
+  }
+}
+
+int Engine::cgs_stage_doubles() const {
+  int st = (vcap + 2) * 32;
+  return st < 6144 ? 6144 : st;
+}
+
+// One Arnoldi orthogonalisation: 3 fused sweeps; the last also finishes the
+// Hessenberg column (Givens, estimate, exit test) in its final CTA.
+void Engine::cgs(long long n) {
+  const int stage = cgs_stage_doubles();
+  const size_t smem = 2 * (size_t)stage * sizeof(double);
+  if (cgs_smem_set < smem) {
+    check(cudaFuncSetAttribute(k_cgs<CGS_DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem), "smem attr");
+    check(cudaFuncSetAttribute(k_cgs<CGS_UPD_DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem), "smem attr");
+    check(cudaFuncSetAttribute(k_cgs<CGS_UPD_NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem), "smem attr");
+    cgs_smem_set = smem;
+  }
+  const int uc = cond_active ? 1 : 0;
+  k_cgs<CGS_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, nullptr, wbuf, nullptr, part,
+                                              G, counter, stage, 0, cond_handle);
+  k_cgs<CGS_UPD_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c1, wbuf, wbuf, part, G,
+                                                  counter, stage, 0, cond_handle);
+  k_cgs<CGS_UPD_NORM><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c2, wbuf, nullptr,
+                                                   part, G, counter, stage, uc, cond_handle);
+  count(3);
+}
+
+}  // namespace irkg

@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -84,6 +85,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st) : prob(p), devic
   dalloc(&ufield, N);
   check(cudaEventCreate(&ev0), "event");
   check(cudaEventCreate(&ev1), "event");
+  if (const char *e = getenv("IRKG_GRAPHS")) use_graphs = (atoi(e) != 0);
   for (int i = 0; i < MAXS; ++i)
     for (int j = 0; j < MAXS; ++j) od_slot[i][j] = -1;
 }
@@ -98,6 +100,8 @@ Engine::~Engine() {
   if (ctrl_host) cudaFreeHost(ctrl_host);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
+  drop_graphs();
+  if (cap_stream) cudaStreamDestroy(cap_stream);
 }
 
 void Engine::ensure_stage_buffers() {
@@ -111,9 +115,10 @@ void Engine::ensure_stage_buffers() {
 }
 
 void Engine::ensure_basis(int restart) {
-  if (restart > MAXR) throw SolveError(IRKG_ERR_CONFIG, "restart exceeds MAXR=512");
+  if (restart > MAXR) throw SolveError(IRKG_ERR_CONFIG, "restart exceeds MAXR=256");
   if (V && restart <= vcap) return;
   vpitch = ((2 * N + 31) / 32) * 32;
+  drop_graphs();  // graphs bake the basis pointer in
   dalloc(&V, (size_t)(restart + 1) * vpitch);
   vcap = restart;
 }
@@ -152,6 +157,80 @@ void Engine::ensure_res(int maxit) {
 void Engine::read_ctrl() {
   check(cudaMemcpyAsync(ctrl_host, ctrl_dev, sizeof(GCtrl), cudaMemcpyDeviceToHost, stream));
   check(cudaStreamSynchronize(stream), "sync");
+}
+
+// One Arnoldi step: z = M^{-1} v_j, w = A z, CGS2 + column finish.
+void Engine::arnoldi_iteration(const BlockSpec &B, long long n) {
+  VecIn vslot{V, vpitch, ctrl_dev, W.alpha};
+  precond(B, &vslot, zbuf, ctrl_dev);
+  block_op(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev);
+  cgs(n);
+}
+
+void Engine::drop_graphs() {
+  for (auto &kv : graphs) {
+    if (kv.second.ex) cudaGraphExecDestroy(kv.second.ex);
+    if (kv.second.g) cudaGraphDestroy(kv.second.g);
+  }
+  graphs.clear();
+}
+
+// Graph of one restart cycle: WHILE(cond) { Arnoldi step }.  Kernel
+// arguments are fixed per block system (pointers, eta/beta/phi/gamma/dt,
+// operator fields); the Arnoldi index and exit state live in the device
+// control block, so the same executable serves every cycle and Newton
+// iteration of that block.
+Engine::CycleGraph &Engine::cycle_graph(const BlockSpec &B, long long n) {
+  char key[512];
+  snprintf(key, sizeof key, "%d|%a|%a|%a|%a|%a|%d|%p|%a|%d|%p|%a|%d|%p|%a|%d|%p|%a|%d|%lld|%p|%d",
+           B.size, B.eta, B.beta, B.phi, B.gamma, B.dt, B.inner, (const void *)B.l1.a, B.l1.sigma,
+           B.l1.present, (const void *)B.l2.a, B.l2.sigma, B.l2.present, (const void *)B.c12.a,
+           B.c12.sigma, B.c12.present, (const void *)B.c21.a, B.c21.sigma, B.c21.present, n,
+           (void *)V, vcap);
+  auto it = graphs.find(key);
+  if (it != graphs.end()) return it->second;
+  if (graphs.size() > 64) drop_graphs();
+  if (!cap_stream) check(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking), "stream");
+  check(cudaStreamSynchronize(stream), "sync");
+  CycleGraph cg;
+  check(cudaGraphCreate(&cg.g, 0), "cudaGraphCreate");
+  check(cudaGraphConditionalHandleCreate(&cg.h, cg.g, 1, cudaGraphCondAssignDefault), "cond handle");
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = cg.h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  check(cudaGraphAddNode(&node, cg.g, nullptr, 0, &np), "cond node");
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  cudaStream_t saved = stream;
+  stream = cap_stream;
+  const long long launches0 = counters.kernel_launches;
+  const double pb = counters.precond_bytes, ob = counters.op_bytes;
+  check(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeRelaxed), "capture");
+  cond_active = true;
+  cond_handle = cg.h;
+  try {
+    arnoldi_iteration(B, n);
+  } catch (...) {
+    cond_active = false;
+    stream = saved;
+    cudaGraph_t tmp;
+    cudaStreamEndCapture(cap_stream, &tmp);
+    throw;
+  }
+  cond_active = false;
+  cudaGraph_t captured;
+  check(cudaStreamEndCapture(cap_stream, &captured), "end capture");
+  stream = saved;
+  cg.body_kernels = (int)(counters.kernel_launches - launches0);
+  counters.kernel_launches = launches0;
+  counters.precond_bytes = pb;
+  counters.op_bytes = ob;
+  check(cudaGraphInstantiate(&cg.ex, cg.g, 0), "cudaGraphInstantiate");
+  auto res = graphs.emplace(key, cg);
+  return res.first->second;
 }
 
 double Engine::gamma_of(double eta, double beta) const {
@@ -200,32 +279,41 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
   while (!converged && total_it < maxit) {
     int m = std::min(restart, maxit - total_it);
     cycle_init(m);
-    for (int it = 0; it < m; ++it) {
-      precond(B, &vslot, zbuf, ctrl_dev);                           // z = M^{-1} v_j
-      block_op(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev);          // w = A z
-      if (timing) check(cudaEventRecord(ev0, stream));
-      mdot(n, wbuf, W.c1, &ctrl_dev->wn2);                          // CGS pass 1 dots + ||w||
-      mupdate(n, W.c1, wbuf, wbuf, false, nullptr);                 // w -= V c1
-      mdot(n, wbuf, W.c2, nullptr);                                 // CGS pass 2 dots
-      mupdate(n, W.c2, wbuf, nullptr, true, &ctrl_dev->hn2);        // s_{j+1} = w - V c2
-      if (timing) check(cudaEventRecord(ev1, stream));
-      counters.cgs_launches += 4;
-      arnoldi_finish();
-      counters.arnoldi_iterations += 1;
+    if (use_graphs && !timing) {
+      // whole Arnoldi loop of this cycle as one graph launch (device-side WHILE)
+      CycleGraph &cg = cycle_graph(B, n);
+      check(cudaGraphLaunch(cg.ex, stream), "cudaGraphLaunch");
       read_ctrl();
-      if (timing) {
-        float ms = 0.f;
-        check(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
-        counters.cgs_time_ms += ms;
+      const int its = ctrl_host->j + 1;
+      counters.kernel_launches += (long long)cg.body_kernels * its;
+      counters.cgs_launches += 3LL * its;
+      counters.arnoldi_iterations += its;
+    } else {
+      for (int it = 0; it < m; ++it) {
+        precond(B, &vslot, zbuf, ctrl_dev);                           // z = M^{-1} v_j
+        block_op(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev);          // w = A z
+        if (timing) check(cudaEventRecord(ev0, stream));
+        cgs(n);  // CGS2 in 3 fused sweeps + Hessenberg column / Givens / exit test
+        if (timing) check(cudaEventRecord(ev1, stream));
+        counters.cgs_launches += 3;
+        counters.arnoldi_iterations += 1;
+        read_ctrl();
+        if (timing) {
+          float ms = 0.f;
+          check(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
+          counters.cgs_time_ms += ms;
+        }
+        if (ctrl_host->cycle_done) break;
       }
-      if (ctrl_host->cycle_done) break;
     }
     {
       // algorithmic CGS2 bytes of this cycle: per iteration j, 4 sweeps over
       // (j+1) basis vectors + w traffic (2 reads, 1 rmw, 1 read + 1 write)
       double its = (double)(ctrl_host->j + 1);
       double sumj1 = its * (its + 1.0) / 2.0;  // sum_{j=0}^{its-1} (j+1)
-      counters.cgs_bytes += 8.0 * (double)n * (4.0 * sumj1 + 6.0 * its);
+      // 3 sweeps: DOT reads (j+1)+1 vectors, UPD_DOT reads (j+1)+1 and writes 1,
+      // UPD_NORM reads (j+1)+1 and writes 1  ->  3(j+1) + 5 passes of n doubles
+      counters.cgs_bytes += 8.0 * (double)n * (3.0 * sumj1 + 5.0 * its);
     }
     // cycle end: x += M^{-1} (V (alpha .* y)); r = b - A x (src/sparsela.py:258-272)
     backsolve();

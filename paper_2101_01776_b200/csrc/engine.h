@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -102,9 +103,39 @@ struct Engine {
   void ensure_basis(int restart);
   void ensure_res(int maxit);
   int rescap = 0;
+  size_t cgs_smem_set = 0;
+  // CUDA-graph execution of the Arnoldi loop: one graph per block system,
+  // a WHILE conditional node whose condition the last CGS kernel clears.
+  struct CycleGraph {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ex = nullptr;
+    cudaGraphConditionalHandle h{};
+    int body_kernels = 0;
+  };
+  std::map<std::string, CycleGraph> graphs;
+  bool use_graphs = true;
+  bool cond_active = false;
+  cudaGraphConditionalHandle cond_handle{};
+  cudaStream_t cap_stream = nullptr;
+  CycleGraph &cycle_graph(const BlockSpec &B, long long n);
+  void arnoldi_iteration(const BlockSpec &B, long long n);
+  void drop_graphs();
+  int cgs_stage_doubles() const;
+  void cgs(long long n);  // cgs.cu
+  // stencil.cu (register-sliding 2-D / 3-D kernels)
+  dim3 slide_grid(int &span) const;
+  void jac_sweep_s(const Op &L, double alpha, double dt, const VecIn &vin, int in_off,
+                   const double *t_in, const double *x, double *x_out, const GCtrl *skip);
+  void block_op_s(const BlockSpec &B, const double *z, double *w, const double *b,
+                  double *out_norm, const GCtrl *skip);
+  double residual_s(const double *U, const double *K, double *F);
 
   // launch helpers (kernels.cu)
   int grid_for(long long n) const;
+  int row_grid() const {  // CTAs of row-structured stencil kernels
+    int rows = grid.ny * grid.nz;
+    return rows < sms * 8 ? rows : sms * 8;
+  }
   void count(int k);
   double norm2(const double *x, long long n, const GCtrl *skip = nullptr);
   void stage_values(const double *u, const double *K, double dt, double *U);

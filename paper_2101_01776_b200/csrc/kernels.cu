@@ -103,12 +103,18 @@ __global__ void k_residual(Grid g, KindParams kp, int s, const double *__restric
                            int G, double *out, unsigned *counter) {
   __shared__ double sm[32];
   const int n = g.n;
+  const int nrows = g.ny * g.nz;
   double acc = 0.0;
-  for (int p = blockIdx.x * BS + threadIdx.x; p < n; p += G * BS) {
-    for (int i = 0; i < s; ++i) {
-      double f = rhs_at<KIND, NDIM>(g, kp, U + (size_t)i * n, p) - K[(size_t)i * n + p];
-      F[(size_t)i * n + p] = f;
-      acc += f * f;
+  for (int row = blockIdx.x; row < nrows; row += G) {
+    const RowCtx rc = row_ctx<NDIM>(g, row);
+    for (int ix = threadIdx.x; ix < g.nx; ix += BS) {
+      int nb[6];
+      const int p = row_neighbours<NDIM>(g, rc, ix, nb);
+      for (int i = 0; i < s; ++i) {
+        double f = rhs_at<KIND, NDIM>(g, kp, U + (size_t)i * n, p, nb) - K[(size_t)i * n + p];
+        F[(size_t)i * n + p] = f;
+        acc += f * f;
+      }
     }
   }
   acc = block_sum<BS>(acc, sm);
@@ -191,9 +197,11 @@ __global__ void k_backsub(Grid g, KindParams kp, double dt, BacksubTerms T,
                           const double *__restrict__ gst, const double *__restrict__ y,
                           double *__restrict__ rhs) {
   const int n = g.n;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+  const int nrows = g.ny * g.nz;
+  for (int row = blockIdx.x; row < nrows; row += gridDim.x)
+  for (int ix = threadIdx.x; ix < g.nx; ix += blockDim.x) {
     int nb[6];
-    neighbours<NDIM>(g, p, nb);
+    const int p = row_neighbours<NDIM>(g, row_ctx<NDIM>(g, row), ix, nb);
     for (int r = 0; r < T.rows; ++r) {
       double acc = gst[(size_t)(T.row0 + r) * n + p];
       for (int q = 0; q < T.njs; ++q) {
@@ -259,15 +267,18 @@ __global__ void k_jac_sweep(Grid g, KindParams kp, Op L, double alpha, double dt
     resolve_in(vin, in, scale);
     in += in_off;
   }
-  const int n = g.n;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+  const int nrows = g.ny * g.nz;
+  for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const RowCtx rc = row_ctx<NDIM>(g, row);
+    for (int ix = threadIdx.x; ix < g.nx; ix += blockDim.x) {
     int nb[6];
-    neighbours<NDIM>(g, p, nb);
+    const int p = row_neighbours<NDIM>(g, rc, ix, nb);
     double r = t_in ? t_in[p] : scale * in[p];
     double xp = x[p];
     double sx = alpha * xp - dt * lx_at<KIND, NDIM>(g, kp, L.a, L.sigma, x, p, nb);
     double D = alpha - dt * ldiag_at<KIND>(g, kp, L.a, L.sigma, p);
     x_out[p] = xp + OMEGA * ((1.0 / D) * (r - sx));
+    }
   }
 }
 
@@ -283,9 +294,11 @@ __global__ void k_block_op(Grid g, KindParams kp, double eta, double beta, doubl
   if (skip && skip->cycle_done) return;
   const int n = g.n;
   double nrm = 0.0;
-  for (int p = blockIdx.x * BS + threadIdx.x; p < n; p += G * BS) {
+  const int nrows = g.ny * g.nz;
+  for (int row = blockIdx.x; row < nrows; row += G)
+  for (int ix = threadIdx.x; ix < g.nx; ix += BS) {
     int nb[6];
-    neighbours<NDIM>(g, p, nb);
+    const int p = row_neighbours<NDIM>(g, row_ctx<NDIM>(g, row), ix, nb);
     if (SIZE == 1) {
       double v = eta * z[p] - dt * lx_at<KIND, NDIM>(g, kp, l1.a, l1.sigma, z, p, nb);
       if (b) {
@@ -575,6 +588,7 @@ void Engine::stage_values(const double *u, const double *K, double dt, double *U
 }
 
 double Engine::residual(const double *U, const double *K, double *F) {
+  if (ndim >= 2) return residual_s(U, K, F);
   dispatch_kd(prob.kind, ndim, [&](auto KD, auto ND) {
     k_residual<decltype(KD)::value, decltype(ND)::value, 256>
         <<<G, 256, 0, stream>>>(grid, kp, s, U, K, F, part, G, &scal_dev[0], counter);
@@ -614,7 +628,7 @@ void Engine::backsub(double dt, const BacksubTerms &T, const double *gst, const 
                      double *rhs) {
   dispatch_kd(prob.kind, ndim, [&](auto KD, auto ND) {
     k_backsub<decltype(KD)::value, decltype(ND)::value>
-        <<<grid_for(N), 256, 0, stream>>>(grid, kp, dt, T, gst, y, rhs);
+        <<<row_grid(), 256, 0, stream>>>(grid, kp, dt, T, gst, y, rhs);
   });
   count(1);
 }
@@ -637,9 +651,13 @@ void Engine::jacobi_chain(const Op &L, double alpha, double dt, int inner, const
   for (int i = 2; i <= inner; ++i) {
     const double *xin = dst(i - 1);
     double *xo = dst(i);
+    if (ndim >= 2) {
+      jac_sweep_s(L, alpha, dt, vin, in_off, tbuf, xin, xo, skip);
+      continue;
+    }
     dispatch_kd(prob.kind, ndim, [&](auto KD, auto ND) {
       k_jac_sweep<decltype(KD)::value, decltype(ND)::value>
-          <<<gb, 256, 0, stream>>>(grid, kp, L, alpha, dt, vin, in_off, tbuf, xin, xo, skip);
+          <<<row_grid(), 256, 0, stream>>>(grid, kp, L, alpha, dt, vin, in_off, tbuf, xin, xo, skip);
     });
     count(1);
   }
@@ -658,6 +676,11 @@ void Engine::precond(const BlockSpec &B, const void *vin_p, double *z, const GCt
 
 void Engine::block_op(const BlockSpec &B, const double *z, double *w, const double *b,
                       double *out_norm, const GCtrl *skip) {
+  counters.op_bytes += 8.0 * N * B.size * 3.0;
+  if (ndim >= 2) {
+    block_op_s(B, z, w, b, out_norm, skip);
+    return;
+  }
   dispatch_kd(prob.kind, ndim, [&](auto KD, auto ND) {
     constexpr int K_ = decltype(KD)::value, D_ = decltype(ND)::value;
     if (B.size == 1)
@@ -670,7 +693,6 @@ void Engine::block_op(const BlockSpec &B, const double *z, double *w, const doub
                                                          G, out_norm, counter, skip);
   });
   count(1);
-  counters.op_bytes += 8.0 * N * B.size * 3.0;
 }
 
 void Engine::mdot(long long n, const double *w, double *out_c, double *out_norm) {

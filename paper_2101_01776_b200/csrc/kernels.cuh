@@ -18,7 +18,7 @@
 namespace irkg {
 
 constexpr int MAXS = 8;       // max stages
-constexpr int MAXR = 512;     // max restart length
+constexpr int MAXR = 256;     // max restart length
 constexpr int MAXOPS = 48;    // max operator fields per linearisation
 constexpr double OMEGA = 2.0 / 3.0;  // damped-Jacobi weight, src/irk_core.py:123
 

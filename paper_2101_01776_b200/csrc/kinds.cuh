@@ -38,6 +38,45 @@ struct KindParams {
   double nu, c, lam, mu;
 };
 
+// Row-structured traversal: a "row" is one x-line (fixed iy, iz).  Kernels
+// loop rows across CTAs and x across threads, so the periodic neighbour
+// offsets are computed once per row (no per-element integer division).
+struct RowCtx {
+  int base;      // row * nx
+  int dym, dyp;  // element offsets to the y-neighbour rows
+  int dzm, dzp;  // element offsets to the z-neighbour planes
+};
+
+template <int NDIM>
+__device__ __forceinline__ RowCtx row_ctx(const Grid &g, int row) {
+  RowCtx rc;
+  rc.base = row * g.nx;
+  rc.dym = rc.dyp = rc.dzm = rc.dzp = 0;
+  if (NDIM >= 2) {
+    const int iy = (NDIM == 3) ? row % g.ny : row;
+    rc.dym = (iy == 0) ? (g.ny - 1) * g.nx : -g.nx;
+    rc.dyp = (iy == g.ny - 1) ? -(g.ny - 1) * g.nx : g.nx;
+    if (NDIM == 3) {
+      const int iz = row / g.ny;
+      rc.dzm = (iz == 0) ? (g.nz - 1) * g.nxy : -g.nxy;
+      rc.dzp = (iz == g.nz - 1) ? -(g.nz - 1) * g.nxy : g.nxy;
+    }
+  }
+  return rc;
+}
+
+template <int NDIM>
+__device__ __forceinline__ int row_neighbours(const Grid &g, const RowCtx &rc, int ix, int nb[6]) {
+  const int p = rc.base + ix;
+  nb[0] = p + (ix == 0 ? g.nx - 1 : -1);
+  nb[1] = p + (ix == g.nx - 1 ? 1 - g.nx : 1);
+  nb[2] = p + rc.dym;
+  nb[3] = p + rc.dyp;
+  nb[4] = p + rc.dzm;
+  nb[5] = p + rc.dzp;
+  return p;
+}
+
 // Periodic neighbours of p: [xm, xp, ym, yp, zm, zp].
 template <int NDIM>
 __device__ __forceinline__ void neighbours(const Grid &g, int p, int nb[6]) {
@@ -77,9 +116,7 @@ __device__ __forceinline__ double dsum_of(const Grid &g, const int nb[6], F v) {
 // N(u)[p]
 template <int KIND, int NDIM>
 __device__ __forceinline__ double rhs_at(const Grid &g, const KindParams &kp,
-                                         const double *__restrict__ u, int p) {
-  int nb[6];
-  neighbours<NDIM>(g, p, nb);
+                                         const double *__restrict__ u, int p, const int nb[6]) {
   double up = u[p];
   if (KIND == KIND_NLDIFF) {
     auto phi = [&](int q) {
@@ -126,6 +163,68 @@ __device__ __forceinline__ double lx_at(const Grid &g, const KindParams &kp,
     return sigma * (kp.nu * lap_of<NDIM>(g, nb, x[p], xv) + kp.c * dsum_of<NDIM>(g, nb, xv)) +
            a[p] * x[p];
   }
+}
+
+// ---- value-based forms (register-sliding kernels, stencil.cu) ----------
+// A field sampled at a point and its periodic neighbours [xm, xp, ym, yp, zm, zp].
+struct Nb {
+  double c;
+  double v[6];
+};
+
+template <int NDIM, class F>
+__device__ __forceinline__ double lap_nb(const Grid &g, const Nb &f, F op) {
+  double cp = op(f.c, 6);
+  double s = g.ih2[0] * (op(f.v[0], 0) + op(f.v[1], 1) - 2.0 * cp);
+  if (NDIM >= 2) s += g.ih2[1] * (op(f.v[2], 2) + op(f.v[3], 3) - 2.0 * cp);
+  if (NDIM == 3) s += g.ih2[2] * (op(f.v[4], 4) + op(f.v[5], 5) - 2.0 * cp);
+  return s;
+}
+
+template <int NDIM, class F>
+__device__ __forceinline__ double dsum_nb(const Grid &g, const Nb &f, F op) {
+  double s = g.i2h[0] * (op(f.v[1], 1) - op(f.v[0], 0));
+  if (NDIM >= 2) s += g.i2h[1] * (op(f.v[3], 3) - op(f.v[2], 2));
+  if (NDIM == 3) s += g.i2h[2] * (op(f.v[5], 5) - op(f.v[4], 4));
+  return s;
+}
+
+// N(u) from neighbour values
+template <int KIND, int NDIM>
+__device__ __forceinline__ double rhs_nb(const Grid &g, const KindParams &kp, const Nb &u) {
+  if (KIND == KIND_NLDIFF) {
+    return lap_nb<NDIM>(g, u, [](double v, int) { return v + v * v * v / 3.0; });
+  } else if (KIND == KIND_BURGERS) {
+    return -dsum_nb<NDIM>(g, u, [](double v, int) { return 0.5 * v * v; }) +
+           kp.nu * lap_nb<NDIM>(g, u, [](double v, int) { return v; });
+  } else {
+    const double up = u.c;
+    return kp.nu * lap_nb<NDIM>(g, u, [](double v, int) { return v; }) +
+           kp.c * dsum_nb<NDIM>(g, u, [](double v, int) { return v; }) + kp.lam * up +
+           kp.mu * up * up;
+  }
+}
+
+// L_eff(a, sigma) x from neighbour values of a and x
+template <int KIND, int NDIM>
+__device__ __forceinline__ double lx_nb(const Grid &g, const KindParams &kp, const Nb &a,
+                                        double sigma, const Nb &x) {
+  if (KIND == KIND_NLDIFF) {
+    return lap_nb<NDIM>(g, x, [&](double v, int k) { return (k == 6 ? a.c : a.v[k]) * v; });
+  } else if (KIND == KIND_BURGERS) {
+    return -dsum_nb<NDIM>(g, x, [&](double v, int k) { return (k == 6 ? a.c : a.v[k]) * v; }) +
+           sigma * kp.nu * lap_nb<NDIM>(g, x, [](double v, int) { return v; });
+  } else {
+    return sigma * (kp.nu * lap_nb<NDIM>(g, x, [](double v, int) { return v; }) +
+                    kp.c * dsum_nb<NDIM>(g, x, [](double v, int) { return v; })) +
+           a.c * x.c;
+  }
+}
+
+// whether L_eff reads the coefficient field at neighbour points
+template <int KIND>
+__device__ __forceinline__ constexpr bool a_stencil() {
+  return KIND != KIND_RAD;
 }
 
 // diagonal entry of L_eff(a, sigma) at p

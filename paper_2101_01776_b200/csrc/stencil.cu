@@ -1,0 +1,415 @@
+// stencil.cu -- register-sliding stencil kernels (2-D / 3-D).
+//
+// Each thread owns one column along the slowest axis (y in 2-D, z in 3-D)
+// and slides along it, keeping every input field's (-1, 0, +1) values in
+// registers; in-plane neighbours are L1 hits (loaded by neighbouring lanes /
+// warps of the same CTA).  Every field therefore crosses L2->SM roughly once
+// instead of three times (the row-per-CTA layout re-fetched each y-neighbour
+// row from L2).  Used by the Jacobi sweeps (ShiftedSolver inner solves,
+// src/irk_core.py:117-123), the block operators (src/irk_core.py:126-140,
+// 216-219) and the stage residual (src/nonlinear.py:145-152).
+#include "engine.h"
+
+namespace irkg {
+
+namespace {
+
+constexpr int SBX = 128;  // threads per CTA
+
+// Geometry of the slide: plane size P, number of planes NS, in-plane extents.
+struct Slide {
+  int P, NS;
+};
+
+template <int NDIM>
+__device__ __forceinline__ Slide slide_of(const Grid &g) {
+  Slide s;
+  if (NDIM == 2) {
+    s.P = g.nx;
+    s.NS = g.ny;
+  } else {
+    s.P = g.nxy;
+    s.NS = g.nz;
+  }
+  return s;
+}
+
+// column owned by this thread: in-plane offset q, or -1 if outside
+template <int NDIM>
+__device__ __forceinline__ int column_q(const Grid &g, int &ix, int &iy) {
+  if (NDIM == 2) {
+    ix = blockIdx.x * SBX + threadIdx.x;
+    iy = 0;
+    return ix < g.nx ? ix : -1;
+  } else {
+    ix = blockIdx.x * 32 + (threadIdx.x & 31);
+    iy = blockIdx.y * (SBX / 32) + (threadIdx.x >> 5);
+    return (ix < g.nx && iy < g.ny) ? iy * g.nx + ix : -1;
+  }
+}
+
+// in-plane neighbour offsets relative to the point (periodic)
+struct InPlane {
+  int dxm, dxp, dym, dyp;
+};
+
+template <int NDIM>
+__device__ __forceinline__ InPlane in_plane(const Grid &g, int ix, int iy) {
+  InPlane o;
+  o.dxm = (ix == 0) ? g.nx - 1 : -1;
+  o.dxp = (ix == g.nx - 1) ? 1 - g.nx : 1;
+  o.dym = o.dyp = 0;
+  if (NDIM == 3) {
+    o.dym = (iy == 0) ? (g.ny - 1) * g.nx : -g.nx;
+    o.dyp = (iy == g.ny - 1) ? -(g.ny - 1) * g.nx : g.nx;
+  }
+  return o;
+}
+
+struct Win {
+  double m, c, p;
+};
+
+template <int NDIM>
+__device__ __forceinline__ Nb gather(const Win &w, const double *f, int p, const InPlane &o) {
+  Nb n;
+  n.c = w.c;
+  n.v[0] = f[p + o.dxm];
+  n.v[1] = f[p + o.dxp];
+  if (NDIM == 2) {
+    n.v[2] = w.m;
+    n.v[3] = w.p;
+    n.v[4] = n.v[5] = 0.0;
+  } else {
+    n.v[2] = f[p + o.dym];
+    n.v[3] = f[p + o.dyp];
+    n.v[4] = w.m;
+    n.v[5] = w.p;
+  }
+  return n;
+}
+
+__device__ __forceinline__ int wrap_plane(int s, int NS) {
+  return s < 0 ? s + NS : (s >= NS ? s - NS : s);
+}
+
+__device__ __forceinline__ double wsum2(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// fold one value per CTA through the last-CTA ticket (deterministic order)
+__device__ void cta_reduce_store(double v, double *part, int nblk, unsigned *counter,
+                                 double *out) {
+  __shared__ double red[SBX / 32];
+  __shared__ bool last;
+  const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  v = wsum2(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < SBX / 32; ++w) t += red[w];
+    part[bid] = t;
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == (unsigned)(nblk - 1));
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int c = threadIdx.x; c < nblk; c += 32) s += __ldcg(part + c);
+    s = wsum2(s);
+    if (threadIdx.x == 0) {
+      *out = s;
+      *counter = 0u;
+    }
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------- Jacobi sweep
+// x' = x + omega * (r - (alpha x - dt L x)) / D   (src/irk_core.py:121-123)
+template <int KIND, int NDIM>
+__global__ void __launch_bounds__(SBX) k_jac_sweep_s(Grid g, KindParams kp, Op L, double alpha,
+                                                     double dt, VecIn vin, int in_off,
+                                                     const double *__restrict__ t_in,
+                                                     const double *__restrict__ x,
+                                                     double *__restrict__ x_out, int span,
+                                                     const GCtrl *skip) {
+  if (skip && skip->cycle_done) return;
+  const double *in = nullptr;
+  double scale = 1.0;
+  if (!t_in) {
+    if (vin.ctrl) {
+      const int j = vin.ctrl->j;
+      in = vin.base + (size_t)j * vin.pitch;
+      scale = vin.alpha[j];
+    } else {
+      in = vin.base;
+    }
+    in += in_off;
+  }
+  int ix, iy;
+  const int q = column_q<NDIM>(g, ix, iy);
+  if (q < 0) return;
+  const Slide sl = slide_of<NDIM>(g);
+  const InPlane o = in_plane<NDIM>(g, ix, iy);
+  const int s0 = (NDIM == 2 ? blockIdx.y : blockIdx.z) * span;
+  const int s1 = min(sl.NS, s0 + span);
+  const double *a = L.a;
+  Win wx, wa;
+  {
+    const int pm = wrap_plane(s0 - 1, sl.NS) * sl.P + q, pc = s0 * sl.P + q;
+    wx.m = x[pm];
+    wx.c = x[pc];
+    if (a_stencil<KIND>()) {
+      wa.m = a[pm];
+      wa.c = a[pc];
+    }
+  }
+  for (int s = s0; s < s1; ++s) {
+    const int p = s * sl.P + q;
+    const int pn = wrap_plane(s + 1, sl.NS) * sl.P + q;
+    wx.p = x[pn];
+    if (a_stencil<KIND>()) wa.p = a[pn];
+    const double r = t_in ? t_in[p] : scale * in[p];
+    Nb xn = gather<NDIM>(wx, x, p, o);
+    Nb an;
+    if (a_stencil<KIND>()) {
+      an = gather<NDIM>(wa, a, p, o);
+    } else {
+      an.c = a[p];
+    }
+    const double lx = lx_nb<KIND, NDIM>(g, kp, an, L.sigma, xn);
+    const double diag = ldiag_at<KIND>(g, kp, a, L.sigma, p);
+    const double D = alpha - dt * diag;
+    const double sx = alpha * wx.c - dt * lx;
+    x_out[p] = wx.c + OMEGA * ((1.0 / D) * (r - sx));
+    wx.m = wx.c;
+    wx.c = wx.p;
+    if (a_stencil<KIND>()) {
+      wa.m = wa.c;
+      wa.c = wa.p;
+    }
+  }
+}
+
+// --------------------------------------------------------- block operator
+// SIZE 1: w = eta z - dt L1 z (src/irk_core.py:216-219)
+// SIZE 2: apply_block2x2 (src/irk_core.py:126-140); b != null: w = b - A z, ||w||^2
+template <int KIND, int NDIM, int SIZE>
+__global__ void __launch_bounds__(SBX)
+    k_block_op_s(Grid g, KindParams kp, double eta, double beta, double phi, double dt, Op l1,
+                 Op l2, Op c12, Op c21, const double *__restrict__ z, double *__restrict__ w,
+                 const double *__restrict__ b, int span, double *part, unsigned *counter,
+                 double *out_norm, const GCtrl *skip) {
+  if (skip && skip->cycle_done) return;
+  const int n = g.n;
+  int ix, iy;
+  const int q = column_q<NDIM>(g, ix, iy);
+  double nrm = 0.0;
+  if (q >= 0) {
+    const Slide sl = slide_of<NDIM>(g);
+    const InPlane o = in_plane<NDIM>(g, ix, iy);
+    const int s0 = (NDIM == 2 ? blockIdx.y : blockIdx.z) * span;
+    const int s1 = min(sl.NS, s0 + span);
+    const double *z1 = z, *z2 = z + n;
+    constexpr bool AS = a_stencil<KIND>();
+    const bool h12 = SIZE == 2 && c12.present, h21 = SIZE == 2 && c21.present;
+    Win w1{}, w2{}, wa1{}, wa2{}, wc12{}, wc21{};
+    auto init = [&](Win &wv, const double *f) {
+      wv.m = f[wrap_plane(s0 - 1, sl.NS) * sl.P + q];
+      wv.c = f[s0 * sl.P + q];
+    };
+    init(w1, z1);
+    if (AS) init(wa1, l1.a);
+    if (SIZE == 2) {
+      init(w2, z2);
+      if (AS) init(wa2, l2.a);
+      if (AS && h12) init(wc12, c12.a);
+      if (AS && h21) init(wc21, c21.a);
+    }
+    for (int s = s0; s < s1; ++s) {
+      const int p = s * sl.P + q;
+      const int pn = wrap_plane(s + 1, sl.NS) * sl.P + q;
+      w1.p = z1[pn];
+      if (AS) wa1.p = l1.a[pn];
+      if (SIZE == 2) {
+        w2.p = z2[pn];
+        if (AS) wa2.p = l2.a[pn];
+        if (AS && h12) wc12.p = c12.a[pn];
+        if (AS && h21) wc21.p = c21.a[pn];
+      }
+      auto field = [&](const Win &wv, const double *f) {
+        Nb r;
+        if (AS) {
+          r = gather<NDIM>(wv, f, p, o);
+        } else {
+          r.c = f[p];
+        }
+        return r;
+      };
+      const Nb x1 = gather<NDIM>(w1, z1, p, o);
+      if (SIZE == 1) {
+        double v = eta * x1.c - dt * lx_nb<KIND, NDIM>(g, kp, field(wa1, l1.a), l1.sigma, x1);
+        if (b) {
+          v = b[p] - v;
+          nrm += v * v;
+        }
+        w[p] = v;
+      } else {
+        const Nb x2 = gather<NDIM>(w2, z2, p, o);
+        double top = eta * x1.c - dt * lx_nb<KIND, NDIM>(g, kp, field(wa1, l1.a), l1.sigma, x1) +
+                     phi * x2.c;
+        double bot = -(beta * beta / phi) * x1.c + eta * x2.c -
+                     dt * lx_nb<KIND, NDIM>(g, kp, field(wa2, l2.a), l2.sigma, x2);
+        if (h12) top -= dt * lx_nb<KIND, NDIM>(g, kp, field(wc12, c12.a), c12.sigma, x2);
+        if (h21) bot -= dt * lx_nb<KIND, NDIM>(g, kp, field(wc21, c21.a), c21.sigma, x1);
+        if (b) {
+          top = b[p] - top;
+          bot = b[p + n] - bot;
+          nrm += top * top + bot * bot;
+        }
+        w[p] = top;
+        w[p + n] = bot;
+      }
+      auto shift = [](Win &wv) {
+        wv.m = wv.c;
+        wv.c = wv.p;
+      };
+      shift(w1);
+      if (AS) shift(wa1);
+      if (SIZE == 2) {
+        shift(w2);
+        if (AS) shift(wa2);
+        if (AS && h12) shift(wc12);
+        if (AS && h21) shift(wc21);
+      }
+    }
+  }
+  if (b) {
+    const int nblk = gridDim.x * gridDim.y * gridDim.z;
+    cta_reduce_store(nrm, part, nblk, counter, out_norm);
+  }
+}
+
+// ------------------------------------------------------- stage residual
+// F_i = N(U_i) - K_i, ||F||^2   (src/nonlinear.py:148-152)
+template <int KIND, int NDIM>
+__global__ void __launch_bounds__(SBX)
+    k_residual_s(Grid g, KindParams kp, int s_st, const double *__restrict__ U,
+                 const double *__restrict__ K, double *__restrict__ F, int span, double *part,
+                 unsigned *counter, double *out) {
+  const int n = g.n;
+  int ix, iy;
+  const int q = column_q<NDIM>(g, ix, iy);
+  double acc = 0.0;
+  if (q >= 0) {
+    const Slide sl = slide_of<NDIM>(g);
+    const InPlane o = in_plane<NDIM>(g, ix, iy);
+    const int s0 = (NDIM == 2 ? blockIdx.y : blockIdx.z) * span;
+    const int s1 = min(sl.NS, s0 + span);
+    for (int i = 0; i < s_st; ++i) {
+      const double *u = U + (size_t)i * n;
+      Win wu;
+      wu.m = u[wrap_plane(s0 - 1, sl.NS) * sl.P + q];
+      wu.c = u[s0 * sl.P + q];
+      for (int s = s0; s < s1; ++s) {
+        const int p = s * sl.P + q;
+        wu.p = u[wrap_plane(s + 1, sl.NS) * sl.P + q];
+        const Nb un = gather<NDIM>(wu, u, p, o);
+        const double f = rhs_nb<KIND, NDIM>(g, kp, un) - K[(size_t)i * n + p];
+        F[(size_t)i * n + p] = f;
+        acc += f * f;
+        wu.m = wu.c;
+        wu.c = wu.p;
+      }
+    }
+  }
+  const int nblk = gridDim.x * gridDim.y * gridDim.z;
+  cta_reduce_store(acc, part, nblk, counter, out);
+}
+
+// ============================================================ launchers
+
+template <class F>
+static void dispatch_kd23(int kind, int ndim, F f) {
+  auto with_dim = [&](auto K) {
+    if (ndim == 2)
+      f(K, std::integral_constant<int, 2>{});
+    else
+      f(K, std::integral_constant<int, 3>{});
+  };
+  switch (kind) {
+    case KIND_NLDIFF: with_dim(std::integral_constant<int, KIND_NLDIFF>{}); break;
+    case KIND_BURGERS: with_dim(std::integral_constant<int, KIND_BURGERS>{}); break;
+    default: with_dim(std::integral_constant<int, KIND_RAD>{}); break;
+  }
+}
+
+// grid + slide span for ~8 CTAs per SM
+dim3 Engine::slide_grid(int &span) const {
+  if (ndim == 2) {
+    const int bx = (grid.nx + SBX - 1) / SBX;
+    long long target = (long long)sms * 8;
+    int sp = (int)((long long)bx * grid.ny / target);
+    sp = sp < 2 ? 2 : (sp > 32 ? 32 : sp);
+    span = sp;
+    return dim3(bx, (grid.ny + sp - 1) / sp, 1);
+  }
+  const int bx = (grid.nx + 31) / 32, by = (grid.ny + SBX / 32 - 1) / (SBX / 32);
+  long long target = (long long)sms * 8;
+  int sp = (int)((long long)bx * by * grid.nz / target);
+  sp = sp < 2 ? 2 : (sp > 32 ? 32 : sp);
+  span = sp;
+  return dim3(bx, by, (grid.nz + sp - 1) / sp);
+}
+
+void Engine::jac_sweep_s(const Op &L, double alpha, double dt, const VecIn &vin, int in_off,
+                         const double *t_in, const double *x, double *x_out, const GCtrl *skip) {
+  int span;
+  const dim3 gr = slide_grid(span);
+  dispatch_kd23(prob.kind, ndim, [&](auto KD, auto ND) {
+    k_jac_sweep_s<decltype(KD)::value, decltype(ND)::value>
+        <<<gr, SBX, 0, stream>>>(grid, kp, L, alpha, dt, vin, in_off, t_in, x, x_out, span, skip);
+  });
+  count(1);
+}
+
+void Engine::block_op_s(const BlockSpec &B, const double *z, double *w, const double *b,
+                        double *out_norm, const GCtrl *skip) {
+  int span;
+  const dim3 gr = slide_grid(span);
+  dispatch_kd23(prob.kind, ndim, [&](auto KD, auto ND) {
+    constexpr int K_ = decltype(KD)::value, D_ = decltype(ND)::value;
+    if (B.size == 1)
+      k_block_op_s<K_, D_, 1><<<gr, SBX, 0, stream>>>(grid, kp, B.eta, B.beta, B.phi, B.dt, B.l1,
+                                                      B.l2, B.c12, B.c21, z, w, b, span, part,
+                                                      counter, out_norm, skip);
+    else
+      k_block_op_s<K_, D_, 2><<<gr, SBX, 0, stream>>>(grid, kp, B.eta, B.beta, B.phi, B.dt, B.l1,
+                                                      B.l2, B.c12, B.c21, z, w, b, span, part,
+                                                      counter, out_norm, skip);
+  });
+  count(1);
+}
+
+double Engine::residual_s(const double *Ust, const double *K, double *Fo) {
+  int span;
+  const dim3 gr = slide_grid(span);
+  dispatch_kd23(prob.kind, ndim, [&](auto KD, auto ND) {
+    k_residual_s<decltype(KD)::value, decltype(ND)::value>
+        <<<gr, SBX, 0, stream>>>(grid, kp, s, Ust, K, Fo, span, part, counter, &scal_dev[0]);
+  });
+  count(1);
+  double v = 0.0;
+  check(cudaMemcpyAsync(&v, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost, stream));
+  check(cudaStreamSynchronize(stream));
+  return v;
+}
+
+}  // namespace irkg

@@ -236,3 +236,9 @@ def test_device_entry_points_fail_loudly_without_gpu():
     with pytest.raises(RuntimeError):
         pk.step(prob, np.zeros(64), 0.0, 1e-3, pk.make_tableau("gauss", 2),
                 pk.SolverConfig(precond=pk.PrecondSpec(inner=4)))
+
+
+def test_built_library_matches_sources():
+    from paper_2101_01776_b200 import _build
+
+    assert _build.is_fresh(), "libirkg.so is stale: run python -m paper_2101_01776_b200._build"
