@@ -129,6 +129,8 @@ typedef struct {
   int64_t cgs_launches;
   double precond_bytes;
   double op_bytes;
+  double precond_time_ms; /* device time of the inner solves (if timing on) */
+  double op_time_ms;      /* device time of the block operator (if timing on) */
 } irkg_counters;
 
 const char *irkg_last_error(void);

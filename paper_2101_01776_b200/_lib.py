@@ -115,6 +115,8 @@ class Counters(C.Structure):
         ("cgs_launches", C.c_int64),
         ("precond_bytes", C.c_double),
         ("op_bytes", C.c_double),
+        ("precond_time_ms", C.c_double),
+        ("op_time_ms", C.c_double),
     ]
 
 

@@ -85,7 +85,11 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st) : prob(p), devic
   dalloc(&ufield, N);
   check(cudaEventCreate(&ev0), "event");
   check(cudaEventCreate(&ev1), "event");
+  check(cudaEventCreate(&evp[0]), "event");
+  check(cudaEventCreate(&evp[1]), "event");
   if (const char *e = getenv("IRKG_GRAPHS")) use_graphs = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_FUSED_JACOBI")) fused_jacobi = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_JSPAN")) jspan_override = atoi(e);
   for (int i = 0; i < MAXS; ++i)
     for (int j = 0; j < MAXS; ++j) od_slot[i][j] = -1;
 }
@@ -290,7 +294,9 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
       counters.arnoldi_iterations += its;
     } else {
       for (int it = 0; it < m; ++it) {
+        if (timing) check(cudaEventRecord(evp[0], stream));
         precond(B, &vslot, zbuf, ctrl_dev);                           // z = M^{-1} v_j
+        if (timing) check(cudaEventRecord(evp[1], stream));
         block_op(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev);          // w = A z
         if (timing) check(cudaEventRecord(ev0, stream));
         cgs(n);  // CGS2 in 3 fused sweeps + Hessenberg column / Givens / exit test
@@ -302,6 +308,10 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
           float ms = 0.f;
           check(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
           counters.cgs_time_ms += ms;
+          check(cudaEventElapsedTime(&ms, evp[0], evp[1]), "elapsed");
+          counters.precond_time_ms += ms;
+          check(cudaEventElapsedTime(&ms, evp[1], ev0), "elapsed");
+          counters.op_time_ms += ms;
         }
         if (ctrl_host->cycle_done) break;
       }

@@ -84,7 +84,7 @@ struct Engine {
   double *opA = nullptr;        // (nops, N) operator fields
   int nops_cap = 0;
   GCtrl *ctrl_host = nullptr;   // pinned mirror
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evp[2] = {nullptr, nullptr};
 
   // current linearisation: operator slot per diag row and per offdiag key
   int nops = 0;
@@ -129,6 +129,12 @@ struct Engine {
   void block_op_s(const BlockSpec &B, const double *z, double *w, const double *b,
                   double *out_norm, const GCtrl *skip);
   double residual_s(const double *U, const double *K, double *F);
+  // jacobi.cu (temporally blocked inner solves, 2-D)
+  bool fused_jacobi = true;
+  int jspan_override = 0;
+  bool jacobi_chain_fused(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
+                          int in_off, const double *zc, double cpl, double *x_out,
+                          const GCtrl *skip);
 
   // launch helpers (kernels.cu)
   int grid_for(long long n) const;

@@ -1,0 +1,221 @@
+// jacobi.cu -- temporally blocked damped-Jacobi inner solves (2-D).
+//
+// ShiftedSolver(alpha, I, L, dt, inner=K).solve(r) (src/irk_core.py:117-123):
+//     x_0 = 0;  x_m = x_{m-1} + (2/3) D^{-1} (r - (alpha I - dt L) x_{m-1}),  m = 1..K
+// computed in ONE pass over the grid instead of K: every warp owns a strip of
+// 32 columns and slides along y; sweep m runs one row behind sweep m-1 and
+// keeps its last three output rows in registers, so all K sweeps are fused
+// with no intermediate x written to memory (temporal blocking, halo K-1).
+// x-neighbours come from warp shuffles; the valid columns shrink by one per
+// sweep on each side, so a warp emits 34-2K columns.  The inputs r (= scale *
+// basis slot j [+ coupling * z1 for the second block row]) and the operator
+// field a are read once; x_K is written once:  3-4 passes of N instead of
+// 4K-1.  Inputs are prefetched PF rows ahead (register FIFO) for HBM MLP.
+#include "engine.h"
+
+namespace irkg {
+
+namespace {
+
+constexpr int JW = 4;   // warps per CTA
+constexpr int JPF = 4;  // prefetch depth (rows)
+
+__device__ __forceinline__ double shfl_up1(double v) {
+  return __shfl_sync(0xffffffffu, v, (threadIdx.x + 31) & 31);
+}
+__device__ __forceinline__ double shfl_dn1(double v) {
+  return __shfl_sync(0xffffffffu, v, (threadIdx.x + 1) & 31);
+}
+
+// (L_eff x) at a point from own-column rows (m, c, p) and x-neighbours
+template <int KIND>
+__device__ __forceinline__ double lx_col(const Grid &g, const KindParams &kp, double sigma,
+                                         double am, double ac, double ap, double xm, double xc,
+                                         double xp) {
+  if (KIND == KIND_NLDIFF) {
+    const double axc = ac * xc;
+    const double axl = shfl_up1(axc), axr = shfl_dn1(axc);
+    return g.ih2[0] * (axl + axr - 2.0 * axc) + g.ih2[1] * (am * xm + ap * xp - 2.0 * axc);
+  } else if (KIND == KIND_BURGERS) {
+    const double axc = ac * xc;
+    const double axl = shfl_up1(axc), axr = shfl_dn1(axc);
+    const double xl = shfl_up1(xc), xr = shfl_dn1(xc);
+    const double adv = g.i2h[0] * (axr - axl) + g.i2h[1] * (ap * xp - am * xm);
+    const double lap = g.ih2[0] * (xl + xr - 2.0 * xc) + g.ih2[1] * (xm + xp - 2.0 * xc);
+    return -adv + sigma * kp.nu * lap;
+  } else {
+    const double xl = shfl_up1(xc), xr = shfl_dn1(xc);
+    const double lap = g.ih2[0] * (xl + xr - 2.0 * xc) + g.ih2[1] * (xm + xp - 2.0 * xc);
+    const double ds = g.i2h[0] * (xr - xl) + g.i2h[1] * (xp - xm);
+    return sigma * (kp.nu * lap + kp.c * ds) + ac * xc;
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ double diag_of(const Grid &g, const KindParams &kp, double a,
+                                          double sigma) {
+  if (KIND == KIND_NLDIFF) return g.lapdiag * a;
+  if (KIND == KIND_BURGERS) return sigma * kp.nu * g.lapdiag;
+  return sigma * kp.nu * g.lapdiag + a;
+}
+
+}  // namespace
+
+template <int KIND, int K>
+__global__ void __launch_bounds__(JW * 32)
+    k_jacobi_chain2d(Grid g, KindParams kp, Op L, double alpha, double dt, VecIn vin, int in_off,
+                     const double *__restrict__ zc, double cpl, double *__restrict__ x_out,
+                     int span, GCtrl *flag_ctrl, const GCtrl *skip) {
+  if (skip && skip->cycle_done) return;
+  constexpr int H = K - 1;
+  constexpr int WCOLS = 32 - 2 * H;  // valid output columns per warp
+  const double *in;
+  double scale;
+  if (vin.ctrl) {
+    const int j = vin.ctrl->j;
+    in = vin.base + (size_t)j * vin.pitch;
+    scale = vin.alpha[j];
+  } else {
+    in = vin.base;
+    scale = 1.0;
+  }
+  in += in_off;
+  const int lane = threadIdx.x & 31;
+  const int wtile = blockIdx.x * JW + (threadIdx.x >> 5);
+  const int x0 = wtile * WCOLS;
+  if (x0 >= g.nx) return;  // whole warp idle
+  int col = x0 - H + lane;
+  col = col < 0 ? col + g.nx : (col >= g.nx ? col - g.nx : col);
+  // degenerate tiny grids: a column may alias another lane's; still correct
+  // because every lane computes its own column's values.
+  const bool valid_lane = (lane >= H) && (lane < 32 - H) && (x0 - H + lane < g.nx);
+  const int y0 = blockIdx.y * span;
+  const int y1 = min(g.ny, y0 + span);
+  const double *a = L.a;
+  const double sig = L.sigma;
+  const int ny = g.ny;
+  auto wrapy = [&](int y) { return y < 0 ? y + ny : (y >= ny ? y - ny : y); };
+
+  // windows (rows relative to the current input row t)
+  double A[K + 1];   // a rows t-K .. t
+  double ID[K + 1];  // 1/D rows t-K .. t (D = alpha - dt diag L)
+  double R[K];       // r rows t-K+1 .. t
+  double X[K][3];    // X[m][.]: sweep m (1..K-1) outputs rows rho_m-2, rho_m-1, rho_m
+#pragma unroll
+  for (int i = 0; i <= K; ++i) A[i] = ID[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) R[i] = 0.0;
+#pragma unroll
+  for (int m = 0; m < K; ++m) X[m][0] = X[m][1] = X[m][2] = 0.0;
+  // two statically named prefetch banks of JPF rows each (no register moves
+  // of in-flight load destinations, which would stall on the scoreboard)
+  double pa[JPF], pr[JPF], qa[JPF], qr[JPF];
+  const int t0 = y0 - H, t1 = y1 + H;  // input rows [t0, t1)
+  auto load_row = [&](int t, double &av, double &rv) {
+    if (t < t1) {
+      const int p = wrapy(t) * g.nx + col;
+      av = a[p];
+      double r = scale * in[p];
+      if (zc) r = r + cpl * zc[p];
+      rv = r;
+    } else {
+      av = 0.0;
+      rv = 0.0;
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < JPF; ++i) load_row(t0 + i, pa[i], pr[i]);
+
+  bool zero_diag = false;
+  auto step = [&](int t, double a_in, double r_in) {
+    // shift windows and take row t
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      A[i] = A[i + 1];
+      ID[i] = ID[i + 1];
+    }
+#pragma unroll
+    for (int i = 0; i < K - 1; ++i) R[i] = R[i + 1];
+    A[K] = a_in;
+    R[K - 1] = r_in;
+    {
+      const double D = alpha - dt * diag_of<KIND>(g, kp, A[K], sig);
+      zero_diag |= (D == 0.0);
+      ID[K] = 1.0 / D;
+    }
+    // sweep 1 at row t (pointwise from x_0 = 0)
+    double xnew = OMEGA * (ID[K] * R[K - 1]);
+    // sweeps 2..K: sweep m at row rho = t - m + 1
+#pragma unroll
+    for (int m = 2; m <= K; ++m) {
+      // sweep m-1's window gets its newest row
+      X[m - 1][0] = X[m - 1][1];
+      X[m - 1][1] = X[m - 1][2];
+      X[m - 1][2] = xnew;
+      const double am = A[K - m], ac = A[K - m + 1], ap = A[K - m + 2];
+      const double xm = X[m - 1][0], xc = X[m - 1][1], xp = X[m - 1][2];
+      const double lx = lx_col<KIND>(g, kp, sig, am, ac, ap, xm, xc, xp);
+      const double sx = alpha * xc - dt * lx;
+      xnew = xc + OMEGA * (ID[K - m + 1] * (R[K - m] - sx));
+    }
+    // sweep K output row t - H
+    const int yo = t - H;
+    if (valid_lane && yo >= y0 && yo < y1) x_out[yo * g.nx + col] = xnew;
+  };
+  for (int t = t0; t < t1; t += 2 * JPF) {
+#pragma unroll
+    for (int i = 0; i < JPF; ++i) load_row(t + JPF + i, qa[i], qr[i]);
+#pragma unroll
+    for (int i = 0; i < JPF; ++i)
+      if (t + i < t1) step(t + i, pa[i], pr[i]);
+#pragma unroll
+    for (int i = 0; i < JPF; ++i) load_row(t + 2 * JPF + i, pa[i], pr[i]);
+#pragma unroll
+    for (int i = 0; i < JPF; ++i)
+      if (t + JPF + i < t1) step(t + JPF + i, qa[i], qr[i]);
+  }
+  if (zero_diag && flag_ctrl) flag_ctrl->zero_diag = 1;
+}
+
+// launcher: returns false when the fused path does not apply
+bool Engine::jacobi_chain_fused(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
+                                int in_off, const double *zc, double cpl, double *x_out,
+                                const GCtrl *skip) {
+  if (!fused_jacobi || ndim != 2 || inner < 1 || inner > 6 || grid.nx < 32 ||
+      grid.ny < 2 * inner)
+    return false;
+  const int H = inner - 1;
+  const int wcols = 32 - 2 * H;
+  const int xt = (grid.nx + wcols - 1) / wcols;
+  const int bx = (xt + JW - 1) / JW;
+  long long target = (long long)sms * 16 / JW;  // ~16 warps per SM
+  int span = (int)((long long)bx * grid.ny / target);
+  span = span < 8 ? 8 : (span > 64 ? 64 : span);
+  if (jspan_override > 0) span = jspan_override;
+  if (span > grid.ny) span = grid.ny;
+  const dim3 gr(bx, (grid.ny + span - 1) / span);
+  auto go = [&](auto KD, auto KK) {
+    k_jacobi_chain2d<decltype(KD)::value, decltype(KK)::value><<<gr, JW * 32, 0, stream>>>(
+        grid, kp, L, alpha, dt, vin, in_off, zc, cpl, x_out, span, ctrl_dev, skip);
+  };
+  auto with_k = [&](auto KD) {
+    switch (inner) {
+      case 1: go(KD, std::integral_constant<int, 1>{}); break;
+      case 2: go(KD, std::integral_constant<int, 2>{}); break;
+      case 3: go(KD, std::integral_constant<int, 3>{}); break;
+      case 4: go(KD, std::integral_constant<int, 4>{}); break;
+      case 5: go(KD, std::integral_constant<int, 5>{}); break;
+      default: go(KD, std::integral_constant<int, 6>{}); break;
+    }
+  };
+  switch (prob.kind) {
+    case KIND_NLDIFF: with_k(std::integral_constant<int, KIND_NLDIFF>{}); break;
+    case KIND_BURGERS: with_k(std::integral_constant<int, KIND_BURGERS>{}); break;
+    default: with_k(std::integral_constant<int, KIND_RAD>{}); break;
+  }
+  count(1);
+  counters.precond_bytes += 8.0 * N * (zc ? 4.0 : 3.0);
+  return true;
+}
+
+}  // namespace irkg

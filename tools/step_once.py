@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--family", default=None)
     ap.add_argument("--s", type=int, default=None)
+    ap.add_argument("--timing", action="store_true", help="per-phase CUDA-event timing")
     args = ap.parse_args()
     import torch
 
@@ -37,6 +38,8 @@ def main():
     ctx.set_prep(pk.prepare_stages(tab))
     ctx.set_config(cfg)
     u = torch.from_numpy(spec.u0()).cuda()
+    if args.timing:
+        ctx.set_timing(True)
     t = 0.0
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
