@@ -35,6 +35,7 @@ extern "C" {
 #define IRKG_ERR_STEP_FAILURE -4   /* StepFailureError(stats) */
 #define IRKG_ERR_BREAKDOWN -5      /* KrylovBreakdownError */
 #define IRKG_ERR_CUDA -6           /* CUDA / NCCL runtime failure */
+#define IRKG_ERR_INDEX -7          /* IndexViolationError (singular constraint block) */
 
 #define IRKG_MAX_STAGES 8
 #define IRKG_MAX_NEWTON 512
@@ -44,6 +45,7 @@ extern "C" {
 #define IRKG_KIND_NLDIFF 0   /* N(u) = Lap_h(u + u^3/3) */
 #define IRKG_KIND_BURGERS 1  /* N(u) = -Dsum(u^2/2) + nu Lap_h u */
 #define IRKG_KIND_RAD 2      /* N(u) = nu Lap_h u + c Dsum u + lam u + mu u^2 */
+#define IRKG_KIND_ARAKAWA 3  /* DAE: w_t = -J(psi,w) + nu Lap w, 0 = h^2(Lap psi + w) */
 
 typedef struct irkg_ctx irkg_ctx;
 
@@ -118,6 +120,10 @@ typedef struct {
   /* StageSolveError payload (valid when a call returned IRKG_ERR_STAGE_SOLVE) */
   int fail_block_offset;
   irkg_krylov_report fail_report;
+  /* DAE paths (src/nonlinear.py:170-172 fields; zero on ODE paths) */
+  int differential_solves;
+  int constraint_solves;
+  double constraint_residual;
 } irkg_step_stats;
 
 /* Engine counters since creation (bench.py: launches / algorithmic bytes). */
@@ -213,6 +219,23 @@ int irkg_prepare_linearization(irkg_ctx *ctx, const double *u_dev, const double 
                                double dt);
 int irkg_transformed_solve(irkg_ctx *ctx, double dt, const double *rhs_dev, double *dk_dev,
                            irkg_step_stats *stats);
+
+/* ---- index-1 DAE (vorticity/streamfunction, IRKG_KIND_ARAKAWA) ----
+ * State uw = [u; w] (2N: vorticity then streamfunction), stage arrays
+ * (s, 2N) with rows [k_i; l_i] -- the reference's composite layout
+ * (src/dae.py:98).  Reordered mode only (coupled mode hard-codes exact
+ * differential solves, src/dae.py:140). */
+
+/* dae_stage_residual (src/dae.py:94-105) */
+int irkg_dae_stage_residual(irkg_ctx *ctx, const double *uw_dev, const double *k2_dev, double t,
+                            double dt, double *f2_dev, double *norm);
+/* dae_step (src/dae.py:474-498): uw_dev in/out; stats->constraint_residual set */
+int irkg_dae_step(irkg_ctx *ctx, double *uw_dev, double t, double dt, irkg_step_stats *stats);
+/* same with host buffers (H2D + step + D2H) */
+int irkg_dae_step_host(irkg_ctx *ctx, double *uw_host, double t, double dt,
+                       irkg_step_stats *stats);
+/* ||G(u, w, t)||_2 -- the consistency check of dae_integrate (src/dae.py:527-531) */
+int irkg_dae_constraint_norm(irkg_ctx *ctx, const double *uw_dev, double *norm);
 
 #ifdef __cplusplus
 }

@@ -112,6 +112,113 @@ class ProblemDef:
         )
 
 
+def _shift_index(nx, ny, dx, dy):
+    """Flat index of the periodic neighbour (i+dx, j+dy) for every point (x fastest)."""
+    j, i = np.divmod(np.arange(nx * ny), nx)
+    return ((j + dy) % ny) * nx + (i + dx) % nx
+
+
+def arakawa_jacobian_matrix(psi, nx, ny, hx, hy):
+    """CSR of x -> J(psi, x), Arakawa's energy/enstrophy-conserving form
+    J = (J++ + J+x + Jx+)/3 on a periodic grid (x fastest)."""
+    n = nx * ny
+    s = lambda dx, dy: _shift_index(nx, ny, dx, dy)  # noqa: E731
+    pE, pW, pN, pS = psi[s(1, 0)], psi[s(-1, 0)], psi[s(0, 1)], psi[s(0, -1)]
+    pNE, pNW, pSE, pSW = psi[s(1, 1)], psi[s(-1, 1)], psi[s(1, -1)], psi[s(-1, -1)]
+    coef = {
+        (0, 1): (pE - pW) + (pNE - pNW),
+        (0, -1): -(pE - pW) - (pSE - pSW),
+        (1, 0): -(pN - pS) - (pNE - pSE),
+        (-1, 0): (pN - pS) + (pNW - pSW),
+        (1, 1): pE - pN,
+        (1, -1): -pE + pS,
+        (-1, 1): -pW + pN,
+        (-1, -1): pW - pS,
+    }
+    scale = 1.0 / (12.0 * hx * hy)
+    rows = np.concatenate([np.arange(n)] * len(coef))
+    cols = np.concatenate([s(dx, dy) for (dx, dy) in coef])
+    vals = np.concatenate([c * scale for c in coef.values()])
+    return sp.csr_matrix((vals, (rows, cols)), shape=(n, n))
+
+
+def arakawa_jacobian(psi, w, nx, ny, hx, hy):
+    """J(psi, w) evaluated directly from the three Arakawa forms."""
+    s = lambda dx, dy: _shift_index(nx, ny, dx, dy)  # noqa: E731
+    P = {d: psi[s(*d)] for d in [(1, 0), (-1, 0), (0, 1), (0, -1), (1, 1), (-1, 1), (1, -1), (-1, -1)]}
+    W = {d: w[s(*d)] for d in P}
+    j1 = (P[1, 0] - P[-1, 0]) * (W[0, 1] - W[0, -1]) - (P[0, 1] - P[0, -1]) * (W[1, 0] - W[-1, 0])
+    j2 = (P[1, 0] * (W[1, 1] - W[1, -1]) - P[-1, 0] * (W[-1, 1] - W[-1, -1])
+          - P[0, 1] * (W[1, 1] - W[-1, 1]) + P[0, -1] * (W[1, -1] - W[-1, -1]))
+    j3 = (W[0, 1] * (P[1, 1] - P[-1, 1]) - W[0, -1] * (P[1, -1] - P[-1, -1])
+          - W[1, 0] * (P[1, 1] - P[1, -1]) + W[-1, 0] * (P[-1, 1] - P[-1, -1]))
+    return (j1 + j2 + j3) / (12.0 * hx * hy)
+
+
+class DaeProblemDef:
+    """Vorticity/streamfunction index-1 DAE on a periodic box (BASELINE
+    configs[4]), on the reference plugin API DaeSystem(dim_u, dim_w, rhs,
+    constraint, blocks) (src/dae.py:52-66), modelled on shear_layer_small
+    (src/problems.py:245-315):
+
+    * differential  w_t = N(w, psi) = -J(psi, w) + nu Lap w   (Arakawa J)
+    * constraint    0 = G(w, psi) = h^2 (Lap psi + w), row 0 pinned: G_0 = psi_0
+      (h^2-scaled rows: the 1e-10 consistency check of dae_integrate,
+      src/dae.py:527-531, rejects unscaled rows at n >= 128 -- SURVEY 8a a19)
+    * linearisation with lagged advection: L_u = -J(psi, .) + nu Lap,
+      L_w = 0 (so the reordered mode applies), G_u = h^2 I (row 0 zero),
+      G_w = h^2 Lap with row 0 replaced by e_0.
+    """
+
+    def __init__(self, shape, nu, length=1.0):
+        nx, ny = (int(x) for x in shape)
+        self.shape = (nx, ny)
+        self.nu = float(nu)
+        self.dim = nx * ny
+        hx, hy = length / nx, length / ny
+        self.h2 = hx * hy
+        _, lap, _ = grid_operators((nx, ny), (length, length))
+        self.lap = lap
+        n = self.dim
+
+        def rhs(u, w, t):
+            return -arakawa_jacobian(w, u, nx, ny, hx, hy) + self.nu * (lap @ u)
+
+        def constraint(u, w, t):
+            g = self.h2 * (lap @ w + u)
+            g[0] = w[0]
+            return g
+
+        gw = (self.h2 * lap).tolil()
+        gw[0, :] = 0.0
+        gw[0, 0] = 1.0
+        self.gw = gw.tocsr()
+        gu = (self.h2 * sp.identity(n, format="csr")).tolil()
+        gu[0, :] = 0.0
+        self.gu = gu.tocsr()
+        self.lw = sp.csr_matrix((n, n))
+
+        def blocks(u, w, t):
+            lu = (-arakawa_jacobian_matrix(w, nx, ny, hx, hy) + self.nu * lap).tocsr()
+            return lu, self.lw, self.gu, self.gw
+
+        self.rhs = rhs
+        self.constraint = constraint
+        self.blocks_csr = blocks
+
+    def as_dae_system(self, dae_cls, sparse_cls):
+        nx = self.shape[0]
+        blocks = self.blocks_csr
+
+        def blocks_wrapped(u, w, t):
+            lu, lw, gu, gw = blocks(u, w, t)
+            return (sparse_cls(lu, bandwidth=nx + 1), sparse_cls(lw, bandwidth=0),
+                    sparse_cls(gu, bandwidth=0), sparse_cls(gw, bandwidth=nx))
+
+        return dae_cls(dim_u=self.dim, dim_w=self.dim, rhs=self.rhs,
+                       constraint=self.constraint, blocks=blocks_wrapped, name="vorticity2d")
+
+
 def build_problem(kind, shape, **params):
     shape = tuple(int(n) for n in shape)
     lengths = params.get("lengths")

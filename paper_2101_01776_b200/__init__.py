@@ -20,15 +20,25 @@ from .errors import (
     StageSolveError,
     StepFailureError,
 )
-from .problems import GridProblem, RunSpec, baseline_config, fourier_u0
+from .problems import (
+    GridProblem,
+    RunSpec,
+    VorticityProblem,
+    baseline_config,
+    fourier_u0,
+    vorticity_initial_state,
+)
 from .solver import (
     Block2x2System,
+    DaeIntegrationResult,
     OperatorField,
     ShiftedSolver,
     StageLinearization,
     StageState,
     apply_block2x2,
     block_gmres,
+    dae_integrate,
+    dae_step,
     integrate,
     newton_like_step,
     precond_block2x2,
@@ -52,6 +62,11 @@ __all__ = [
     "Block2x2System",
     "ButcherTableau",
     "ConfigurationError",
+    "DaeIntegrationResult",
+    "VorticityProblem",
+    "dae_integrate",
+    "dae_step",
+    "vorticity_initial_state",
     "DecompositionError",
     "EigenBlock",
     "GridProblem",

@@ -23,6 +23,7 @@ ERR_STAGE_SOLVE = -3
 ERR_STEP_FAILURE = -4
 ERR_BREAKDOWN = -5
 ERR_CUDA = -6
+ERR_INDEX = -7
 
 
 class Problem(C.Structure):
@@ -103,6 +104,9 @@ class StepStatsC(C.Structure):
         ("wall_time", C.c_double),
         ("fail_block_offset", C.c_int),
         ("fail_report", KrylovReportC),
+        ("differential_solves", C.c_int),
+        ("constraint_solves", C.c_int),
+        ("constraint_residual", C.c_double),
     ]
 
 
@@ -160,6 +164,10 @@ _SIGS = {
     ),
     "irkg_prepare_linearization": (_I, [_P, _P, _P, _D]),
     "irkg_transformed_solve": (_I, [_P, _D, _P, _P, C.POINTER(StepStatsC)]),
+    "irkg_dae_stage_residual": (_I, [_P, _P, _P, _D, _D, _P, C.POINTER(_D)]),
+    "irkg_dae_step": (_I, [_P, _P, _D, _D, C.POINTER(StepStatsC)]),
+    "irkg_dae_step_host": (_I, [_P, _P, _D, _D, C.POINTER(StepStatsC)]),
+    "irkg_dae_constraint_norm": (_I, [_P, _P, C.POINTER(_D)]),
 }
 
 EXPORTED = tuple(_SIGS)

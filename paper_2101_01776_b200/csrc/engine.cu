@@ -82,7 +82,9 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st) : prob(p), devic
   dalloc(&tmp_x, N);
   dalloc(&tmp_t, N);
   dalloc(&RHS, 2 * N);
-  dalloc(&ufield, N);
+  dae = (p.kind == KIND_ARAKAWA);
+  dalloc(&ufield, Nst());
+  dae_init();
   check(cudaEventCreate(&ev0), "event");
   check(cudaEventCreate(&ev1), "event");
   check(cudaEventCreate(&evp[0]), "event");
@@ -106,16 +108,24 @@ Engine::~Engine() {
   if (ev1) cudaEventDestroy(ev1);
   drop_graphs();
   if (cap_stream) cudaStreamDestroy(cap_stream);
+  dae_fini();
 }
 
 void Engine::ensure_stage_buffers() {
   if (U) return;
-  dalloc(&U, (size_t)s * N);
-  dalloc(&F, (size_t)s * N);
-  dalloc(&Gs, (size_t)s * N);
-  dalloc(&Y, (size_t)s * N);
-  dalloc(&DK, (size_t)s * N);
-  dalloc(&Kst, (size_t)s * N);
+  const size_t ns = (size_t)s * Nst();
+  dalloc(&U, ns);
+  dalloc(&F, ns);
+  dalloc(&Gs, ns);
+  dalloc(&Y, ns);
+  dalloc(&DK, ns);
+  dalloc(&Kst, ns);
+}
+
+void Engine::dalloc_raw(void **p, size_t bytes) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  if (bytes) check(cudaMalloc(p, bytes), "cudaMalloc");
 }
 
 void Engine::ensure_basis(int restart) {
@@ -357,8 +367,13 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
 }
 
 // ------------------------------------------------------- linearisation
-// variant_weights (src/nonlinear.py:99-126) -> operator slots.
+// variant_weights (src/nonlinear.py:99-126) -> operator slots, then fields.
 void Engine::build_linearization(const double *Ust) {
+  build_weights();
+  opfields(Ust, weights, opA);
+}
+
+void Engine::build_weights() {
   const int v = cfg.variant;
   double dw[MAXS][MAXS] = {};
   struct Key {
@@ -435,7 +450,6 @@ void Engine::build_linearization(const double *Ust) {
     op_sigma[o] = sig;
     op_zero[o] = allzero;
   }
-  opfields(Ust, weights, opA);
 }
 
 Op Engine::op_of(int slot) const {
@@ -620,7 +634,9 @@ int irkg_create(irkg_ctx **out, const irkg_problem *prob, int device, void *stre
     if (nranks != 1) throw SolveError(IRKG_ERR_CONFIG, "multi-rank contexts not built in this version");
     (void)nccl_id;
     (void)rank;
-    if (prob->kind < 0 || prob->kind > 2) throw SolveError(IRKG_ERR_CONFIG, "unknown problem kind");
+    if (prob->kind < 0 || prob->kind > 3) throw SolveError(IRKG_ERR_CONFIG, "unknown problem kind");
+    if (prob->kind == IRKG_KIND_ARAKAWA && (prob->nz != 1 || prob->nx < 3 || prob->ny < 3))
+      throw SolveError(IRKG_ERR_CONFIG, "the vorticity DAE needs a 2-D grid >= 3x3");
     if (prob->nx < 1 || prob->ny < 1 || prob->nz < 1)
       throw SolveError(IRKG_ERR_VALUE, "grid extents must be positive");
     long long n = (long long)prob->nx * prob->ny * prob->nz;
@@ -677,6 +693,7 @@ int irkg_newton_step(irkg_ctx *ctx, const double *u_dev, double *k_dev, double t
   IRKG_GUARD({
     Engine &e = *ctx->eng;
     if (!e.have_tab || !e.have_cfg) throw SolveError(IRKG_ERR_CONFIG, "tableau/solver not set");
+    if (e.dae) throw SolveError(IRKG_ERR_CONFIG, "DAE context: use the irkg_dae_* entry points");
     irkg_krylov_report fr = stats->fail_report;
     memset(stats, 0, offsetof(irkg_step_stats, fail_report));
     stats->fail_report = fr;
@@ -688,6 +705,7 @@ int irkg_step(irkg_ctx *ctx, double *u_dev, double t, double dt, irkg_step_stats
   IRKG_GUARD({
     Engine &e = *ctx->eng;
     if (!e.have_tab || !e.have_cfg) throw SolveError(IRKG_ERR_CONFIG, "tableau/solver not set");
+    if (e.dae) throw SolveError(IRKG_ERR_CONFIG, "DAE context: use the irkg_dae_* entry points");
     irkg_krylov_report fr = stats->fail_report;
     memset(stats, 0, offsetof(irkg_step_stats, fail_report));
     stats->fail_report = fr;
@@ -702,6 +720,7 @@ int irkg_step_host(irkg_ctx *ctx, double *u_host, double t, double dt, irkg_step
   IRKG_GUARD({
     Engine &e = *ctx->eng;
     if (!e.have_tab || !e.have_cfg) throw SolveError(IRKG_ERR_CONFIG, "tableau/solver not set");
+    if (e.dae) throw SolveError(IRKG_ERR_CONFIG, "DAE context: use the irkg_dae_* entry points");
     irkg_krylov_report fr = stats->fail_report;
     memset(stats, 0, offsetof(irkg_step_stats, fail_report));
     stats->fail_report = fr;
@@ -835,6 +854,7 @@ int irkg_prepare_linearization(irkg_ctx *ctx, const double *u_dev, const double 
   IRKG_GUARD({
     Engine &e = *ctx->eng;
     if (!e.have_tab || !e.have_cfg) throw SolveError(IRKG_ERR_CONFIG, "tableau/solver not set");
+    if (e.dae) throw SolveError(IRKG_ERR_CONFIG, "DAE context: use the irkg_dae_* entry points");
     e.stage_values(u_dev, k_dev, dt, e.U);
     e.build_linearization(e.U);
     check(cudaStreamSynchronize(e.stream));
@@ -846,12 +866,74 @@ int irkg_transformed_solve(irkg_ctx *ctx, double dt, const double *rhs_dev, doub
   IRKG_GUARD({
     Engine &e = *ctx->eng;
     if (!e.have_tab || !e.have_cfg) throw SolveError(IRKG_ERR_CONFIG, "tableau/solver not set");
+    if (e.dae) throw SolveError(IRKG_ERR_CONFIG, "DAE context: use the irkg_dae_* entry points");
     if (!(dt > 0.0)) throw SolveError(IRKG_ERR_VALUE, "dt must be positive");
     irkg_krylov_report fr = stats->fail_report;
     memset(stats, 0, offsetof(irkg_step_stats, fail_report));
     stats->fail_report = fr;
     e.transformed_solve(dt, rhs_dev, dk_dev, stats);
     check(cudaStreamSynchronize(e.stream));
+  });
+}
+
+// ------------------------------------------------------------------- DAE
+
+static Engine &dae_engine(irkg_ctx *ctx, bool need_solver) {
+  Engine &e = *ctx->eng;
+  if (!e.dae) throw SolveError(IRKG_ERR_CONFIG, "not a DAE context (kind IRKG_KIND_ARAKAWA)");
+  if (need_solver && (!e.have_tab || !e.have_cfg))
+    throw SolveError(IRKG_ERR_CONFIG, "tableau/solver not set");
+  return e;
+}
+
+static void reset_stats(irkg_step_stats *stats) {
+  irkg_krylov_report fr = stats->fail_report;
+  memset(stats, 0, sizeof(irkg_step_stats));
+  stats->fail_report = fr;
+}
+
+int irkg_dae_stage_residual(irkg_ctx *ctx, const double *uw_dev, const double *k2_dev, double t,
+                            double dt, double *f2_dev, double *norm) {
+  IRKG_GUARD({
+    Engine &e = dae_engine(ctx, false);
+    if (!e.have_tab) throw SolveError(IRKG_ERR_CONFIG, "tableau not set");
+    (void)t;
+    e.stage_values_n(uw_dev, k2_dev, dt, e.U, 2 * e.N);
+    *norm = std::sqrt(e.dae_residual(e.U, k2_dev, f2_dev));
+  });
+}
+
+int irkg_dae_step(irkg_ctx *ctx, double *uw_dev, double t, double dt, irkg_step_stats *stats) {
+  IRKG_GUARD({
+    Engine &e = dae_engine(ctx, true);
+    reset_stats(stats);
+    check(cudaMemsetAsync(e.Kst, 0, (size_t)e.s * 2 * e.N * sizeof(double), e.stream));
+    e.dae_newton(uw_dev, e.Kst, t, dt, stats);
+    e.step_update_n(dt, e.Kst, uw_dev, 2 * e.N);
+    stats->constraint_residual = e.dae_gnorm(uw_dev);
+  });
+}
+
+int irkg_dae_step_host(irkg_ctx *ctx, double *uw_host, double t, double dt,
+                       irkg_step_stats *stats) {
+  IRKG_GUARD({
+    Engine &e = dae_engine(ctx, true);
+    reset_stats(stats);
+    const size_t bytes = 2 * e.N * sizeof(double);
+    check(cudaMemcpyAsync(e.ufield, uw_host, bytes, cudaMemcpyHostToDevice, e.stream));
+    check(cudaMemsetAsync(e.Kst, 0, (size_t)e.s * bytes, e.stream));
+    e.dae_newton(e.ufield, e.Kst, t, dt, stats);
+    e.step_update_n(dt, e.Kst, e.ufield, 2 * e.N);
+    stats->constraint_residual = e.dae_gnorm(e.ufield);
+    check(cudaMemcpyAsync(uw_host, e.ufield, bytes, cudaMemcpyDeviceToHost, e.stream));
+    check(cudaStreamSynchronize(e.stream));
+  });
+}
+
+int irkg_dae_constraint_norm(irkg_ctx *ctx, const double *uw_dev, double *norm) {
+  IRKG_GUARD({
+    Engine &e = dae_engine(ctx, false);
+    *norm = e.dae_gnorm(uw_dev);
   });
 }
 

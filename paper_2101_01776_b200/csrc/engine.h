@@ -129,6 +129,33 @@ struct Engine {
   void block_op_s(const BlockSpec &B, const double *z, double *w, const double *b,
                   double *out_norm, const GCtrl *skip);
   double residual_s(const double *U, const double *K, double *F);
+  // dae.cu (vorticity/streamfunction DAE, reordered mode)
+  bool dae = false;
+  double h2 = 0.0;
+  double *ACC = nullptr, *XU = nullptr, *CR = nullptr, *PT = nullptr;
+  void *fft_buf = nullptr;
+  int fft_fwd = -1, fft_inv = -1;
+  void dae_init();
+  void dae_fini();
+  int dae_grid() const;
+  void constraint_solve(double sigma, const double *c, double *out, double post);
+  void ara_jacobi_chain(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
+                        int in_off, const double *zc, double cpl, double *x_out,
+                        const GCtrl *skip);
+  void ara_block_op(const BlockSpec &B, const double *z, double *w, const double *b,
+                    double *out_norm, const GCtrl *skip);
+  double dae_residual(const double *UW, const double *K2, double *F2);
+  double dae_gnorm(const double *UW);
+  void dae_transformed_solve(double dt, const double *rhs, double *dk, irkg_step_stats *stats);
+  void dae_newton(const double *uw, double *K2, double t, double dt, irkg_step_stats *stats);
+  // generic helpers
+  long long Nst() const { return dae ? 2 * N : N; }
+  void stage_mix_n(const double *M_rowmajor_s, const double *in, double *out, bool accumulate,
+                   long long n);
+  void stage_values_n(const double *u, const double *K, double dt, double *Uo, long long n);
+  void step_update_n(double dt, const double *K, double *u, long long n);
+  void build_weights();
+  static void dalloc_raw(void **p, size_t bytes);
   // jacobi.cu (temporally blocked inner solves, 2-D)
   bool fused_jacobi = true;
   int jspan_override = 0;

@@ -579,11 +579,15 @@ double Engine::norm2(const double *x, long long n, const GCtrl *skip) {
 }
 
 void Engine::stage_values(const double *u, const double *K, double dt, double *U) {
+  stage_values_n(u, K, dt, U, N);
+}
+
+void Engine::stage_values_n(const double *u, const double *K, double dt, double *Uo, long long n) {
   StageConsts A{};
   A.s = s;
   for (int i = 0; i < s; ++i)
     for (int j = 0; j < s; ++j) A.a[i * MAXS + j] = tab.a0[i * IRKG_MAX_STAGES + j];
-  k_stage_values<<<grid_for(N), 256, 0, stream>>>((int)N, s, u, K, A, dt, U);
+  k_stage_values<<<grid_for(n), 256, 0, stream>>>((int)n, s, u, K, A, dt, Uo);
   count(1);
 }
 
@@ -608,19 +612,26 @@ void Engine::opfields(const double *U, const OpWeights &W, double *A) {
 }
 
 void Engine::stage_mix(const double *M_rowmajor_s, const double *in, double *out, bool accumulate) {
+  stage_mix_n(M_rowmajor_s, in, out, accumulate, N);
+}
+
+void Engine::stage_mix_n(const double *M_rowmajor_s, const double *in, double *out,
+                         bool accumulate, long long n) {
   StageConsts M{};
   M.s = s;
   for (int i = 0; i < s; ++i)
     for (int k = 0; k < s; ++k) M.a[i * MAXS + k] = M_rowmajor_s[i * s + k];
-  k_stage_mix<<<grid_for(N), 256, 0, stream>>>((int)N, s, M, in, out, accumulate ? 1 : 0);
+  k_stage_mix<<<grid_for(n), 256, 0, stream>>>((int)n, s, M, in, out, accumulate ? 1 : 0);
   count(1);
 }
 
-void Engine::step_update(double dt, const double *K, double *u) {
+void Engine::step_update(double dt, const double *K, double *u) { step_update_n(dt, K, u, N); }
+
+void Engine::step_update_n(double dt, const double *K, double *u, long long n) {
   StageConsts B{};
   B.s = s;
   for (int i = 0; i < s; ++i) B.v[i] = tab.b0[i];
-  k_step_update<<<grid_for(N), 256, 0, stream>>>((int)N, s, B, dt, K, u);
+  k_step_update<<<grid_for(n), 256, 0, stream>>>((int)n, s, B, dt, K, u);
   count(1);
 }
 
@@ -638,6 +649,10 @@ void Engine::jacobi_chain(const Op &L, double alpha, double dt, int inner, const
                           int in_off, const double *zc, double cpl, double *x_out,
                           const GCtrl *skip) {
   const VecIn &vin = *static_cast<const VecIn *>(vin_p);
+  if (prob.kind == KIND_ARAKAWA) {
+    ara_jacobi_chain(L, alpha, dt, inner, vin, in_off, zc, cpl, x_out, skip);
+    return;
+  }
   if (jacobi_chain_fused(L, alpha, dt, inner, vin, in_off, zc, cpl, x_out, skip)) return;
   const int gb = grid_for(N);
   double *tbuf = zc ? tmp_t : nullptr;
@@ -678,6 +693,10 @@ void Engine::precond(const BlockSpec &B, const void *vin_p, double *z, const GCt
 void Engine::block_op(const BlockSpec &B, const double *z, double *w, const double *b,
                       double *out_norm, const GCtrl *skip) {
   counters.op_bytes += 8.0 * N * B.size * 3.0;
+  if (prob.kind == KIND_ARAKAWA) {
+    ara_block_op(B, z, w, b, out_norm, skip);
+    return;
+  }
   if (ndim >= 2) {
     block_op_s(B, z, w, b, out_norm, skip);
     return;

@@ -23,7 +23,7 @@
 
 namespace irkg {
 
-enum { KIND_NLDIFF = 0, KIND_BURGERS = 1, KIND_RAD = 2 };
+enum { KIND_NLDIFF = 0, KIND_BURGERS = 1, KIND_RAD = 2, KIND_ARAKAWA = 3 };
 
 struct Grid {
   int nx, ny, nz;  // local extents (ny or nz is the slab axis when partitioned)

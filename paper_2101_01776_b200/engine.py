@@ -17,6 +17,7 @@ from . import _lib
 from .config import gamma_code, inner_sweeps
 from .errors import (
     ConfigurationError,
+    IndexViolationError,
     KrylovBreakdownError,
     StageSolveError,
     StepFailureError,
@@ -58,6 +59,8 @@ def _raise(rc, stats_c=None, fail_res=None):
         raise StepFailureError(msg, stats=st)
     if rc == _lib.ERR_BREAKDOWN:
         raise KrylovBreakdownError(msg)
+    if rc == _lib.ERR_INDEX:
+        raise IndexViolationError(msg)
     raise RuntimeError(f"irkg CUDA failure: {msg}")
 
 
@@ -252,6 +255,33 @@ class Context:
                                              C.byref(st))
         self._check(rc, st)
         return st
+
+    # ------------------------------------------------------------- DAE
+    def dae_step_device(self, uw_dev, t, dt):
+        st = self._new_stats()
+        rc = self.lib.irkg_dae_step(self.h, ptr(uw_dev), float(t), float(dt), C.byref(st))
+        self._check(rc, st)
+        return step_stats_from_c(st)
+
+    def dae_step_host(self, uw_host, t, dt):
+        st = self._new_stats()
+        rc = self.lib.irkg_dae_step_host(self.h, uw_host.ctypes.data_as(C.c_void_p), float(t),
+                                         float(dt), C.byref(st))
+        self._check(rc, st)
+        return step_stats_from_c(st)
+
+    def dae_constraint_norm(self, uw_dev):
+        nrm = C.c_double()
+        rc = self.lib.irkg_dae_constraint_norm(self.h, ptr(uw_dev), C.byref(nrm))
+        self._check(rc)
+        return float(nrm.value)
+
+    def dae_stage_residual(self, uw_dev, k2_dev, t, dt, f2_dev):
+        nrm = C.c_double()
+        rc = self.lib.irkg_dae_stage_residual(self.h, ptr(uw_dev), ptr(k2_dev), float(t),
+                                              float(dt), ptr(f2_dev), C.byref(nrm))
+        self._check(rc)
+        return float(nrm.value)
 
     def linearize(self, U_dev, weights):
         m = U_dev.shape[0]

@@ -33,7 +33,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 KINDS = ("nldiff", "burgers", "rad")
-KIND_CODE = {"nldiff": 0, "burgers": 1, "rad": 2}
+KIND_CODE = {"nldiff": 0, "burgers": 1, "rad": 2, "arakawa": 3}
 
 
 @dataclass(frozen=True)
@@ -143,6 +143,90 @@ def fourier_u0(shape, k_lo=1, k_hi=4, sigma=0.1, seed=0):
     return np.ascontiguousarray(u, dtype=np.float64).ravel()
 
 
+@dataclass(frozen=True)
+class VorticityProblem:
+    """2-D incompressible Navier-Stokes in vorticity/streamfunction DAE form
+    (BASELINE configs[4]) -- the device analogue of the reference's
+    ``DaeSystem`` plugin (src/dae.py:52-66), modelled on shear_layer_small
+    (src/problems.py:245-315):
+
+    * differential u = omega:  omega_t = -J(psi, omega) + nu Lap_h omega
+      (Arakawa Jacobian J = (J++ + J+x + Jx+)/3);
+    * algebraic    w = psi:    0 = G = h^2 (Lap_h psi + omega), row 0 pinned
+      to psi_0 (h^2-scaled so the reference's absolute 1e-10 consistency
+      check holds at every n, SURVEY 8a a19);
+    * linearisation with lagged advection: L_u = -J(psi, .) + nu Lap_h,
+      L_w = 0 (reordered mode), G_u = h^2 I (row 0 zero), G_w = h^2 Lap_h
+      with row 0 replaced by e_0.
+    """
+
+    shape: tuple
+    nu: float = 1e-4
+    length: float = 1.0
+    name: str = "vorticity2d"
+
+    def __post_init__(self):
+        shape = tuple(int(n) for n in self.shape)
+        if len(shape) != 2 or min(shape) < 3:
+            raise ValueError(f"vorticity problem needs a 2-D grid >= 3x3, got {self.shape}")
+        object.__setattr__(self, "shape", shape)
+
+    kind = "arakawa"
+
+    @property
+    def dim_u(self):
+        return self.shape[0] * self.shape[1]
+
+    @property
+    def dim_w(self):
+        return self.dim_u
+
+    @property
+    def dim(self):
+        return self.dim_u
+
+    @property
+    def mass(self):
+        return None
+
+    @property
+    def ndim(self):
+        return 2
+
+    c = 0.0
+    lam = 0.0
+    mu = 0.0
+
+
+def pinned_poisson(f, shape, pin_value=0.0, length=1.0):
+    """Solve Lap_h y = f on rows i != 0 with y_0 = pin_value (periodic, x fastest).
+
+    The rows of Lap_h sum to zero, so row 0 of Lap_h y is -sum_{i != 0} f_i; the
+    zero-mean periodic problem is solved spectrally and shifted so y_0 equals
+    the pin.  Used to build the consistent initial streamfunction."""
+    nx, ny = shape
+    fl = np.array(f, dtype=float).ravel()
+    fl[0] = -(fl[1:].sum())
+    hx, hy = length / nx, length / ny
+    kx = np.arange(nx)
+    ky = np.arange(ny)
+    lam = (-4.0 / hx**2) * np.sin(np.pi * kx / nx)[None, :] ** 2 + (
+        -4.0 / hy**2) * np.sin(np.pi * ky / ny)[:, None] ** 2
+    lam[0, 0] = 1.0
+    yh = np.fft.fft2(fl.reshape(ny, nx)) / lam
+    yh[0, 0] = 0.0
+    y = np.real(np.fft.ifft2(yh)).ravel()
+    return y - y[0] + pin_value
+
+
+def vorticity_initial_state(prob, k_lo=2, k_hi=10, sigma=1.0, seed=0):
+    """(omega0, psi0): seeded Fourier-mode vorticity and the streamfunction
+    satisfying the pinned constraint G(omega0, psi0) = 0."""
+    omega0 = fourier_u0(prob.shape, k_lo, k_hi, sigma, seed)
+    psi0 = pinned_poisson(-omega0, prob.shape, 0.0, prob.length)
+    return omega0, psi0
+
+
 # --------------------------------------------------------------- catalog
 
 
@@ -191,6 +275,11 @@ def baseline_config(index, n=None, nsteps=None, family=None, s=None):
         prob = GridProblem("nldiff", (nn, nn, nn))
         spec = RunSpec("cfg3_nldiff3d", prob, family or "gauss", s or 5, 1e-3, nsteps or 5,
                        dict(k_lo=1, k_hi=6, sigma=0.1, seed=0), dict(BASE_SOLVER))
+    elif index == 4:
+        nn = n or 2048
+        prob = VorticityProblem((nn, nn), nu=1e-4)
+        spec = RunSpec("cfg4_vorticity2d", prob, family or "gauss", s or 2, 1e-3, nsteps or 10,
+                       dict(k_lo=2, k_hi=10, sigma=1.0, seed=0), dict(BASE_SOLVER))
     else:
-        raise ValueError(f"no ODE baseline config {index}")
+        raise ValueError(f"no baseline config {index}")
     return spec

@@ -359,3 +359,97 @@ def solve_transformed_system(prep, stage_ops=None, variant=None, dt=None, rhs_st
         stats.reports.append(
             (int(st.block_offset[i]), KrylovReport(its, True, [], its * size)))
     return _out(dk, rhs_stages), stats
+
+
+# ------------------------------------------------------------------ DAE
+
+
+@dataclass
+class DaeIntegrationResult:
+    """src/dae.py:501-517."""
+
+    times: np.ndarray
+    u_states: list
+    w_states: list
+    step_stats: list
+
+    @property
+    def u_final(self):
+        return self.u_states[-1]
+
+    @property
+    def w_final(self):
+        return self.w_states[-1]
+
+    def total(self, attr):
+        return sum(getattr(s, attr) for s in self.step_stats)
+
+
+def _check_dae(sys, mode):
+    if getattr(sys, "kind", None) != "arakawa":
+        raise ConfigurationError("device DAE solves need a VorticityProblem (problems.py)")
+    if mode != "reordered":
+        raise ConfigurationError(
+            "only mode='reordered' runs on the device: the reference's coupled mode hard-codes "
+            "exact differential solves (src/dae.py:140) and ignores PrecondSpec.inner"
+        )
+
+
+def dae_step(sys, u, w, t, dt, tableau, cfg=SolverConfig(), prep=None, mode="reordered"):
+    """One DAE step (src/dae.py:474-498); returns ``(u_next, w_next, StepStats)``."""
+    _check_dae(sys, mode)
+    if str(tableau.family) in SDIRK_FAMILIES:
+        raise ConfigurationError(
+            "DIRK tableaux are not supported on DAE systems; use a fully implicit "
+            "collocation scheme")
+    prep = _prep_for(tableau, prep)
+    ctx = context_for(sys)
+    ctx.set_prep(prep)
+    ctx.set_config(cfg)
+    n = sys.dim_u
+    if _is_torch(u):
+        uw = torch().cat([as_device(u), as_device(w)]).contiguous()
+        stats = ctx.dae_step_device(uw, t, dt)
+        return uw[:n].clone(), uw[n:].clone(), stats
+    uw = np.ascontiguousarray(np.concatenate([np.asarray(u, float), np.asarray(w, float)]))
+    stats = ctx.dae_step_host(uw, t, dt)
+    return uw[:n].copy(), uw[n:].copy(), stats
+
+
+def dae_integrate(sys, u0, w0, t0, t_final, dt, tableau, cfg=SolverConfig(), mode="reordered"):
+    """Fixed-step DAE march (src/dae.py:520-564) with the device-resident state.
+
+    The initial state must satisfy the constraint to 1e-10 (ConfigurationError
+    otherwise); a failing step raises StepFailureError with ``partial``.
+    """
+    _check_dae(sys, mode)
+    prep = _prep_for(tableau)
+    ctx = context_for(sys)
+    ctx.set_prep(prep)
+    ctx.set_config(cfg)
+    n = sys.dim_u
+    uw = torch().cat([as_device(u0), as_device(w0)]).contiguous()
+    g0 = ctx.dae_constraint_norm(uw)
+    if g0 > 1e-10:
+        raise ConfigurationError(f"inconsistent initial condition: |G(u0, w0, t0)| = {g0:.3e}")
+    span = t_final - t0
+    nsteps_f = span / dt
+    nsteps = int(round(nsteps_f))
+    if abs(nsteps_f - nsteps) > 1e-8 * max(1.0, abs(nsteps_f)):
+        raise ConfigurationError(f"(t_final - t0)/dt = {nsteps_f} is not an integer step count")
+    if str(tableau.family) in SDIRK_FAMILIES:
+        raise ConfigurationError("DIRK tableaux are not supported on DAE systems")
+    on_dev = _is_torch(u0)
+    host = (lambda x: x.clone()) if on_dev else (lambda x: x.cpu().numpy())
+    times, us, ws, sts = [t0], [host(uw[:n])], [host(uw[n:])], []
+    for j in range(nsteps):
+        try:
+            st = ctx.dae_step_device(uw, t0 + j * dt, dt)
+        except StepFailureError as exc:
+            exc.partial = DaeIntegrationResult(np.array(times), us, ws, sts)
+            raise
+        sts.append(st)
+        times.append(t0 + (j + 1) * dt)
+        us.append(host(uw[:n]))
+        ws.append(host(uw[n:]))
+    return DaeIntegrationResult(np.array(times), us, ws, sts)

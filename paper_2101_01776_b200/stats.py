@@ -88,6 +88,9 @@ def step_stats_from_c(cs):
             int(cs.block_iterations[i])
         )
     st.wall_time = float(cs.wall_time)
+    st.differential_solves = int(cs.differential_solves)
+    st.constraint_solves = int(cs.constraint_solves)
+    st.constraint_residual = float(cs.constraint_residual)
     return st
 
 

@@ -11,14 +11,29 @@ import numpy as np
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
-def case_names():
+def case_names(dae=False):
     out = []
     for p in sorted(glob.glob(os.path.join(GOLD, "*.json"))):
         name = os.path.basename(p)[:-5]
         if name in ("tableaux", "transformed"):
             continue
+        if name.startswith("dae_") != dae:
+            continue
         out.append(name)
     return out
+
+
+def load_dae_case(name):
+    with open(os.path.join(GOLD, name + ".json")) as fh:
+        meta = json.load(fh)
+    arrs = np.load(os.path.join(GOLD, name + ".npz"))
+    for key in ("u0", "w0", "u_final", "w_final"):
+        meta[key] = arrs[key]
+    for st in meta["steps"]:
+        st["residual_history"] = [float.fromhex(x) for x in st["residual_history"]]
+        st["constraint_residual"] = float.fromhex(st["constraint_residual"])
+        st["block_iterations"] = {int(k): v for k, v in st["block_iterations"].items()}
+    return meta
 
 
 def load_case(name):

@@ -144,3 +144,56 @@ def test_variant3_keys_and_lumping():
             assert (blk.offset + 1, blk.offset) in ow
     picked = sorted(int(np.argmax(np.abs(prep.d[i, i]))) for i in range(4))
     assert picked == [0, 1, 2, 3]
+
+
+# --------------------------------------------------------------- DAE path
+
+from _golden import load_dae_case  # noqa: E402
+
+
+@pytest.mark.parametrize("name", [c for c in case_names(dae=True) if "n128" not in c])
+def test_oracle_dae_matches_reference_run(name):
+    from oracle import dae as odae
+    from oracle.problems import DaeProblemDef
+
+    meta = load_dae_case(name)
+    pd = DaeProblemDef(tuple(meta["shape"]), meta["nu"])
+    sysr = odae.DaeSystem(pd.dim, pd.dim, pd.rhs, pd.constraint, pd.blocks_csr)
+    prep = otab.prepare(meta["family"], meta["s"])
+    us, ws, sts = odae.dae_integrate(sysr, meta["u0"], meta["w0"], 0.0,
+                                     meta["nsteps"] * meta["dt"], meta["dt"], prep,
+                                     oracle_config(meta["solver"]))
+    assert np.linalg.norm(us[-1] - meta["u_final"]) <= 1e-13 * np.linalg.norm(meta["u_final"])
+    assert np.linalg.norm(ws[-1] - meta["w_final"]) <= 1e-12 * np.linalg.norm(meta["w_final"])
+    for got, want in zip(sts, meta["steps"]):
+        assert got.newton_iterations == want["newton_iterations"]
+        assert got.krylov_iterations == want["krylov_iterations"]
+        assert got.differential_solves == want["differential_solves"]
+        assert got.constraint_solves == want["constraint_solves"]
+        assert got.block_iterations == want["block_iterations"]
+        assert got.constraint_residual <= 1e-12
+
+
+def test_vorticity_initial_state_is_consistent():
+    from oracle.problems import DaeProblemDef
+    from paper_2101_01776_b200.problems import VorticityProblem, vorticity_initial_state
+
+    for n in (16, 128, 256):
+        prob = VorticityProblem((n, n))
+        w0, p0 = vorticity_initial_state(prob)
+        g = DaeProblemDef(prob.shape, prob.nu).constraint(w0, p0, 0.0)
+        assert np.linalg.norm(g) <= 1e-10 and p0[0] == 0.0
+
+
+def test_arakawa_matrix_matches_direct_form():
+    from oracle.problems import arakawa_jacobian, arakawa_jacobian_matrix
+
+    rng = np.random.default_rng(0)
+    nx, ny = 9, 7
+    psi, w = rng.standard_normal(nx * ny), rng.standard_normal(nx * ny)
+    m = arakawa_jacobian_matrix(psi, nx, ny, 1 / nx, 1 / ny)
+    np.testing.assert_allclose(m @ w, arakawa_jacobian(psi, w, nx, ny, 1 / nx, 1 / ny),
+                               atol=1e-10)
+    # Arakawa's form conserves energy and enstrophy: sum psi J = sum w J = 0
+    j = arakawa_jacobian(psi, w, nx, ny, 1 / nx, 1 / ny)
+    assert abs(np.dot(psi, j)) < 1e-9 * np.abs(j).sum() and abs(np.dot(w, j)) < 1e-9 * np.abs(j).sum()
