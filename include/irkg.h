@@ -137,7 +137,18 @@ typedef struct {
   double op_bytes;
   double precond_time_ms; /* device time of the inner solves (if timing on) */
   double op_time_ms;      /* device time of the block operator (if timing on) */
+  int64_t halo_exchanges; /* slab-partition halo exchanges issued */
 } irkg_counters;
+
+/* Host-callback transport for the slab partition (alternative to NCCL):
+ * allreduce: in-place sum of `count` doubles at device pointer `dev`;
+ * halo: send my first planes (send_lo) to rank-1 and my last (send_hi) to
+ * rank+1 (periodic ring), receive rank+1's first into recv_hi and rank-1's
+ * last into recv_lo; `count` doubles each.  Called with the stream drained;
+ * must complete before returning. */
+typedef void (*irkg_allreduce_fn)(void *user, double *dev, int count);
+typedef void (*irkg_halo_fn)(void *user, const double *send_lo, const double *send_hi,
+                             double *recv_lo, double *recv_hi, long long count);
 
 const char *irkg_last_error(void);
 const char *irkg_version(void);
@@ -148,6 +159,11 @@ const char *irkg_version(void);
  * Replaces the per-call workspaces of gmres (src/sparsela.py:208-213). */
 int irkg_create(irkg_ctx **out, const irkg_problem *prob, int device, void *stream,
                 const void *nccl_id, int rank, int nranks);
+/* Multi-rank context over host callbacks (nccl_id-free variant of irkg_create):
+ * the slab partition is the same; only the transport differs. */
+int irkg_create_callback(irkg_ctx **out, const irkg_problem *prob, int device, void *stream,
+                         int rank, int nranks, irkg_allreduce_fn allreduce, irkg_halo_fn halo,
+                         void *user);
 int irkg_destroy(irkg_ctx *ctx);
 int irkg_get_local_extent(irkg_ctx *ctx, int *n_local, int *y0, int *ny_local);
 int irkg_nccl_unique_id(void *out128);

@@ -121,7 +121,13 @@ class Counters(C.Structure):
         ("op_bytes", C.c_double),
         ("precond_time_ms", C.c_double),
         ("op_time_ms", C.c_double),
+        ("halo_exchanges", C.c_int64),
     ]
+
+
+ALLREDUCE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_int)
+HALO_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                      C.c_longlong)
 
 
 class OpField(C.Structure):
@@ -136,6 +142,9 @@ _SIGS = {
     "irkg_last_error": (C.c_char_p, []),
     "irkg_version": (C.c_char_p, []),
     "irkg_create": (_I, [C.POINTER(_P), C.POINTER(Problem), _I, _P, _P, _I, _I]),
+    "irkg_create_callback": (
+        _I, [C.POINTER(_P), C.POINTER(Problem), _I, _P, _I, _I, ALLREDUCE_FN, HALO_FN, _P]
+    ),
     "irkg_destroy": (_I, [_P]),
     "irkg_get_local_extent": (_I, [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
     "irkg_nccl_unique_id": (_I, [_P]),

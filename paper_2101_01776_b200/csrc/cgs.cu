@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   GCtrl *ctrl = W.ctrl;
   if (ctrl->cycle_done) {
     // inside the graph WHILE body: make sure the loop terminates
-    if (MODE == CGS_UPD_NORM && use_cond && blockIdx.x == 0 && threadIdx.x == 0)
+    if (MODE == CGS_UPD_NORM && use_cond > 0 && blockIdx.x == 0 && threadIdx.x == 0)
       cudaGraphSetConditional(cond, 0);
     return;
   }
@@ -297,10 +297,11 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   }
   __syncthreads();
   if (tid == 0) {
-    if (MODE == CGS_UPD_NORM) {
+    // use_cond < 0: multi-rank -- the column is finished after the all-reduce
+    if (MODE == CGS_UPD_NORM && use_cond >= 0) {
       __threadfence();
       arnoldi_finish_dev(W);
-      if (use_cond) cudaGraphSetConditional(cond, ctrl->cycle_done ? 0u : 1u);
+      if (use_cond > 0) cudaGraphSetConditional(cond, ctrl->cycle_done ? 0u : 1u);
     }
     *counter = 0u;
   }
@@ -333,6 +334,36 @@ void Engine::cgs(long long n) {
   k_cgs<CGS_UPD_NORM><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c2, wbuf, nullptr,
                                                    part, G, counter, stage, uc, cond_handle);
   count(3);
+}
+
+// Multi-rank CGS2: the same sweeps over the local slab with the partial
+// dot products summed across ranks between them; the Hessenberg column is
+// finished (k_arnoldi_finish) from the global ||w||.  j is known on the host.
+void Engine::cgs_slab(long long n, int j) {
+  const int stage = cgs_stage_doubles();
+  const size_t smem = 2 * (size_t)stage * sizeof(double);
+  if (cgs_smem_set < smem) {
+    check(cudaFuncSetAttribute(k_cgs<CGS_DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem), "smem attr");
+    check(cudaFuncSetAttribute(k_cgs<CGS_UPD_DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem), "smem attr");
+    check(cudaFuncSetAttribute(k_cgs<CGS_UPD_NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem), "smem attr");
+    cgs_smem_set = smem;
+  }
+  const int L = j + 1;
+  k_cgs<CGS_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, nullptr, wbuf, nullptr, part,
+                                              G, counter, stage, 0, cond_handle);
+  allreduce(W.c1, L);
+  allreduce(&ctrl_dev->wn2, 1);
+  k_cgs<CGS_UPD_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c1, wbuf, wbuf, part, G,
+                                                  counter, stage, 0, cond_handle);
+  allreduce(W.c2, L);
+  k_cgs<CGS_UPD_NORM><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c2, wbuf, nullptr,
+                                                   part, G, counter, stage, -1, cond_handle);
+  allreduce(&ctrl_dev->hn2, 1);
+  count(3);
+  arnoldi_finish();
 }
 
 }  // namespace irkg

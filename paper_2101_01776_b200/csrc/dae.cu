@@ -208,18 +208,8 @@ __global__ void k_ara_jac(Grid g, double nu, Op L, double alpha, double dt, VecI
                           const double *__restrict__ t_in, const double *__restrict__ x,
                           double *__restrict__ x_out, const GCtrl *skip) {
   if (skip && skip->cycle_done) return;
-  const double *in = nullptr;
   double scale = 1.0;
-  if (!t_in) {
-    if (vin.ctrl) {
-      const int j = vin.ctrl->j;
-      in = vin.base + (size_t)j * vin.pitch;
-      scale = vin.alpha[j];
-    } else {
-      in = vin.base;
-    }
-    in += in_off;
-  }
+  const double *in = t_in ? nullptr : vin_resolve(vin, in_off, scale).base;
   const double D = alpha - dt * (L.sigma * nu * g.lapdiag);
   const double invD = 1.0 / D;
   ROWS_LOOP(g) {

@@ -29,7 +29,9 @@ static void dalloc(T **p, size_t count) {
   check(cudaMalloc((void **)p, count * sizeof(T)), "cudaMalloc");
 }
 
-Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st) : prob(p), device(dev), stream(st) {
+Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int nranks_,
+               Comm *comm_)
+    : prob(p), device(dev), stream(st), comm(comm_), rank(rank_), nranks(nranks_) {
   check(cudaSetDevice(dev), "cudaSetDevice");
   cudaDeviceProp prop;
   check(cudaGetDeviceProperties(&prop, dev), "props");
@@ -37,11 +39,19 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st) : prob(p), devic
   G = 2 * sms;
   int ext[3] = {p.nx, p.ny, p.nz};
   ndim = (p.nz > 1) ? 3 : (p.ny > 1 ? 2 : 1);
-  grid.nx = p.nx;
-  grid.ny = p.ny;
-  grid.nz = p.nz;
-  grid.nxy = p.nx * p.ny;
-  grid.n = p.nx * p.ny * p.nz;
+  // slab partition of the slowest axis: rank r owns planes [p0, p0 + nl)
+  gplanes = ndim == 3 ? p.nz : p.ny;
+  {
+    const int base = gplanes / nranks, rem = gplanes % nranks;
+    const int nl = base + (rank < rem ? 1 : 0);
+    p0 = rank * base + (rank < rem ? rank : rem);
+    grid.nx = p.nx;
+    grid.ny = ndim == 3 ? p.ny : nl;
+    grid.nz = ndim == 3 ? nl : p.nz;
+  }
+  grid.slab = nranks > 1 ? 1 : 0;
+  grid.nxy = grid.nx * grid.ny;
+  grid.n = grid.nx * grid.ny * grid.nz;
   double lapdiag = 0.0;
   for (int a = 0; a < 3; ++a) {
     double h = p.length / ext[a];
@@ -109,6 +119,8 @@ Engine::~Engine() {
   drop_graphs();
   if (cap_stream) cudaStreamDestroy(cap_stream);
   dae_fini();
+  free_ghosts();
+  delete comm;
 }
 
 void Engine::ensure_stage_buffers() {
@@ -293,7 +305,21 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
   while (!converged && total_it < maxit) {
     int m = std::min(restart, maxit - total_it);
     cycle_init(m);
-    if (use_graphs && !timing) {
+    if (slab()) {
+      // multi-rank: host-driven Arnoldi loop (slot j resolved on the host,
+      // halo exchanges inside precond/block_op, all-reduces inside cgs_slab)
+      for (int it = 0; it < m; ++it) {
+        VecIn vj{V + (size_t)it * vpitch, 0, nullptr, nullptr};
+        vj.scale_ptr = W.alpha + it;
+        precond(B, &vj, zbuf, nullptr);
+        block_op(B, zbuf, wbuf, nullptr, nullptr, nullptr);
+        cgs_slab(n, it);
+        counters.cgs_launches += 3;
+        counters.arnoldi_iterations += 1;
+        read_ctrl();
+        if (ctrl_host->cycle_done) break;
+      }
+    } else if (use_graphs && !timing) {
       // whole Arnoldi loop of this cycle as one graph launch (device-side WHILE)
       CycleGraph &cg = cycle_graph(B, n);
       check(cudaGraphLaunch(cg.ex, stream), "cudaGraphLaunch");
@@ -371,6 +397,9 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
 void Engine::build_linearization(const double *Ust) {
   build_weights();
   opfields(Ust, weights, opA);
+  if (slab())  // operator fields feed stencils (fused Jacobi halo: K-1 planes)
+    for (int o = 0; o < nops; ++o)
+      if (!op_zero[o]) exchange(R_OP + o, opA + (size_t)o * N, jhalo());
 }
 
 void Engine::build_weights() {
@@ -623,6 +652,26 @@ static int fail(int code, const std::string &msg) {
     return fail(IRKG_ERR_CUDA, e.what());                         \
   }
 
+static void validate_problem(const irkg_problem *prob, int rank, int nranks) {
+  if (prob->kind < 0 || prob->kind > 3) throw SolveError(IRKG_ERR_CONFIG, "unknown problem kind");
+  if (prob->kind == IRKG_KIND_ARAKAWA && (prob->nz != 1 || prob->nx < 3 || prob->ny < 3))
+    throw SolveError(IRKG_ERR_CONFIG, "the vorticity DAE needs a 2-D grid >= 3x3");
+  if (prob->nx < 1 || prob->ny < 1 || prob->nz < 1)
+    throw SolveError(IRKG_ERR_VALUE, "grid extents must be positive");
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw SolveError(IRKG_ERR_VALUE, "bad rank/nranks");
+  if (nranks > 1) {
+    const int nd = (prob->nz > 1) ? 3 : (prob->ny > 1 ? 2 : 1);
+    if (nd == 1) throw SolveError(IRKG_ERR_CONFIG, "slab partition needs a 2-D or 3-D grid");
+    if (prob->kind == IRKG_KIND_ARAKAWA)
+      throw SolveError(IRKG_ERR_CONFIG, "the DAE path runs on one rank in this version");
+    const int planes = nd == 3 ? prob->nz : prob->ny;
+    if (planes / nranks < GH)
+      throw SolveError(IRKG_ERR_CONFIG, "slabs must hold at least 6 planes per rank");
+  }
+  const long long nl = ((long long)(nranks > 1 ? 1 : 1)) * prob->nx * prob->ny * prob->nz / nranks + prob->nx * prob->ny;
+  if (2 * nl >= (1LL << 31)) throw SolveError(IRKG_ERR_VALUE, "grid too large for one rank");
+}
+
 extern "C" {
 
 const char *irkg_last_error(void) { return g_last_error.c_str(); }
@@ -631,18 +680,28 @@ const char *irkg_version(void) { return "irkg 0.1 sm_100a"; }
 int irkg_create(irkg_ctx **out, const irkg_problem *prob, int device, void *stream,
                 const void *nccl_id, int rank, int nranks) {
   IRKG_GUARD({
-    if (nranks != 1) throw SolveError(IRKG_ERR_CONFIG, "multi-rank contexts not built in this version");
-    (void)nccl_id;
-    (void)rank;
-    if (prob->kind < 0 || prob->kind > 3) throw SolveError(IRKG_ERR_CONFIG, "unknown problem kind");
-    if (prob->kind == IRKG_KIND_ARAKAWA && (prob->nz != 1 || prob->nx < 3 || prob->ny < 3))
-      throw SolveError(IRKG_ERR_CONFIG, "the vorticity DAE needs a 2-D grid >= 3x3");
-    if (prob->nx < 1 || prob->ny < 1 || prob->nz < 1)
-      throw SolveError(IRKG_ERR_VALUE, "grid extents must be positive");
-    long long n = (long long)prob->nx * prob->ny * prob->nz;
-    if (2 * n >= (1LL << 31)) throw SolveError(IRKG_ERR_VALUE, "grid too large for one rank");
+    validate_problem(prob, rank, nranks);
+    Comm *comm = nullptr;
+    if (nranks > 1) {
+      if (!nccl_id) throw SolveError(IRKG_ERR_VALUE, "nccl_id required when nranks > 1");
+      check(cudaSetDevice(device), "cudaSetDevice");
+      comm = make_nccl_comm(nccl_id, rank, nranks);
+    }
     auto *c = new irkg_ctx;
-    c->eng = new Engine(*prob, device, (cudaStream_t)stream);
+    c->eng = new Engine(*prob, device, (cudaStream_t)stream, rank, nranks, comm);
+    *out = c;
+  });
+}
+
+int irkg_create_callback(irkg_ctx **out, const irkg_problem *prob, int device, void *stream,
+                         int rank, int nranks, irkg_allreduce_fn allreduce, irkg_halo_fn halo,
+                         void *user) {
+  IRKG_GUARD({
+    validate_problem(prob, rank, nranks);
+    if (!allreduce || !halo) throw SolveError(IRKG_ERR_VALUE, "callbacks required");
+    Comm *comm = nranks > 1 ? make_callback_comm(rank, nranks, allreduce, halo, user) : nullptr;
+    auto *c = new irkg_ctx;
+    c->eng = new Engine(*prob, device, (cudaStream_t)stream, rank, nranks, comm);
     *out = c;
   });
 }
@@ -659,17 +718,12 @@ int irkg_destroy(irkg_ctx *ctx) {
 int irkg_get_local_extent(irkg_ctx *ctx, int *n_local, int *y0, int *ny_local) {
   IRKG_GUARD({
     *n_local = (int)ctx->eng->N;
-    *y0 = 0;
-    *ny_local = ctx->eng->ndim == 3 ? ctx->eng->prob.nz : ctx->eng->prob.ny;
+    *y0 = ctx->eng->p0;
+    *ny_local = ctx->eng->local_planes();
   });
 }
 
-int irkg_nccl_unique_id(void *out128) {
-  IRKG_GUARD({
-    memset(out128, 0, 128);
-    throw SolveError(IRKG_ERR_CONFIG, "NCCL not built in this version");
-  });
-}
+int irkg_nccl_unique_id(void *out128) { IRKG_GUARD(nccl_unique_id(out128)); }
 
 int irkg_set_tableau(irkg_ctx *ctx, const irkg_tableau *tab) { IRKG_GUARD(ctx->eng->set_tableau(*tab)); }
 int irkg_set_solver(irkg_ctx *ctx, const irkg_solver *cfg) { IRKG_GUARD(ctx->eng->set_solver(*cfg)); }

@@ -36,6 +36,26 @@ struct BlockSpec {
   Op l1, l2, c12, c21;
 };
 
+// Transport of the slab partition (comm.cu)
+struct Comm {
+  int rank = 0, nranks = 1;
+  virtual ~Comm() {}
+  virtual void allreduce_sum(double *dev, int count, cudaStream_t st) = 0;
+  // send my first `count` values (send_lo) to rank-1 and my last (send_hi) to
+  // rank+1 (periodic); receive rank+1's first into recv_hi, rank-1's last into recv_lo
+  virtual void halo(const double *send_lo, const double *send_hi, double *recv_lo,
+                    double *recv_hi, long long count, cudaStream_t st) = 0;
+};
+Comm *make_nccl_comm(const void *id128, int rank, int nranks);
+Comm *make_callback_comm(int rank, int nranks, irkg_allreduce_fn a, irkg_halo_fn h, void *u);
+void nccl_unique_id(void *out128);
+
+// ghost-buffer roles (one ghost pair per role, re-pointed by exchange())
+enum GhostRole {
+  R_VIN0 = 0, R_VIN1 = 1, R_Z0 = 2, R_Z1 = 3, R_X0 = 4, R_X1 = 5, R_JX = 6,
+  R_STAGE = 16, R_Y = 32, R_OP = 64
+};
+
 struct KrylovOut {
   int iterations = 0;
   int converged = 0;
@@ -94,7 +114,30 @@ struct Engine {
   bool op_zero[MAXOPS];
   OpWeights weights{};
 
-  Engine(const irkg_problem &p, int dev, cudaStream_t st);
+  // slab partition (comm.cu); nranks == 1: periodic wrap, no communication
+  Comm *comm = nullptr;
+  int rank = 0, nranks = 1;
+  int gplanes = 1, p0 = 0;  // global planes along the slab axis, my first plane
+  struct Ghost {
+    double *lo = nullptr, *hi = nullptr;
+    const double *field = nullptr;
+  };
+  std::map<int, Ghost> ghosts;
+  std::map<const double *, int> owner;
+  bool slab() const { return nranks > 1; }
+  int local_planes() const { return ndim == 3 ? grid.nz : grid.ny; }
+  int plane_size() const;
+  Ghost &role(int r);
+  void exchange(int role, const double *f, int depth);
+  void allreduce(double *dev, int count);
+  FRef ref(const double *p) const;
+  Op opref(const Op &o) const;
+  StageGhosts stage_ghosts(const double *Ub, long long stride) const;
+  void free_ghosts();
+  int jhalo() const { return cfg.inner > 1 ? cfg.inner - 1 : 1; }
+
+  Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_ = 0, int nranks_ = 1,
+         Comm *comm_ = nullptr);
   ~Engine();
 
   void set_tableau(const irkg_tableau &t);
@@ -129,6 +172,8 @@ struct Engine {
   void block_op_s(const BlockSpec &B, const double *z, double *w, const double *b,
                   double *out_norm, const GCtrl *skip);
   double residual_s(const double *U, const double *K, double *F);
+  void backsub_s(double dt, BacksubTerms T, const double *gst, const double *y, double *rhs);
+  void cgs_slab(long long n, int j);  // CGS2 with all-reduces between sweeps (multi-rank)
   // dae.cu (vorticity/streamfunction DAE, reordered mode)
   bool dae = false;
   double h2 = 0.0;

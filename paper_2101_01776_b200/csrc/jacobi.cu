@@ -64,22 +64,15 @@ __device__ __forceinline__ double diag_of(const Grid &g, const KindParams &kp, d
 template <int KIND, int K>
 __global__ void __launch_bounds__(JW * 32)
     k_jacobi_chain2d(Grid g, KindParams kp, Op L, double alpha, double dt, VecIn vin, int in_off,
-                     const double *__restrict__ zc, double cpl, double *__restrict__ x_out,
+                     FRef zcr, double cpl, double *__restrict__ x_out,
                      int span, GCtrl *flag_ctrl, const GCtrl *skip) {
   if (skip && skip->cycle_done) return;
   constexpr int H = K - 1;
   constexpr int WCOLS = 32 - 2 * H;  // valid output columns per warp
-  const double *in;
   double scale;
-  if (vin.ctrl) {
-    const int j = vin.ctrl->j;
-    in = vin.base + (size_t)j * vin.pitch;
-    scale = vin.alpha[j];
-  } else {
-    in = vin.base;
-    scale = 1.0;
-  }
-  in += in_off;
+  const FRef inr = vin_resolve(vin, in_off, scale);
+  const FRef ar = fref(L);
+  const bool has_zc = zcr.base != nullptr;
   const int lane = threadIdx.x & 31;
   const int wtile = blockIdx.x * JW + (threadIdx.x >> 5);
   const int x0 = wtile * WCOLS;
@@ -91,10 +84,8 @@ __global__ void __launch_bounds__(JW * 32)
   const bool valid_lane = (lane >= H) && (lane < 32 - H) && (x0 - H + lane < g.nx);
   const int y0 = blockIdx.y * span;
   const int y1 = min(g.ny, y0 + span);
-  const double *a = L.a;
   const double sig = L.sigma;
   const int ny = g.ny;
-  auto wrapy = [&](int y) { return y < 0 ? y + ny : (y >= ny ? y - ny : y); };
 
   // windows (rows relative to the current input row t)
   double A[K + 1];   // a rows t-K .. t
@@ -113,10 +104,17 @@ __global__ void __launch_bounds__(JW * 32)
   const int t0 = y0 - H, t1 = y1 + H;  // input rows [t0, t1)
   auto load_row = [&](int t, double &av, double &rv) {
     if (t < t1) {
-      const int p = wrapy(t) * g.nx + col;
-      av = a[p];
-      double r = scale * in[p];
-      if (zc) r = r + cpl * zc[p];
+      double r;
+      if (!g.slab) {
+        const int p = (t < 0 ? t + ny : (t >= ny ? t - ny : t)) * g.nx + col;
+        av = ar.base[p];
+        r = scale * inr.base[p];
+        if (has_zc) r = r + cpl * zcr.base[p];
+      } else {
+        av = plane_ptr(ar, t, ny, g.nx, 1)[col];
+        r = scale * plane_ptr(inr, t, ny, g.nx, 1)[col];
+        if (has_zc) r = r + cpl * plane_ptr(zcr, t, ny, g.nx, 1)[col];
+      }
       rv = r;
     } else {
       av = 0.0;
@@ -196,7 +194,8 @@ bool Engine::jacobi_chain_fused(const Op &L, double alpha, double dt, int inner,
   const dim3 gr(bx, (grid.ny + span - 1) / span);
   auto go = [&](auto KD, auto KK) {
     k_jacobi_chain2d<decltype(KD)::value, decltype(KK)::value><<<gr, JW * 32, 0, stream>>>(
-        grid, kp, L, alpha, dt, vin, in_off, zc, cpl, x_out, span, ctrl_dev, skip);
+        grid, kp, opref(L), alpha, dt, vin, in_off, zc ? ref(zc) : FRef{nullptr, nullptr, nullptr},
+        cpl, x_out, span, ctrl_dev, skip);
   };
   auto with_k = [&](auto KD) {
     switch (inner) {

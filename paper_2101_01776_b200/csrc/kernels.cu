@@ -219,14 +219,7 @@ __global__ void k_backsub(Grid g, KindParams kp, double dt, BacksubTerms T,
 // ---------------------------------------------------- inner solves / ops
 
 __device__ __forceinline__ void resolve_in(const VecIn &vi, const double *&ptr, double &scale) {
-  if (vi.ctrl) {
-    int j = vi.ctrl->j;
-    ptr = vi.base + (size_t)j * vi.pitch;
-    scale = vi.alpha[j];
-  } else {
-    ptr = vi.base;
-    scale = 1.0;
-  }
+  ptr = vin_resolve(vi, 0, scale).base;
 }
 
 // First damped-Jacobi sweep from x = 0:  x = omega * (r / D)
@@ -572,6 +565,7 @@ void Engine::count(int k) { counters.kernel_launches += k; }
 double Engine::norm2(const double *x, long long n, const GCtrl *skip) {
   k_norm2<256><<<G, 256, 0, stream>>>((int)n, x, part, G, &scal_dev[0], counter, skip);
   count(1);
+  allreduce(&scal_dev[0], 1);
   double v = 0.0;
   check(cudaMemcpyAsync(&v, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost, stream));
   check(cudaStreamSynchronize(stream));
@@ -637,6 +631,17 @@ void Engine::step_update_n(double dt, const double *K, double *u, long long n) {
 
 void Engine::backsub(double dt, const BacksubTerms &T, const double *gst, const double *y,
                      double *rhs) {
+  if (ndim >= 2) {
+    if (slab()) {
+      bool any_od = false;
+      for (int q = 0; q < T.njs; ++q)
+        for (int r = 0; r < T.rows; ++r) any_od |= (T.od[r][q].present != 0);
+      for (int q = 0; q < T.njs && any_od; ++q)
+        exchange(R_Y + T.j[q], y + (size_t)T.j[q] * N, 1);
+    }
+    backsub_s(dt, T, gst, y, rhs);
+    return;
+  }
   dispatch_kd(prob.kind, ndim, [&](auto KD, auto ND) {
     k_backsub<decltype(KD)::value, decltype(ND)::value>
         <<<row_grid(), 256, 0, stream>>>(grid, kp, dt, T, gst, y, rhs);
@@ -668,6 +673,7 @@ void Engine::jacobi_chain(const Op &L, double alpha, double dt, int inner, const
     const double *xin = dst(i - 1);
     double *xo = dst(i);
     if (ndim >= 2) {
+      if (slab()) exchange(R_JX, xin, 1);
       jac_sweep_s(L, alpha, dt, vin, in_off, tbuf, xin, xo, skip);
       continue;
     }
@@ -681,11 +687,27 @@ void Engine::jacobi_chain(const Op &L, double alpha, double dt, int inner, const
 }
 
 void Engine::precond(const BlockSpec &B, const void *vin_p, double *z, const GCtrl *skip) {
+  VecIn vin = *static_cast<const VecIn *>(vin_p);
+  if (slab()) {
+    // the input must be a fixed pointer here (the multi-rank loop resolves
+    // slot j on the host); exchange the halves' boundary planes
+    if (vin.ctrl) throw SolveError(IRKG_ERR_CONFIG, "internal: slot-indexed input in slab mode");
+    const int H = jhalo();
+    exchange(R_VIN0, vin.base, H);
+    vin.lo[0] = role(R_VIN0).lo;
+    vin.hi[0] = role(R_VIN0).hi;
+    if (B.size == 2) {
+      exchange(R_VIN1, vin.base + N, H);
+      vin.lo[1] = role(R_VIN1).lo;
+      vin.hi[1] = role(R_VIN1).hi;
+    }
+  }
   if (B.size == 1) {
-    jacobi_chain(B.l1, B.eta, B.dt, B.inner, vin_p, 0, nullptr, 0.0, z, skip);
+    jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vin, 0, nullptr, 0.0, z, skip);
   } else {
-    jacobi_chain(B.l1, B.eta, B.dt, B.inner, vin_p, 0, nullptr, 0.0, z, skip);
-    jacobi_chain(B.l2, B.gamma, B.dt, B.inner, vin_p, (int)N, z, B.beta * B.beta / B.phi, z + N,
+    jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vin, 0, nullptr, 0.0, z, skip);
+    if (slab()) exchange(R_Z0, z, jhalo());  // z1 feeds the second row's rhs
+    jacobi_chain(B.l2, B.gamma, B.dt, B.inner, &vin, (int)N, z, B.beta * B.beta / B.phi, z + N,
                  skip);
   }
 }
@@ -698,7 +720,12 @@ void Engine::block_op(const BlockSpec &B, const double *z, double *w, const doub
     return;
   }
   if (ndim >= 2) {
+    if (slab()) {
+      exchange(R_X0, z, 1);
+      if (B.size == 2) exchange(R_X1, z + N, 1);
+    }
     block_op_s(B, z, w, b, out_norm, skip);
+    if (b) allreduce(out_norm, 1);
     return;
   }
   dispatch_kd(prob.kind, ndim, [&](auto KD, auto ND) {

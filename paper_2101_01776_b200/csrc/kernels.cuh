@@ -26,7 +26,11 @@ struct Op {
   const double *a;
   double sigma;
   int present;
+  const double *alo = nullptr;  // ghost planes of a (slab mode)
+  const double *ahi = nullptr;
 };
+
+__device__ __forceinline__ FRef fref(const Op &o) { return FRef{o.a, o.alo, o.ahi}; }
 
 // Device-resident GMRES control block (src/sparsela.py:206-272 state).
 struct GCtrl {
@@ -78,6 +82,8 @@ struct BacksubTerms {
   int j[MAXS];
   double coef[2][MAXS];   // R0[r, j]
   Op od[2][MAXS];         // variant-3 coupling operators (present flag)
+  const double *ylo[MAXS];  // ghost planes of y_j (slab mode)
+  const double *yhi[MAXS];
 };
 
 // Resolve the input vector of a preconditioner: a fixed pointer, or the
@@ -87,6 +93,32 @@ struct VecIn {
   long long pitch;   // slot pitch when ctrl != null
   const GCtrl *ctrl; // if set: base + j*pitch, scale alpha[j]
   const double *alpha;
+  const double *scale_ptr = nullptr;       // fixed-pointer input scaled by *scale_ptr
+  const double *lo[2] = {nullptr, nullptr};  // ghost planes of the two halves (slab mode)
+  const double *hi[2] = {nullptr, nullptr};
 };
+
+// ghost planes of the s stage fields (slab mode; unused otherwise)
+struct StageGhosts {
+  const double *lo[MAXS];
+  const double *hi[MAXS];
+};
+
+// Input of an inner solve: basis slot j of the control block scaled by
+// alpha[j] (v_j = alpha_j s_j), or a fixed pointer (scaled by *scale_ptr);
+// returns the half selected by in_off together with its ghost planes.
+__device__ __forceinline__ FRef vin_resolve(const VecIn &vi, int in_off, double &scale) {
+  const double *p;
+  if (vi.ctrl) {
+    const int j = vi.ctrl->j;
+    p = vi.base + (size_t)j * vi.pitch;
+    scale = vi.alpha[j];
+  } else {
+    p = vi.base;
+    scale = vi.scale_ptr ? *vi.scale_ptr : 1.0;
+  }
+  const int h = in_off ? 1 : 0;
+  return FRef{p + in_off, vi.lo[h], vi.hi[h]};
+}
 
 }  // namespace irkg

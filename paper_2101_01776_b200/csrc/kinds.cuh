@@ -32,7 +32,30 @@ struct Grid {
   double ih2[3];   // 1/h^2 per axis, 0 for an axis of extent 1
   double i2h[3];   // 1/(2h) per axis, 0 for an axis of extent 1
   double lapdiag;  // diagonal of Lap: -2 * sum ih2
+  int slab;        // 1: slab-partitioned (ghost planes), 0: periodic wrap locally
 };
+
+// Depth of the ghost-plane buffers (>= Jacobi halo K-1 for K <= 6, and 1).
+constexpr int GH = 6;
+
+// A field and its ghost planes along the slab (slowest) axis.  In slab mode
+// plane -d (1 <= d <= GH) is lo + (GH - d) * P and plane nl + e is hi + e * P;
+// in single-rank mode the accessor wraps periodically inside base.
+struct FRef {
+  const double *base;
+  const double *lo;
+  const double *hi;
+};
+
+__device__ __forceinline__ const double *plane_ptr(const FRef &f, int s, int nl, int P, int slab) {
+  if (!slab) {
+    s = s < 0 ? s + nl : (s >= nl ? s - nl : s);
+    return f.base + (size_t)s * P;
+  }
+  if (s < 0) return f.lo + (size_t)(s + GH) * P;
+  if (s >= nl) return f.hi + (size_t)(s - nl) * P;
+  return f.base + (size_t)s * P;
+}
 
 struct KindParams {
   double nu, c, lam, mu;

@@ -137,22 +137,11 @@ template <int KIND, int NDIM>
 __global__ void __launch_bounds__(SBX) k_jac_sweep_s(Grid g, KindParams kp, Op L, double alpha,
                                                      double dt, VecIn vin, int in_off,
                                                      const double *__restrict__ t_in,
-                                                     const double *__restrict__ x,
-                                                     double *__restrict__ x_out, int span,
-                                                     const GCtrl *skip) {
+                                                     FRef xr, double *__restrict__ x_out,
+                                                     int span, const GCtrl *skip) {
   if (skip && skip->cycle_done) return;
-  const double *in = nullptr;
   double scale = 1.0;
-  if (!t_in) {
-    if (vin.ctrl) {
-      const int j = vin.ctrl->j;
-      in = vin.base + (size_t)j * vin.pitch;
-      scale = vin.alpha[j];
-    } else {
-      in = vin.base;
-    }
-    in += in_off;
-  }
+  const double *in = t_in ? nullptr : vin_resolve(vin, in_off, scale).base;
   int ix, iy;
   const int q = column_q<NDIM>(g, ix, iy);
   if (q < 0) return;
@@ -161,21 +150,20 @@ __global__ void __launch_bounds__(SBX) k_jac_sweep_s(Grid g, KindParams kp, Op L
   const int s0 = (NDIM == 2 ? blockIdx.y : blockIdx.z) * span;
   const int s1 = min(sl.NS, s0 + span);
   const double *a = L.a;
+  const double *x = xr.base;
+  const FRef ar = fref(L);
+  auto at = [&](const FRef &f, int s) { return plane_ptr(f, s, sl.NS, sl.P, g.slab)[q]; };
   Win wx, wa;
-  {
-    const int pm = wrap_plane(s0 - 1, sl.NS) * sl.P + q, pc = s0 * sl.P + q;
-    wx.m = x[pm];
-    wx.c = x[pc];
-    if (a_stencil<KIND>()) {
-      wa.m = a[pm];
-      wa.c = a[pc];
-    }
+  wx.m = at(xr, s0 - 1);
+  wx.c = x[s0 * sl.P + q];
+  if (a_stencil<KIND>()) {
+    wa.m = at(ar, s0 - 1);
+    wa.c = a[s0 * sl.P + q];
   }
   for (int s = s0; s < s1; ++s) {
     const int p = s * sl.P + q;
-    const int pn = wrap_plane(s + 1, sl.NS) * sl.P + q;
-    wx.p = x[pn];
-    if (a_stencil<KIND>()) wa.p = a[pn];
+    wx.p = at(xr, s + 1);
+    if (a_stencil<KIND>()) wa.p = at(ar, s + 1);
     const double r = t_in ? t_in[p] : scale * in[p];
     Nb xn = gather<NDIM>(wx, x, p, o);
     Nb an;
@@ -204,7 +192,7 @@ __global__ void __launch_bounds__(SBX) k_jac_sweep_s(Grid g, KindParams kp, Op L
 template <int KIND, int NDIM, int SIZE>
 __global__ void __launch_bounds__(SBX)
     k_block_op_s(Grid g, KindParams kp, double eta, double beta, double phi, double dt, Op l1,
-                 Op l2, Op c12, Op c21, const double *__restrict__ z, double *__restrict__ w,
+                 Op l2, Op c12, Op c21, FRef z1r, FRef z2r, double *__restrict__ w,
                  const double *__restrict__ b, int span, double *part, unsigned *counter,
                  double *out_norm, const GCtrl *skip) {
   if (skip && skip->cycle_done) return;
@@ -217,32 +205,44 @@ __global__ void __launch_bounds__(SBX)
     const InPlane o = in_plane<NDIM>(g, ix, iy);
     const int s0 = (NDIM == 2 ? blockIdx.y : blockIdx.z) * span;
     const int s1 = min(sl.NS, s0 + span);
-    const double *z1 = z, *z2 = z + n;
+    const double *z1 = z1r.base, *z2 = z2r.base;
     constexpr bool AS = a_stencil<KIND>();
     const bool h12 = SIZE == 2 && c12.present, h21 = SIZE == 2 && c21.present;
-    Win w1{}, w2{}, wa1{}, wa2{}, wc12{}, wc21{};
-    auto init = [&](Win &wv, const double *f) {
-      wv.m = f[wrap_plane(s0 - 1, sl.NS) * sl.P + q];
-      wv.c = f[s0 * sl.P + q];
+    const FRef a1r = fref(l1), a2r = fref(l2), c12r = fref(c12), c21r = fref(c21);
+    // plane s of field f: one wrapped index shared by all fields (single rank)
+    // or the ghost-aware pointer (slab mode)
+    int pw = 0;
+    auto at = [&](const FRef &f, int s) {
+      return g.slab ? plane_ptr(f, s, sl.NS, sl.P, 1)[q] : f.base[pw];
     };
-    init(w1, z1);
-    if (AS) init(wa1, l1.a);
+    auto wrap_idx = [&](int s) {
+      s = s < 0 ? s + sl.NS : (s >= sl.NS ? s - sl.NS : s);
+      return s * sl.P + q;
+    };
+    Win w1{}, w2{}, wa1{}, wa2{}, wc12{}, wc21{};
+    auto init = [&](Win &wv, const FRef &f) {
+      wv.m = at(f, s0 - 1);
+      wv.c = f.base[s0 * sl.P + q];
+    };
+    pw = wrap_idx(s0 - 1);
+    init(w1, z1r);
+    if (AS) init(wa1, a1r);
     if (SIZE == 2) {
-      init(w2, z2);
-      if (AS) init(wa2, l2.a);
-      if (AS && h12) init(wc12, c12.a);
-      if (AS && h21) init(wc21, c21.a);
+      init(w2, z2r);
+      if (AS) init(wa2, a2r);
+      if (AS && h12) init(wc12, c12r);
+      if (AS && h21) init(wc21, c21r);
     }
     for (int s = s0; s < s1; ++s) {
       const int p = s * sl.P + q;
-      const int pn = wrap_plane(s + 1, sl.NS) * sl.P + q;
-      w1.p = z1[pn];
-      if (AS) wa1.p = l1.a[pn];
+      pw = wrap_idx(s + 1);
+      w1.p = at(z1r, s + 1);
+      if (AS) wa1.p = at(a1r, s + 1);
       if (SIZE == 2) {
-        w2.p = z2[pn];
-        if (AS) wa2.p = l2.a[pn];
-        if (AS && h12) wc12.p = c12.a[pn];
-        if (AS && h21) wc21.p = c21.a[pn];
+        w2.p = at(z2r, s + 1);
+        if (AS) wa2.p = at(a2r, s + 1);
+        if (AS && h12) wc12.p = at(c12r, s + 1);
+        if (AS && h21) wc21.p = at(c21r, s + 1);
       }
       auto field = [&](const Win &wv, const double *f) {
         Nb r;
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(SBX)
 // F_i = N(U_i) - K_i, ||F||^2   (src/nonlinear.py:148-152)
 template <int KIND, int NDIM>
 __global__ void __launch_bounds__(SBX)
-    k_residual_s(Grid g, KindParams kp, int s_st, const double *__restrict__ U,
+    k_residual_s(Grid g, KindParams kp, int s_st, const double *__restrict__ U, StageGhosts ug,
                  const double *__restrict__ K, double *__restrict__ F, int span, double *part,
                  unsigned *counter, double *out) {
   const int n = g.n;
@@ -315,12 +315,14 @@ __global__ void __launch_bounds__(SBX)
     const int s1 = min(sl.NS, s0 + span);
     for (int i = 0; i < s_st; ++i) {
       const double *u = U + (size_t)i * n;
+      const FRef ur{u, ug.lo[i], ug.hi[i]};
+      auto at = [&](int s) { return plane_ptr(ur, s, sl.NS, sl.P, g.slab)[q]; };
       Win wu;
-      wu.m = u[wrap_plane(s0 - 1, sl.NS) * sl.P + q];
+      wu.m = at(s0 - 1);
       wu.c = u[s0 * sl.P + q];
       for (int s = s0; s < s1; ++s) {
         const int p = s * sl.P + q;
-        wu.p = u[wrap_plane(s + 1, sl.NS) * sl.P + q];
+        wu.p = at(s + 1);
         const Nb un = gather<NDIM>(wu, u, p, o);
         const double f = rhs_nb<KIND, NDIM>(g, kp, un) - K[(size_t)i * n + p];
         F[(size_t)i * n + p] = f;
@@ -332,6 +334,67 @@ __global__ void __launch_bounds__(SBX)
   }
   const int nblk = gridDim.x * gridDim.y * gridDim.z;
   cta_reduce_store(acc, part, nblk, counter, out);
+}
+
+// ------------------------------------------------ back-substitution rhs
+// acc_r = g_r - sum_j R0[r,j] y_j + dt sum_j od(r,j) y_j (src/irk_core.py:273-283),
+// neighbours gathered directly (called once per block per Newton iteration).
+template <int NDIM>
+__device__ __forceinline__ Nb gather_direct(const FRef &f, int s, int q, int p, const InPlane &o,
+                                            const Slide &sl, int slab) {
+  Nb n;
+  n.c = f.base[p];
+  n.v[0] = f.base[p + o.dxm];
+  n.v[1] = f.base[p + o.dxp];
+  const double m = plane_ptr(f, s - 1, sl.NS, sl.P, slab)[q];
+  const double pp = plane_ptr(f, s + 1, sl.NS, sl.P, slab)[q];
+  if (NDIM == 2) {
+    n.v[2] = m;
+    n.v[3] = pp;
+    n.v[4] = n.v[5] = 0.0;
+  } else {
+    n.v[2] = f.base[p + o.dym];
+    n.v[3] = f.base[p + o.dyp];
+    n.v[4] = m;
+    n.v[5] = pp;
+  }
+  return n;
+}
+
+template <int KIND, int NDIM>
+__global__ void __launch_bounds__(SBX)
+    k_backsub_s(Grid g, KindParams kp, double dt, BacksubTerms T, const double *__restrict__ gst,
+                const double *__restrict__ y, double *__restrict__ rhs, int span) {
+  const int n = g.n;
+  int ix, iy;
+  const int q = column_q<NDIM>(g, ix, iy);
+  if (q < 0) return;
+  const Slide sl = slide_of<NDIM>(g);
+  const InPlane o = in_plane<NDIM>(g, ix, iy);
+  const int s0 = (NDIM == 2 ? blockIdx.y : blockIdx.z) * span;
+  const int s1 = min(sl.NS, s0 + span);
+  for (int s = s0; s < s1; ++s) {
+    const int p = s * sl.P + q;
+    for (int r = 0; r < T.rows; ++r) {
+      double acc = gst[(size_t)(T.row0 + r) * n + p];
+      for (int qq = 0; qq < T.njs; ++qq) {
+        const FRef yr{y + (size_t)T.j[qq] * n, T.ylo[qq], T.yhi[qq]};
+        const double c = T.coef[r][qq];
+        if (c != 0.0) acc -= c * yr.base[p];
+        const Op od = T.od[r][qq];
+        if (od.present) {
+          const Nb xn = gather_direct<NDIM>(yr, s, q, p, o, sl, g.slab);
+          Nb an;
+          if (a_stencil<KIND>())
+            an = gather_direct<NDIM>(fref(od), s, q, p, o, sl, g.slab);
+          else
+            an.c = od.a[p];
+          acc += dt * lx_nb<KIND, NDIM>(g, kp, an, od.sigma, xn);
+        }
+      }
+      rhs[(size_t)r * n + p] = acc;
+    }
+  }
 }
 
 // ============================================================ launchers
@@ -375,7 +438,8 @@ void Engine::jac_sweep_s(const Op &L, double alpha, double dt, const VecIn &vin,
   const dim3 gr = slide_grid(span);
   dispatch_kd23(prob.kind, ndim, [&](auto KD, auto ND) {
     k_jac_sweep_s<decltype(KD)::value, decltype(ND)::value>
-        <<<gr, SBX, 0, stream>>>(grid, kp, L, alpha, dt, vin, in_off, t_in, x, x_out, span, skip);
+        <<<gr, SBX, 0, stream>>>(grid, kp, opref(L), alpha, dt, vin, in_off, t_in, ref(x), x_out,
+                                 span, skip);
   });
   count(1);
 }
@@ -387,13 +451,31 @@ void Engine::block_op_s(const BlockSpec &B, const double *z, double *w, const do
   dispatch_kd23(prob.kind, ndim, [&](auto KD, auto ND) {
     constexpr int K_ = decltype(KD)::value, D_ = decltype(ND)::value;
     if (B.size == 1)
-      k_block_op_s<K_, D_, 1><<<gr, SBX, 0, stream>>>(grid, kp, B.eta, B.beta, B.phi, B.dt, B.l1,
-                                                      B.l2, B.c12, B.c21, z, w, b, span, part,
-                                                      counter, out_norm, skip);
+      k_block_op_s<K_, D_, 1><<<gr, SBX, 0, stream>>>(
+          grid, kp, B.eta, B.beta, B.phi, B.dt, opref(B.l1), opref(B.l2), opref(B.c12),
+          opref(B.c21), ref(z), FRef{nullptr, nullptr, nullptr}, w, b, span, part, counter,
+          out_norm, skip);
     else
-      k_block_op_s<K_, D_, 2><<<gr, SBX, 0, stream>>>(grid, kp, B.eta, B.beta, B.phi, B.dt, B.l1,
-                                                      B.l2, B.c12, B.c21, z, w, b, span, part,
-                                                      counter, out_norm, skip);
+      k_block_op_s<K_, D_, 2><<<gr, SBX, 0, stream>>>(
+          grid, kp, B.eta, B.beta, B.phi, B.dt, opref(B.l1), opref(B.l2), opref(B.c12),
+          opref(B.c21), ref(z), ref(z + N), w, b, span, part, counter, out_norm, skip);
+  });
+  count(1);
+}
+
+void Engine::backsub_s(double dt, BacksubTerms T, const double *gst, const double *y,
+                       double *rhs) {
+  int span;
+  const dim3 gr = slide_grid(span);
+  for (int qq = 0; qq < T.njs; ++qq) {
+    const FRef f = ref(y + (size_t)T.j[qq] * N);
+    T.ylo[qq] = f.lo;
+    T.yhi[qq] = f.hi;
+    for (int r = 0; r < T.rows; ++r) T.od[r][qq] = opref(T.od[r][qq]);
+  }
+  dispatch_kd23(prob.kind, ndim, [&](auto KD, auto ND) {
+    k_backsub_s<decltype(KD)::value, decltype(ND)::value>
+        <<<gr, SBX, 0, stream>>>(grid, kp, dt, T, gst, y, rhs, span);
   });
   count(1);
 }
@@ -401,11 +483,15 @@ void Engine::block_op_s(const BlockSpec &B, const double *z, double *w, const do
 double Engine::residual_s(const double *Ust, const double *K, double *Fo) {
   int span;
   const dim3 gr = slide_grid(span);
+  if (slab())
+    for (int i = 0; i < s; ++i) exchange(R_STAGE + i, Ust + (size_t)i * N, 1);
   dispatch_kd23(prob.kind, ndim, [&](auto KD, auto ND) {
     k_residual_s<decltype(KD)::value, decltype(ND)::value>
-        <<<gr, SBX, 0, stream>>>(grid, kp, s, Ust, K, Fo, span, part, counter, &scal_dev[0]);
+        <<<gr, SBX, 0, stream>>>(grid, kp, s, Ust, stage_ghosts(Ust, N), K, Fo, span, part,
+                                 counter, &scal_dev[0]);
   });
   count(1);
+  allreduce(&scal_dev[0], 1);
   double v = 0.0;
   check(cudaMemcpyAsync(&v, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost, stream));
   check(cudaStreamSynchronize(stream));

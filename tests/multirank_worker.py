@@ -1,0 +1,88 @@
+"""Worker for the multi-rank GPU test (launched by torch.distributed.run).
+
+Every rank runs the slab-partitioned CUDA engine on its slab (host-callback
+transport over gloo, so several ranks can share one GPU without any kernel
+waiting on another rank); rank 0 also runs the same integration on one rank
+and writes both results to ``--out``.
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kind", default="burgers")
+    ap.add_argument("--shape", default="64,64")
+    ap.add_argument("--family", default="gauss")
+    ap.add_argument("--stages", type=int, default=3)
+    ap.add_argument("--dt", type=float, default=5e-4)
+    ap.add_argument("--nsteps", type=int, default=2)
+    ap.add_argument("--transport", default="callback")
+    ap.add_argument("--out", required=True)
+    args = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2101_01776_b200 as pk
+    from paper_2101_01776_b200.distributed import SlabContext, gather, scatter
+
+    rank = int(os.environ["RANK"])
+    ws = int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
+    backend = "gloo" if args.transport == "callback" else "nccl"
+    dist.init_process_group(backend)
+    shape = tuple(int(x) for x in args.shape.split(","))
+    params = {"burgers": dict(nu=1e-2), "nldiff": {}, "rad": dict(nu=0.01, c=0.3, lam=-0.2)}
+    prob = pk.GridProblem(args.kind, shape, **params[args.kind])
+    u0 = pk.fourier_u0(shape, 1, 4, 0.5 if args.kind == "burgers" else 0.1, 0)
+    tab = pk.make_tableau(args.family, args.stages)
+    prep = pk.prepare_stages(tab)
+    cfg = pk.SolverConfig(krylov_maxit=5000, precond=pk.PrecondSpec(inner=4))
+
+    ctx = SlabContext(prob, rank, ws, transport=args.transport)
+    ctx.set_prep(prep)
+    ctx.set_config(cfg)
+    u = torch.from_numpy(np.ascontiguousarray(scatter(u0, shape, rank, ws))).cuda()
+    stats = []
+    for j in range(args.nsteps):
+        st = ctx.step_device(u, j * args.dt, args.dt)
+        stats.append([st.newton_iterations, st.krylov_iterations,
+                      {str(k): v for k, v in st.block_iterations.items()}])
+    local = u.cpu().numpy()
+    parts = [None] * ws
+    dist.all_gather_object(parts, local)
+    halos = ctx.counters()["halo_exchanges"]
+    ctx.close()
+    if rank == 0:
+        uglob = gather(parts, shape)
+        from paper_2101_01776_b200.engine import Context
+
+        single = Context(prob)
+        single.set_prep(prep)
+        single.set_config(cfg)
+        us = torch.from_numpy(u0).cuda()
+        sstats = []
+        for j in range(args.nsteps):
+            st = single.step_device(us, j * args.dt, args.dt)
+            sstats.append([st.newton_iterations, st.krylov_iterations,
+                           {str(k): v for k, v in st.block_iterations.items()}])
+        ref = us.cpu().numpy()
+        rel = float(np.linalg.norm(uglob - ref) / np.linalg.norm(ref))
+        with open(args.out, "w") as fh:
+            json.dump({"rel": rel, "stats": stats, "single_stats": sstats, "halos": halos,
+                       "world": ws}, fh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
