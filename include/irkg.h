@@ -58,6 +58,7 @@ typedef struct {
   int nx, ny, nz;        /* global extents; 1 for absent axes */
   double length;         /* periodic box side per axis (h = length / n) */
   double nu, c, lam, mu; /* kind parameters */
+  double length_y, length_z; /* per-axis box sides (0: same as length) */
 } irkg_problem;
 
 /* Prepared stage constants: ButcherTableau + StagePrep

@@ -37,6 +37,8 @@ class Problem(C.Structure):
         ("c", C.c_double),
         ("lam", C.c_double),
         ("mu", C.c_double),
+        ("length_y", C.c_double),
+        ("length_z", C.c_double),
     ]
 
 

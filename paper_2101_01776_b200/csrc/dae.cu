@@ -398,7 +398,8 @@ void Engine::dae_init() {
   dalloc_raw((void **)&CR, sizeof(double) * N);
   dalloc_raw((void **)&PT, sizeof(double) * N);
   dalloc_raw((void **)&fft_buf, sizeof(cufftDoubleComplex) * (size_t)grid.ny * (grid.nx / 2 + 1));
-  h2 = (prob.length / grid.nx) * (prob.length / grid.ny);
+  h2 = (prob.length / grid.nx) *
+       ((prob.length_y > 0.0 ? prob.length_y : prob.length) / grid.ny);
   cufftHandle p1, p2;
   if (cufftPlan2d(&p1, grid.ny, grid.nx, CUFFT_D2Z) != CUFFT_SUCCESS ||
       cufftPlan2d(&p2, grid.ny, grid.nx, CUFFT_Z2D) != CUFFT_SUCCESS)

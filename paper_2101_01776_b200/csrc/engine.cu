@@ -30,8 +30,9 @@ static void dalloc(T **p, size_t count) {
 }
 
 Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int nranks_,
-               Comm *comm_)
-    : prob(p), device(dev), stream(st), comm(comm_), rank(rank_), nranks(nranks_) {
+               Comm *comm_, bool force_slab)
+    : prob(p), device(dev), stream(st), comm(comm_), rank(rank_), nranks(nranks_),
+      slab_forced(force_slab) {
   check(cudaSetDevice(dev), "cudaSetDevice");
   cudaDeviceProp prop;
   check(cudaGetDeviceProperties(&prop, dev), "props");
@@ -49,12 +50,14 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
     grid.ny = ndim == 3 ? p.ny : nl;
     grid.nz = ndim == 3 ? nl : p.nz;
   }
-  grid.slab = nranks > 1 ? 1 : 0;
+  grid.slab = slab() ? 1 : 0;
   grid.nxy = grid.nx * grid.ny;
   grid.n = grid.nx * grid.ny * grid.nz;
   double lapdiag = 0.0;
   for (int a = 0; a < 3; ++a) {
-    double h = p.length / ext[a];
+    const double len = (a == 1 && p.length_y > 0.0) ? p.length_y
+                       : (a == 2 && p.length_z > 0.0) ? p.length_z : p.length;
+    double h = len / ext[a];
     if (ext[a] > 1) {
       grid.ih2[a] = 1.0 / (h * h);
       grid.i2h[a] = 1.0 / (2.0 * h);
@@ -313,7 +316,15 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
         vj.scale_ptr = W.alpha + it;
         precond(B, &vj, zbuf, nullptr);
         block_op(B, zbuf, wbuf, nullptr, nullptr, nullptr);
-        cgs_slab(n, it);
+        if (timing) check(cudaEventRecord(ev0, stream));
+        cgs_slab(n, it);  // includes the all-reduces between the sweeps
+        if (timing) {
+          check(cudaEventRecord(ev1, stream));
+          check(cudaEventSynchronize(ev1), "sync");
+          float ms = 0.f;
+          check(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
+          counters.cgs_time_ms += ms;
+        }
         counters.cgs_launches += 3;
         counters.arnoldi_iterations += 1;
         read_ctrl();
@@ -682,13 +693,18 @@ int irkg_create(irkg_ctx **out, const irkg_problem *prob, int device, void *stre
   IRKG_GUARD({
     validate_problem(prob, rank, nranks);
     Comm *comm = nullptr;
-    if (nranks > 1) {
+    // IRKG_FORCE_SLAB=1 with one rank: slab mode over a 1-rank NCCL ring (self
+    // send/recv) -- exercises the NCCL transport on a single GPU
+    const char *fs = getenv("IRKG_FORCE_SLAB");
+    const bool force = nranks == 1 && nccl_id && fs && atoi(fs) != 0;
+    if (nranks > 1 || force) {
       if (!nccl_id) throw SolveError(IRKG_ERR_VALUE, "nccl_id required when nranks > 1");
       check(cudaSetDevice(device), "cudaSetDevice");
       comm = make_nccl_comm(nccl_id, rank, nranks);
     }
     auto *c = new irkg_ctx;
-    c->eng = new Engine(*prob, device, (cudaStream_t)stream, rank, nranks, comm);
+    Engine *e = new Engine(*prob, device, (cudaStream_t)stream, rank, nranks, comm, force);
+    c->eng = e;
     *out = c;
   });
 }

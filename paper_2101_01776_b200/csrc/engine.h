@@ -124,7 +124,8 @@ struct Engine {
   };
   std::map<int, Ghost> ghosts;
   std::map<const double *, int> owner;
-  bool slab() const { return nranks > 1; }
+  bool slab_forced = false;  // 1-rank slab mode over the transport (tests the NCCL path)
+  bool slab() const { return nranks > 1 || slab_forced; }
   int local_planes() const { return ndim == 3 ? grid.nz : grid.ny; }
   int plane_size() const;
   Ghost &role(int r);
@@ -137,7 +138,7 @@ struct Engine {
   int jhalo() const { return cfg.inner > 1 ? cfg.inner - 1 : 1; }
 
   Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_ = 0, int nranks_ = 1,
-         Comm *comm_ = nullptr);
+         Comm *comm_ = nullptr, bool force_slab = false);
   ~Engine();
 
   void set_tableau(const irkg_tableau &t);

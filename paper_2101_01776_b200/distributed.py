@@ -23,8 +23,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .engine import Context, _raise, torch
-from .problems import KIND_CODE
+from .engine import Context, _raise, problem_struct, torch
 
 
 def slab_range(planes, rank, nranks):
@@ -128,15 +127,7 @@ class SlabContext(Context):
         dev = t.cuda.current_device() if device is None else int(device)
         self.device = dev
         self.stream = t.cuda.current_stream(dev)
-        shape = tuple(problem.shape) + (1,) * (3 - len(problem.shape))
-        p = _lib.Problem()
-        p.kind = KIND_CODE[problem.kind]
-        p.nx, p.ny, p.nz = (int(x) for x in shape)
-        p.length = float(problem.length)
-        p.nu = float(problem.nu)
-        p.c = float(problem.c)
-        p.lam = float(problem.lam)
-        p.mu = float(problem.mu)
+        p = problem_struct(problem)
         h = C.c_void_p()
         self.rank, self.nranks = int(rank), int(nranks)
         if transport == "callback":

@@ -111,6 +111,24 @@ def tableau_struct(prep):
     return out
 
 
+def problem_struct(problem):
+    """Pack a GridProblem / VorticityProblem into the C irkg_problem."""
+    shape = tuple(problem.shape) + (1,) * (3 - len(problem.shape))
+    p = _lib.Problem()
+    p.kind = KIND_CODE[problem.kind]
+    p.nx, p.ny, p.nz = (int(x) for x in shape)
+    box = getattr(problem, "box", None) or (problem.length,) * len(problem.shape)
+    box = tuple(box) + (problem.length,) * (3 - len(box))
+    p.length = float(box[0])
+    p.length_y = float(box[1])
+    p.length_z = float(box[2])
+    p.nu = float(problem.nu)
+    p.c = float(problem.c)
+    p.lam = float(problem.lam)
+    p.mu = float(problem.mu)
+    return p
+
+
 def solver_struct(cfg):
     out = _lib.Solver()
     out.variant = int(cfg.variant)
@@ -141,15 +159,7 @@ class Context:
         dev = t.cuda.current_device() if device is None else int(device)
         self.device = dev
         self.stream = t.cuda.current_stream(dev)
-        shape = tuple(problem.shape) + (1,) * (3 - len(problem.shape))
-        p = _lib.Problem()
-        p.kind = KIND_CODE[problem.kind]
-        p.nx, p.ny, p.nz = (int(x) for x in shape)
-        p.length = float(problem.length)
-        p.nu = float(problem.nu)
-        p.c = float(problem.c)
-        p.lam = float(problem.lam)
-        p.mu = float(problem.mu)
+        p = problem_struct(problem)
         h = C.c_void_p()
         rc = self.lib.irkg_create(C.byref(h), C.byref(p), dev,
                                   C.c_void_p(self.stream.cuda_stream), None, 0, 1)

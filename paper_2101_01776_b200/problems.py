@@ -46,8 +46,11 @@ class GridProblem:
     mu: float = 0.0
     length: float = 1.0
     name: str = ""
+    lengths: tuple = None  # per-axis box sides (default: ``length`` on every axis)
 
     def __post_init__(self):
+        if self.lengths is not None:
+            object.__setattr__(self, "lengths", tuple(float(x) for x in self.lengths))
         if self.kind not in KINDS:
             raise ValueError(f"unknown problem kind {self.kind!r}; available: {KINDS}")
         shape = tuple(int(n) for n in self.shape)
@@ -70,12 +73,16 @@ class GridProblem:
         return len(self.shape)
 
     @property
+    def box(self):
+        return self.lengths if self.lengths is not None else (self.length,) * self.ndim
+
+    @property
     def h(self):
-        return tuple(self.length / n for n in self.shape)
+        return tuple(L / n for L, n in zip(self.box, self.shape))
 
     def oracle_params(self):
         """Keyword arguments for ``oracle.problems.build_problem`` (tests only)."""
-        p = {"lengths": (self.length,) * self.ndim}
+        p = {"lengths": self.box}
         if self.kind == "burgers":
             p["nu"] = self.nu
         elif self.kind == "rad":

@@ -24,13 +24,14 @@ def _free_port():
     return port
 
 
-def _run(tmp_path, nproc, *args):
+def _run(tmp_path, nproc, *args, env=None):
     out = tmp_path / "mr.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
            f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "multirank_worker.py"),
            "--out", str(out), *args]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env=dict(os.environ, **(env or {})))
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     with open(out) as fh:
         return json.load(fh)
@@ -49,4 +50,15 @@ def test_slab_partition_matches_single_rank(tmp_path, nproc, args):
     for got, want in zip(r["stats"], r["single_stats"]):
         assert got[0] == want[0], (got, want)
         assert abs(got[1] - want[1]) <= want[0], (got, want)
+    assert r["halos"] > 0
+
+
+def test_nccl_transport_single_gpu_ring(tmp_path):
+    """The native NCCL transport (dlopen'ed libnccl, grouped send/recv halos,
+    ncclAllReduce) on a 1-rank ring: slab mode forced, ghost planes arrive
+    through NCCL self send/recv; must equal the plain periodic run."""
+    r = _run(tmp_path, 1, "--kind", "burgers", "--shape", "64,64", "--transport", "nccl",
+             env={"IRKG_FORCE_SLAB": "1"})
+    assert r["rel"] <= 1e-12, r
+    assert [s[0] for s in r["stats"]] == [s[0] for s in r["single_stats"]]
     assert r["halos"] > 0
