@@ -7,11 +7,17 @@
 //     UPD_DOT   w1 = w - V c1 (written back), c2 = V^T w1      (V tile read once)
 //     UPD_NORM  s_{j+1} = w1 - V c2, ||s_{j+1}||^2; last CTA finishes the column
 // Each CTA streams row tiles of all (j+1) basis slots + w into shared memory
-// with 1-D TMA bulk copies (cp.async.bulk + mbarrier, 2-stage pipeline): one
-// thread issues the copies, HBM sees long contiguous bursts, and the tile is
-// read once from HBM for both the update and the dots.  Per-CTA partials are
+// with 1-D TMA bulk copies (cp.async.bulk + mbarrier, 2-stage pipeline; one
+// lane of every warp issues a share of the copies); the tile is read once from HBM for both the update and the dots.  Per-CTA partials are
 // folded by the last CTA in fixed order (deterministic, no fp atomics).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
 
 #include "engine.h"
 
@@ -51,6 +57,17 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// 2-D tile of the basis: box (rows x slots) at (row c0, slot c1), landing in
+// shared memory slot-major, i.e. exactly the stage layout
+__device__ __forceinline__ void tma_load_2d(void *dst, const void *map, int c0, int c1,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -111,8 +128,11 @@ __device__ void arnoldi_finish_dev(GWork W) {
   }
 }
 
+constexpr int VM_TR = 4;  // tensor maps for tile rows 32, 64, 128, 256
+constexpr int VM_B = 9;   // ... and slot boxes 1, 2, ..., 256
 constexpr int CGS_BS = 256;
 constexpr int CGS_NW = CGS_BS / 32;
+constexpr int CGS_Q = (MAXR + 2 + CGS_NW - 1) / CGS_NW;  // slots per warp (<= 33)
 
 enum { CGS_DOT = 0, CGS_UPD_DOT = 1, CGS_UPD_NORM = 2 };
 
@@ -121,11 +141,11 @@ template <int MODE>
 __global__ void __launch_bounds__(CGS_BS, 2)
     k_cgs(int n, double *__restrict__ V, long long pitch, GWork W, const double *cin,
           const double *win, double *wout, double *part, int G, unsigned *counter,
-          int stage_doubles, int use_cond, cudaGraphConditionalHandle cond) {
+          int stage_doubles, int use_cond, cudaGraphConditionalHandle cond,
+          const char *__restrict__ vmaps, int trmax) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bars[2];
   __shared__ double cs[MAXR + 1];
-  __shared__ double dacc[MAXR + 2];
   __shared__ double red[CGS_BS];
   __shared__ bool is_last;
 
@@ -140,7 +160,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double *out = (MODE == CGS_UPD_NORM) ? V + (size_t)L * pitch : wout;
   // tile rows: largest power of two with (L+1)*TR <= stage, within [32, 1024]
-  int TR = 1024;
+  int TR = trmax;
   while (TR > 32 && (L + 1) * TR > stage_doubles) TR >>= 1;
   const int ntiles = (n + TR - 1) / TR;
   double *stage0 = sm, *stage1 = sm + stage_doubles;
@@ -149,7 +169,6 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   for (int l = tid; l < L; l += CGS_BS) {
     if (MODE != CGS_DOT) cs[l] = W.alpha[l] * cin[l];
   }
-  for (int l = tid; l < nd; l += CGS_BS) dacc[l] = 0.0;
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -158,23 +177,51 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   __syncthreads();
 
   auto tile_full = [&](int t) { return (long long)(t + 1) * TR <= (long long)n; };
-  auto issue = [&](int t, int s) {  // single thread
+  // Tile load.  TR <= 256: thread 0 moves the L basis segments with 2-D TMA
+  // boxes of 2^b slots (popcount(L) copies, one tensor map per box shape) and
+  // w with one 1-D copy.  Larger tiles (small j) use one 1-D copy per slot,
+  // spread over the warps with a warp-uniform slot index (cp.async.bulk takes
+  // uniform operands: lane-divergent issue compiles to a serial waterfall).
+  // Thread 0's expect_tx may land after some copies complete (the tx-count
+  // goes transiently negative); the phase cannot flip before its arrival.
+  const bool boxed = TR <= 256 && vmaps != nullptr;
+  const char *maps = boxed ? vmaps + (size_t)(__ffs(TR) - 6) * VM_B * sizeof(CUtensorMap) : nullptr;
+  auto issue = [&](int t, int s) {
     const int r0 = t * TR;
     const uint32_t bytes = TR * 8u;
     uint64_t *bar = &bars[s];
-    mbar_expect_tx(bar, bytes * (uint32_t)(L + 1));
     double *dst = s ? stage1 : stage0;
-    for (int l = 0; l < L; ++l) tma_load_1d(dst + l * TR, V + (size_t)l * pitch + r0, bytes, bar);
-    tma_load_1d(dst + L * TR, win + r0, bytes, bar);
+    if (boxed) {
+      if (tid == 0) {
+        mbar_expect_tx(bar, bytes * (uint32_t)(L + 1));
+        int l0 = 0;
+        for (int b = VM_B - 1; b >= 0; --b) {
+          if (L & (1 << b)) {
+            tma_load_2d(dst + l0 * TR, maps + b * sizeof(CUtensorMap), r0, l0, bar);
+            l0 += 1 << b;
+          }
+        }
+        tma_load_1d(dst + L * TR, win + r0, bytes, bar);
+      }
+      return;
+    }
+    if (tid == 0) mbar_expect_tx(bar, bytes * (uint32_t)(L + 1));
+    if (lane == 0) {
+      for (int l = warp; l <= L; l += CGS_NW) {
+        const double *src = (l < L) ? V + (size_t)l * pitch + r0 : win + r0;
+        tma_load_1d(dst + l * TR, src, bytes, bar);
+      }
+    }
   };
 
   const int t0 = blockIdx.x;
-  if (tid == 0) {
-    if (t0 < ntiles && tile_full(t0)) issue(t0, 0);
-    if (t0 + G < ntiles && tile_full(t0 + G)) issue(t0 + G, 1);
-  }
+  if (t0 < ntiles && tile_full(t0)) issue(t0, 0);
+  if (t0 + G < ntiles && tile_full(t0 + G)) issue(t0 + G, 1);
 
   double nrm = 0.0;
+  double acc[CGS_Q];
+#pragma unroll
+  for (int q = 0; q < CGS_Q; ++q) acc[q] = 0.0;
   const int rpp = TR < CGS_BS ? TR : CGS_BS;  // rows per pass in phase A
   const int parts = CGS_BS / rpp;
 
@@ -226,33 +273,38 @@ __global__ void __launch_bounds__(CGS_BS, 2)
       __syncthreads();
     }
     if (MODE != CGS_UPD_NORM) {
-      // phase B: one warp per basis slot, lanes over rows, per-CTA sums in smem
-      for (int l = warp; l < nd; l += CGS_NW) {
-        const double *vl = buf + l * TR;
-        double a0 = 0.0, a1 = 0.0;
-        int r = lane;
-        for (; r + 32 < TR; r += 64) {
-          a0 += vl[r] * wt[r];
-          a1 += vl[r + 32] * wt[r + 32];
+      // phase B: warp w owns slots l = w + NW*q; each lane keeps its running
+      // partial sum per owned slot in a register across rows and tiles (no
+      // per-tile shuffle reductions; folded once after the tile loop)
+#pragma unroll
+      for (int q = 0; q < CGS_Q; ++q) {
+        const int l = warp + CGS_NW * q;
+        if (l < nd) {
+          const double *vl = buf + l * TR;
+          double a = acc[q];
+          for (int r = lane; r < TR; r += 32) a += vl[r] * wt[r];
+          acc[q] = a;
         }
-        if (r < TR) a0 += vl[r] * wt[r];
-        double a = wsum(a0 + a1);
-        if (lane == 0) dacc[l] += a;
       }
     }
+    if (MODE != CGS_DOT) fence_proxy_async();  // wt was written via the generic proxy
     __syncthreads();  // stage s consumed
-    if (tid == 0) {
+    {
       const int tn = t + 2 * G;
-      if (tn < ntiles && tile_full(tn)) {
-        fence_proxy_async();
-        issue(tn, s);
-      }
+      if (tn < ntiles && tile_full(tn)) issue(tn, s);
     }
   }
 
   // per-CTA partials -> part[l * G + cta]
   if (MODE != CGS_UPD_NORM) {
-    for (int l = tid; l < nd; l += CGS_BS) part[(size_t)l * G + blockIdx.x] = dacc[l];
+#pragma unroll
+    for (int q = 0; q < CGS_Q; ++q) {
+      const int l = warp + CGS_NW * q;
+      if (l < nd) {  // warp-uniform
+        const double v = wsum(acc[q]);
+        if (lane == 0) part[(size_t)l * G + blockIdx.x] = v;
+      }
+    }
   } else {
     double v = wsum(nrm);
     if (lane == 0) red[warp] = v;
@@ -307,6 +359,57 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   }
 }
 
+// Tensor maps over the basis V viewed as a 2-D array (rows: vpitch, slots:
+// vcap+1, slot stride vpitch doubles), one per (tile rows, slot box) shape.
+void Engine::build_vmaps() {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      dalloc_raw(&vmaps, 0);  // no tensor maps: the sweeps use 1-D copies only
+      return;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  std::vector<CUtensorMap> maps(VM_TR * VM_B);
+  const cuuint64_t dims[2] = {(cuuint64_t)vpitch, (cuuint64_t)(vcap + 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)vpitch * sizeof(double)};
+  const cuuint32_t estr[2] = {1, 1};
+  for (int a = 0; a < VM_TR; ++a)
+    for (int b = 0; b < VM_B; ++b) {
+      // shapes larger than a stage are never used (and boxes over 128 KB are
+      // rejected by the encoder): leave those entries zero
+      if ((1u << b) > (cuuint32_t)(vcap + 1) || (32u << a) * (1u << b) * 8u > (128u << 10)) {
+        memset(&maps[a * VM_B + b], 0, sizeof(CUtensorMap));
+        continue;
+      }
+      const cuuint32_t box[2] = {32u << a, 1u << b};
+      CUresult r = encode(&maps[a * VM_B + b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, V, dims,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS)
+        throw SolveError(IRKG_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) +
+                                            ") box " + std::to_string(box[0]) + "x" +
+                                            std::to_string(box[1]) + " dims " +
+                                            std::to_string(dims[0]) + "x" + std::to_string(dims[1]));
+    }
+  dalloc_raw(&vmaps, maps.size() * sizeof(CUtensorMap));
+  check(cudaMemcpy(vmaps, maps.data(), maps.size() * sizeof(CUtensorMap),
+                   cudaMemcpyHostToDevice),
+        "tensor maps");
+}
+
+static int cgs_trmax() {
+  static int v = -1;
+  if (v < 0) { const char *e = getenv("IRKG_CGS_TRMAX"); v = e ? atoi(e) : 1024; }
+  return v;
+}
+
 int Engine::cgs_stage_doubles() const {
   int st = (vcap + 2) * 32;
   return st < 6144 ? 6144 : st;
@@ -328,11 +431,14 @@ void Engine::cgs(long long n) {
   }
   const int uc = cond_active ? 1 : 0;
   k_cgs<CGS_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, nullptr, wbuf, nullptr, part,
-                                              G, counter, stage, 0, cond_handle);
+                                              G, counter, stage, 0, cond_handle,
+      (const char *)vmaps, cgs_trmax());
   k_cgs<CGS_UPD_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c1, wbuf, wbuf, part, G,
-                                                  counter, stage, 0, cond_handle);
+                                                  counter, stage, 0, cond_handle,
+      (const char *)vmaps, cgs_trmax());
   k_cgs<CGS_UPD_NORM><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c2, wbuf, nullptr,
-                                                   part, G, counter, stage, uc, cond_handle);
+                                                   part, G, counter, stage, uc, cond_handle,
+      (const char *)vmaps, cgs_trmax());
   count(3);
 }
 
@@ -353,14 +459,17 @@ void Engine::cgs_slab(long long n, int j) {
   }
   const int L = j + 1;
   k_cgs<CGS_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, nullptr, wbuf, nullptr, part,
-                                              G, counter, stage, 0, cond_handle);
+                                              G, counter, stage, 0, cond_handle,
+      (const char *)vmaps, cgs_trmax());
   allreduce(W.c1, L);
   allreduce(&ctrl_dev->wn2, 1);
   k_cgs<CGS_UPD_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c1, wbuf, wbuf, part, G,
-                                                  counter, stage, 0, cond_handle);
+                                                  counter, stage, 0, cond_handle,
+      (const char *)vmaps, cgs_trmax());
   allreduce(W.c2, L);
   k_cgs<CGS_UPD_NORM><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c2, wbuf, nullptr,
-                                                   part, G, counter, stage, -1, cond_handle);
+                                                   part, G, counter, stage, -1, cond_handle,
+      (const char *)vmaps, cgs_trmax());
   allreduce(&ctrl_dev->hn2, 1);
   count(3);
   arnoldi_finish();

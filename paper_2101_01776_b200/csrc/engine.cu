@@ -113,7 +113,7 @@ Engine::~Engine() {
   cudaStreamSynchronize(stream);
   void *bufs[] = {part, counter, scal_dev, ctrl_dev, W.H, W.cs, W.sn, W.g, W.alpha, W.y,
                   W.c1, W.c2, W.res, V, wbuf, zbuf, ubuf, tmp_x, tmp_t, U, F, Gs, Y, DK,
-                  Kst, RHS, ufield, opA};
+                  Kst, RHS, ufield, opA, vmaps};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (ctrl_host) cudaFreeHost(ctrl_host);
@@ -150,6 +150,7 @@ void Engine::ensure_basis(int restart) {
   drop_graphs();  // graphs bake the basis pointer in
   dalloc(&V, (size_t)(restart + 1) * vpitch);
   vcap = restart;
+  build_vmaps();
 }
 
 void Engine::set_tableau(const irkg_tableau &t) {

@@ -92,6 +92,8 @@ struct Engine {
   double *V = nullptr;          // basis, (restart+1) slots of 2N
   long long vpitch = 0;
   int vcap = 0;                 // allocated restart capacity
+  void *vmaps = nullptr;        // CUtensorMap[4][9] over V: boxes (32<<a rows, 1<<b slots)
+  void build_vmaps();
   double *wbuf = nullptr;       // 2N: w
   double *zbuf = nullptr;       // 2N: z / cycle-end scratch
   double *ubuf = nullptr;       // 2N: V y combination
