@@ -136,6 +136,161 @@ constexpr int CGS_Q = (MAXR + 2 + CGS_NW - 1) / CGS_NW;  // slots per warp (<= 3
 
 enum { CGS_DOT = 0, CGS_UPD_DOT = 1, CGS_UPD_NORM = 2 };
 
+struct TileArgs {
+  int n, L, G, ntiles;
+  const double *V;
+  long long pitch;
+  const double *win;
+  double *out;
+  double *stage0, *stage1;
+  uint64_t *bars;
+  const double *cs;
+  double *red;
+  const char *maps;  // tensor maps of this tile height (null: 1-D copies)
+};
+
+// The tile loop, specialised on the tile height TRC so the per-slot work is
+// straight-line: a tile is (L+1) x TRC doubles in shared memory (rows [0, L)
+// basis slots, row L the w segment), double-buffered through two mbarriers.
+template <int MODE, int TRC>
+__device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q], double &nrm) {
+  constexpr int K = TRC / 32;                       // rows per lane in phase B
+  constexpr int RPP = TRC < CGS_BS ? TRC : CGS_BS;  // rows per pass in phase A
+  constexpr int PARTS = CGS_BS / RPP;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int L = A.L, G = A.G, ntiles = A.ntiles;
+  const int nd = (MODE == CGS_DOT) ? L + 1 : L;
+  const int nq = (nd + CGS_NW - 1) / CGS_NW;
+
+  auto tile_full = [&](int t) { return (long long)(t + 1) * TRC <= (long long)A.n; };
+  // Tile load.  TRC <= 256: thread 0 moves the L basis segments with 2-D TMA
+  // boxes of 2^b slots (popcount(L) copies, one tensor map per box shape) and
+  // w with one 1-D copy.  Taller tiles (small j) use one 1-D copy per slot,
+  // spread over the warps with a warp-uniform slot index (cp.async.bulk takes
+  // uniform operands: lane-divergent issue compiles to a serial waterfall).
+  // Thread 0's expect_tx may land after some copies complete (the tx-count
+  // goes transiently negative); the phase cannot flip before its arrival.
+  auto issue = [&](int t, int s) {
+    const int r0 = t * TRC;
+    constexpr uint32_t bytes = TRC * 8u;
+    uint64_t *bar = &A.bars[s];
+    double *dst = s ? A.stage1 : A.stage0;
+    if (A.maps) {
+      if (tid == 0) {
+        mbar_expect_tx(bar, bytes * (uint32_t)(L + 1));
+        int l0 = 0;
+        for (int b = VM_B - 1; b >= 0; --b) {
+          if (L & (1 << b)) {
+            tma_load_2d(dst + l0 * TRC, A.maps + b * sizeof(CUtensorMap), r0, l0, bar);
+            l0 += 1 << b;
+          }
+        }
+        tma_load_1d(dst + L * TRC, A.win + r0, bytes, bar);
+      }
+      return;
+    }
+    if (tid == 0) mbar_expect_tx(bar, bytes * (uint32_t)(L + 1));
+    if (lane == 0) {
+      for (int l = warp; l <= L; l += CGS_NW) {
+        const double *src = (l < L) ? A.V + (size_t)l * A.pitch + r0 : A.win + r0;
+        tma_load_1d(dst + l * TRC, src, bytes, bar);
+      }
+    }
+  };
+
+  const int t0 = blockIdx.x;
+  if (t0 < ntiles && tile_full(t0)) issue(t0, 0);
+  if (t0 + G < ntiles && tile_full(t0 + G)) issue(t0 + G, 1);
+
+  int it = 0;
+  for (int t = t0; t < ntiles; t += G, ++it) {
+    const int s = it & 1;
+    const int r0 = t * TRC;
+    const int rows = min(TRC, A.n - r0);
+    double *buf = s ? A.stage1 : A.stage0;
+    if (tile_full(t)) {
+      while (!mbar_try_wait(&A.bars[s], (uint32_t)((it >> 1) & 1))) {
+      }
+    } else {  // partial tail tile (only the globally last one): generic loads
+      for (int l = 0; l <= L; ++l) {
+        const double *src = (l < L) ? A.V + (size_t)l * A.pitch + r0 : A.win + r0;
+        for (int r = tid; r < TRC; r += CGS_BS) buf[l * TRC + r] = (r < rows) ? src[r] : 0.0;
+      }
+      __syncthreads();
+    }
+    double *wt = buf + L * TRC;
+    if (MODE != CGS_DOT) {
+      // phase A: w1 = w - sum_l s_l cs_l on this tile; PARTS threads share a
+      // row (slots split round-robin), two accumulators break the DFMA chain
+      const int pid = tid / RPP, rl = tid % RPP;
+#pragma unroll
+      for (int rb = 0; rb < TRC; rb += RPP) {
+        const int r = rb + rl;
+        const double *col = buf + r;
+        double s0 = 0.0, s1 = 0.0;
+        int l = pid;
+        for (; l + PARTS < L; l += 2 * PARTS) {
+          s0 += col[l * TRC] * A.cs[l];
+          s1 += col[(l + PARTS) * TRC] * A.cs[l + PARTS];
+        }
+        if (l < L) s0 += col[l * TRC] * A.cs[l];
+        double sum = s0 + s1;
+        if (PARTS > 1) {
+          A.red[tid] = sum;
+          __syncthreads();
+          if (pid == 0) {
+            double tot = 0.0;
+#pragma unroll
+            for (int p = 0; p < PARTS; ++p) tot += A.red[p * RPP + rl];
+            sum = tot;
+          }
+        }
+        if (pid == 0) {
+          double v = wt[r] - sum;
+          if (r < rows) {
+            if (MODE == CGS_UPD_NORM) nrm += v * v;
+            A.out[r0 + r] = v;
+          } else {
+            v = 0.0;
+          }
+          wt[r] = v;
+        }
+        if (PARTS > 1) __syncthreads();
+      }
+      __syncthreads();
+    }
+    if (MODE != CGS_UPD_NORM) {
+      // phase B: warp w owns slots l = w + NW*q; each lane keeps its running
+      // partial sum per owned slot in a register across rows and tiles (no
+      // per-tile shuffle reductions; folded once after the tile loop)
+      // (w rows cached in registers for short tiles; tall tiles only occur at
+      // small j, where re-reading them from shared memory is cheap)
+      constexpr int KR = K <= 4 ? K : 1;
+      double wr[KR];
+#pragma unroll
+      for (int k = 0; k < KR; ++k) wr[k] = wt[lane + 32 * k];
+#pragma unroll
+      for (int q = 0; q < CGS_Q; ++q) {
+        if (q >= nq) break;
+        const int l = warp + CGS_NW * q;
+        if (l < nd) {
+          const double *vl = buf + l * TRC + lane;
+          double a = acc[q];
+#pragma unroll
+          for (int k = 0; k < K; ++k) a += vl[32 * k] * (K <= 4 ? wr[k < KR ? k : 0] : wt[lane + 32 * k]);
+          acc[q] = a;
+        }
+      }
+    }
+    if (MODE != CGS_DOT) fence_proxy_async();  // wt was written via the generic proxy
+    __syncthreads();  // stage s consumed
+    {
+      const int tn = t + 2 * G;
+      if (tn < ntiles && tile_full(tn)) issue(tn, s);
+    }
+  }
+}
+
 // Stage layout: (L+1) x TR doubles; rows [0, L) are basis slots, row L is w.
 template <int MODE>
 __global__ void __launch_bounds__(CGS_BS, 2)
@@ -165,6 +320,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   const int ntiles = (n + TR - 1) / TR;
   double *stage0 = sm, *stage1 = sm + stage_doubles;
   const int nd = (MODE == CGS_DOT) ? L + 1 : L;  // dot entries (DOT: + ||w||^2)
+  if (TR <= 256 && vmaps) vmaps += (size_t)(__ffs(TR) - 6) * VM_B * sizeof(CUtensorMap);
 
   for (int l = tid; l < L; l += CGS_BS) {
     if (MODE != CGS_DOT) cs[l] = W.alpha[l] * cin[l];
@@ -176,123 +332,19 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   }
   __syncthreads();
 
-  auto tile_full = [&](int t) { return (long long)(t + 1) * TR <= (long long)n; };
-  // Tile load.  TR <= 256: thread 0 moves the L basis segments with 2-D TMA
-  // boxes of 2^b slots (popcount(L) copies, one tensor map per box shape) and
-  // w with one 1-D copy.  Larger tiles (small j) use one 1-D copy per slot,
-  // spread over the warps with a warp-uniform slot index (cp.async.bulk takes
-  // uniform operands: lane-divergent issue compiles to a serial waterfall).
-  // Thread 0's expect_tx may land after some copies complete (the tx-count
-  // goes transiently negative); the phase cannot flip before its arrival.
-  const bool boxed = TR <= 256 && vmaps != nullptr;
-  const char *maps = boxed ? vmaps + (size_t)(__ffs(TR) - 6) * VM_B * sizeof(CUtensorMap) : nullptr;
-  auto issue = [&](int t, int s) {
-    const int r0 = t * TR;
-    const uint32_t bytes = TR * 8u;
-    uint64_t *bar = &bars[s];
-    double *dst = s ? stage1 : stage0;
-    if (boxed) {
-      if (tid == 0) {
-        mbar_expect_tx(bar, bytes * (uint32_t)(L + 1));
-        int l0 = 0;
-        for (int b = VM_B - 1; b >= 0; --b) {
-          if (L & (1 << b)) {
-            tma_load_2d(dst + l0 * TR, maps + b * sizeof(CUtensorMap), r0, l0, bar);
-            l0 += 1 << b;
-          }
-        }
-        tma_load_1d(dst + L * TR, win + r0, bytes, bar);
-      }
-      return;
-    }
-    if (tid == 0) mbar_expect_tx(bar, bytes * (uint32_t)(L + 1));
-    if (lane == 0) {
-      for (int l = warp; l <= L; l += CGS_NW) {
-        const double *src = (l < L) ? V + (size_t)l * pitch + r0 : win + r0;
-        tma_load_1d(dst + l * TR, src, bytes, bar);
-      }
-    }
-  };
-
-  const int t0 = blockIdx.x;
-  if (t0 < ntiles && tile_full(t0)) issue(t0, 0);
-  if (t0 + G < ntiles && tile_full(t0 + G)) issue(t0 + G, 1);
-
+  TileArgs A{n, L, G, ntiles, V, pitch, win, out, stage0, stage1, bars, cs, red,
+             TR <= 256 ? vmaps : nullptr};
   double nrm = 0.0;
   double acc[CGS_Q];
 #pragma unroll
   for (int q = 0; q < CGS_Q; ++q) acc[q] = 0.0;
-  const int rpp = TR < CGS_BS ? TR : CGS_BS;  // rows per pass in phase A
-  const int parts = CGS_BS / rpp;
-
-  int it = 0;
-  for (int t = t0; t < ntiles; t += G, ++it) {
-    const int s = it & 1;
-    const int r0 = t * TR;
-    const int rows = min(TR, n - r0);
-    double *buf = s ? stage1 : stage0;
-    if (tile_full(t)) {
-      while (!mbar_try_wait(&bars[s], (uint32_t)((it >> 1) & 1))) {
-      }
-    } else {  // partial tail tile (only the globally last one): generic loads
-      for (int l = 0; l <= L; ++l) {
-        const double *src = (l < L) ? V + (size_t)l * pitch + r0 : win + r0;
-        for (int r = tid; r < TR; r += CGS_BS) buf[l * TR + r] = (r < rows) ? src[r] : 0.0;
-      }
-      __syncthreads();
-    }
-    double *wt = buf + L * TR;
-    if (MODE != CGS_DOT) {
-      // phase A: w1 = w - sum_l s_l cs_l on this tile
-      const int pid = tid / rpp, rl = tid % rpp;
-      for (int rb = 0; rb < TR; rb += rpp) {
-        const int r = rb + rl;
-        double sum = 0.0;
-        for (int l = pid; l < L; l += parts) sum += buf[l * TR + r] * cs[l];
-        if (parts > 1) {
-          red[tid] = sum;
-          __syncthreads();
-          if (pid == 0) {
-            double tot = 0.0;
-            for (int p = 0; p < parts; ++p) tot += red[p * rpp + rl];
-            sum = tot;
-          }
-        }
-        if (pid == 0) {
-          double v = wt[r] - sum;
-          if (r < rows) {
-            if (MODE == CGS_UPD_NORM) nrm += v * v;
-            out[r0 + r] = v;
-          } else {
-            v = 0.0;
-          }
-          wt[r] = v;
-        }
-        if (parts > 1) __syncthreads();
-      }
-      __syncthreads();
-    }
-    if (MODE != CGS_UPD_NORM) {
-      // phase B: warp w owns slots l = w + NW*q; each lane keeps its running
-      // partial sum per owned slot in a register across rows and tiles (no
-      // per-tile shuffle reductions; folded once after the tile loop)
-#pragma unroll
-      for (int q = 0; q < CGS_Q; ++q) {
-        const int l = warp + CGS_NW * q;
-        if (l < nd) {
-          const double *vl = buf + l * TR;
-          double a = acc[q];
-          for (int r = lane; r < TR; r += 32) a += vl[r] * wt[r];
-          acc[q] = a;
-        }
-      }
-    }
-    if (MODE != CGS_DOT) fence_proxy_async();  // wt was written via the generic proxy
-    __syncthreads();  // stage s consumed
-    {
-      const int tn = t + 2 * G;
-      if (tn < ntiles && tile_full(tn)) issue(tn, s);
-    }
+  switch (TR) {
+    case 32: cgs_tiles<MODE, 32>(A, acc, nrm); break;
+    case 64: cgs_tiles<MODE, 64>(A, acc, nrm); break;
+    case 128: cgs_tiles<MODE, 128>(A, acc, nrm); break;
+    case 256: cgs_tiles<MODE, 256>(A, acc, nrm); break;
+    case 512: cgs_tiles<MODE, 512>(A, acc, nrm); break;
+    default: cgs_tiles<MODE, 1024>(A, acc, nrm); break;
   }
 
   // per-CTA partials -> part[l * G + cta]
