@@ -133,6 +133,7 @@ constexpr int VM_B = 9;   // ... and slot boxes 1, 2, ..., 256
 constexpr int CGS_BS = 256;
 constexpr int CGS_NW = CGS_BS / 32;
 constexpr int CGS_Q = (MAXR + 2 + CGS_NW - 1) / CGS_NW;  // slots per warp (<= 33)
+constexpr int CGS_STAGE_MAX = (MAXR + 2) * 32;             // doubles per stage, upper bound
 
 enum { CGS_DOT = 0, CGS_UPD_DOT = 1, CGS_UPD_NORM = 2 };
 
@@ -149,6 +150,43 @@ struct TileArgs {
   const char *maps;  // tensor maps of this tile height (null: 1-D copies)
 };
 
+// Tile issue, out of line: one copy of the code for every tile height and
+// call site (inlined, the unrolled copy loops made the kernels too large for
+// the instruction cache of a short launch).
+// TR <= 256: one thread moves the L basis segments with 2-D TMA boxes of 2^b
+// slots (popcount(L) copies, one tensor map per box shape) and w with a 1-D
+// copy.
+__device__ __noinline__ void issue_boxed(double *dst, const char *maps, const double *win, int r0,
+                                         int TR, int L, uint64_t *bar) {
+  const uint32_t bytes = TR * 8u;
+  mbar_expect_tx(bar, bytes * (uint32_t)(L + 1));
+  int l0 = 0;
+#pragma unroll 1
+  for (int b = VM_B - 1; b >= 0; --b) {
+    if (L & (1 << b)) {
+      tma_load_2d(dst + l0 * TR, maps + b * sizeof(CUtensorMap), r0, l0, bar);
+      l0 += 1 << b;
+    }
+  }
+  tma_load_1d(dst + L * TR, win + r0, bytes, bar);
+}
+
+// Taller tiles (small j): one 1-D copy per slot, lane 0 of warp w issuing
+// slots w, w+NW, ... (cp.async.bulk takes uniform operands: lane-divergent
+// issue from one warp compiles to a serial waterfall).  Thread 0's expect_tx
+// may land after some copies complete (the tx-count goes transiently
+// negative); the phase cannot flip before its arrival.
+__device__ __noinline__ void issue_slots(double *dst, const double *V, long long pitch,
+                                         const double *win, int r0, int TR, int L, int warp,
+                                         uint64_t *bar) {
+  const uint32_t bytes = TR * 8u;
+#pragma unroll 1
+  for (int l = warp; l <= L; l += CGS_NW) {
+    const double *src = (l < L) ? V + (size_t)l * pitch + r0 : win + r0;
+    tma_load_1d(dst + l * TR, src, bytes, bar);
+  }
+}
+
 // The tile loop, specialised on the tile height TRC so the per-slot work is
 // straight-line: a tile is (L+1) x TRC doubles in shared memory (rows [0, L)
 // basis slots, row L the w segment), double-buffered through two mbarriers.
@@ -157,44 +195,24 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
   constexpr int K = TRC / 32;                       // rows per lane in phase B
   constexpr int RPP = TRC < CGS_BS ? TRC : CGS_BS;  // rows per pass in phase A
   constexpr int PARTS = CGS_BS / RPP;
+  // a stage holds at most CGS_STAGE_MAX doubles, so a tile of TRC rows has at
+  // most CGS_STAGE_MAX/TRC slots: unroll only that many slot bodies per warp
+  // (short launches at small j run from a cold instruction cache)
+  constexpr int QMAX_ = (CGS_STAGE_MAX / TRC + CGS_NW - 1) / CGS_NW;
+  constexpr int QMAX = QMAX_ < CGS_Q ? QMAX_ : CGS_Q;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int L = A.L, G = A.G, ntiles = A.ntiles;
   const int nd = (MODE == CGS_DOT) ? L + 1 : L;
   const int nq = (nd + CGS_NW - 1) / CGS_NW;
 
   auto tile_full = [&](int t) { return (long long)(t + 1) * TRC <= (long long)A.n; };
-  // Tile load.  TRC <= 256: thread 0 moves the L basis segments with 2-D TMA
-  // boxes of 2^b slots (popcount(L) copies, one tensor map per box shape) and
-  // w with one 1-D copy.  Taller tiles (small j) use one 1-D copy per slot,
-  // spread over the warps with a warp-uniform slot index (cp.async.bulk takes
-  // uniform operands: lane-divergent issue compiles to a serial waterfall).
-  // Thread 0's expect_tx may land after some copies complete (the tx-count
-  // goes transiently negative); the phase cannot flip before its arrival.
   auto issue = [&](int t, int s) {
-    const int r0 = t * TRC;
-    constexpr uint32_t bytes = TRC * 8u;
-    uint64_t *bar = &A.bars[s];
     double *dst = s ? A.stage1 : A.stage0;
     if (A.maps) {
-      if (tid == 0) {
-        mbar_expect_tx(bar, bytes * (uint32_t)(L + 1));
-        int l0 = 0;
-        for (int b = VM_B - 1; b >= 0; --b) {
-          if (L & (1 << b)) {
-            tma_load_2d(dst + l0 * TRC, A.maps + b * sizeof(CUtensorMap), r0, l0, bar);
-            l0 += 1 << b;
-          }
-        }
-        tma_load_1d(dst + L * TRC, A.win + r0, bytes, bar);
-      }
-      return;
-    }
-    if (tid == 0) mbar_expect_tx(bar, bytes * (uint32_t)(L + 1));
-    if (lane == 0) {
-      for (int l = warp; l <= L; l += CGS_NW) {
-        const double *src = (l < L) ? A.V + (size_t)l * A.pitch + r0 : A.win + r0;
-        tma_load_1d(dst + l * TRC, src, bytes, bar);
-      }
+      if (tid == 0) issue_boxed(dst, A.maps, A.win, t * TRC, TRC, L, &A.bars[s]);
+    } else {
+      if (tid == 0) mbar_expect_tx(&A.bars[s], TRC * 8u * (uint32_t)(L + 1));
+      if (lane == 0) issue_slots(dst, A.V, A.pitch, A.win, t * TRC, TRC, L, warp, &A.bars[s]);
     }
   };
 
@@ -270,14 +288,24 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
 #pragma unroll
       for (int k = 0; k < KR; ++k) wr[k] = wt[lane + 32 * k];
 #pragma unroll
-      for (int q = 0; q < CGS_Q; ++q) {
+      for (int q = 0; q < QMAX; ++q) {
         if (q >= nq) break;
         const int l = warp + CGS_NW * q;
         if (l < nd) {
           const double *vl = buf + l * TRC + lane;
           double a = acc[q];
+          if constexpr (K <= 4) {
 #pragma unroll
-          for (int k = 0; k < K; ++k) a += vl[32 * k] * (K <= 4 ? wr[k < KR ? k : 0] : wt[lane + 32 * k]);
+            for (int k = 0; k < K; ++k) a += vl[32 * k] * wr[k];
+          } else {  // keep the code small: 33 slot bodies x K rows would not fit the i-cache
+            double a1 = 0.0;
+#pragma unroll 2
+            for (int k = 0; k < K; k += 2) {
+              a += vl[32 * k] * wt[lane + 32 * k];
+              a1 += vl[32 * k + 32] * wt[lane + 32 * k + 32];
+            }
+            a += a1;
+          }
           acc[q] = a;
         }
       }
@@ -349,8 +377,10 @@ __global__ void __launch_bounds__(CGS_BS, 2)
 
   // per-CTA partials -> part[l * G + cta]
   if (MODE != CGS_UPD_NORM) {
+    const int nq = (nd + CGS_NW - 1) / CGS_NW;
 #pragma unroll
     for (int q = 0; q < CGS_Q; ++q) {
+      if (q >= nq) break;  // skip the dead slot blocks (cold code at small j)
       const int l = warp + CGS_NW * q;
       if (l < nd) {  // warp-uniform
         const double v = wsum(acc[q]);
@@ -456,6 +486,12 @@ void Engine::build_vmaps() {
         "tensor maps");
 }
 
+static const char *cgs_maps(const void *vmaps) {
+  static int nobox = -1;
+  if (nobox < 0) nobox = getenv("IRKG_CGS_NOBOX") ? 1 : 0;
+  return nobox ? nullptr : (const char *)vmaps;
+}
+
 static int cgs_trmax() {
   static int v = -1;
   if (v < 0) { const char *e = getenv("IRKG_CGS_TRMAX"); v = e ? atoi(e) : 1024; }
@@ -463,7 +499,8 @@ static int cgs_trmax() {
 }
 
 int Engine::cgs_stage_doubles() const {
-  int st = (vcap + 2) * 32;
+  static_assert(6144 <= CGS_STAGE_MAX, "stage floor above the unroll bound");
+  int st = (vcap + 2) * 32;  // <= CGS_STAGE_MAX (vcap <= MAXR)
   return st < 6144 ? 6144 : st;
 }
 
@@ -484,13 +521,13 @@ void Engine::cgs(long long n) {
   const int uc = cond_active ? 1 : 0;
   k_cgs<CGS_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, nullptr, wbuf, nullptr, part,
                                               G, counter, stage, 0, cond_handle,
-      (const char *)vmaps, cgs_trmax());
+      cgs_maps(vmaps), cgs_trmax());
   k_cgs<CGS_UPD_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c1, wbuf, wbuf, part, G,
                                                   counter, stage, 0, cond_handle,
-      (const char *)vmaps, cgs_trmax());
+      cgs_maps(vmaps), cgs_trmax());
   k_cgs<CGS_UPD_NORM><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c2, wbuf, nullptr,
                                                    part, G, counter, stage, uc, cond_handle,
-      (const char *)vmaps, cgs_trmax());
+      cgs_maps(vmaps), cgs_trmax());
   count(3);
 }
 
@@ -512,16 +549,16 @@ void Engine::cgs_slab(long long n, int j) {
   const int L = j + 1;
   k_cgs<CGS_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, nullptr, wbuf, nullptr, part,
                                               G, counter, stage, 0, cond_handle,
-      (const char *)vmaps, cgs_trmax());
+      cgs_maps(vmaps), cgs_trmax());
   allreduce(W.c1, L);
   allreduce(&ctrl_dev->wn2, 1);
   k_cgs<CGS_UPD_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c1, wbuf, wbuf, part, G,
                                                   counter, stage, 0, cond_handle,
-      (const char *)vmaps, cgs_trmax());
+      cgs_maps(vmaps), cgs_trmax());
   allreduce(W.c2, L);
   k_cgs<CGS_UPD_NORM><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c2, wbuf, nullptr,
                                                    part, G, counter, stage, -1, cond_handle,
-      (const char *)vmaps, cgs_trmax());
+      cgs_maps(vmaps), cgs_trmax());
   allreduce(&ctrl_dev->hn2, 1);
   count(3);
   arnoldi_finish();

@@ -3,7 +3,7 @@
 Runs one 200-iteration restart cycle of block GMRES (2x2 Burgers block,
 rtol tiny so the cycle runs to the restart length) through the C ABI with
 per-phase CUDA-event timing, and prints the CGS2 bandwidth achieved.
-usage: python tools/cgs_bench.py [--n 1024] [--restart 200]
+usage: python tools/cgs_bench.py [--n 1024] [--restart 200] [--reps 3]
 """
 
 import argparse
@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--restart", type=int, default=200)
     ap.add_argument("--timing", type=int, default=1)
     ap.add_argument("--dt", type=float, default=5e-2)
+    ap.add_argument("--reps", type=int, default=3, help="cycles run; the last one is reported")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -35,12 +36,13 @@ def main():
     rhs = np.random.default_rng(0).standard_normal(2 * n * n)
     ctx = context_for(prob)
     ctx.set_timing(bool(args.timing))
-    c0 = ctx.counters()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    x, rep = pk.block_gmres(sysb, rhs, pk.PrecondSpec(inner=4), rtol=1e-15,
-                            maxit=args.restart, restart=args.restart)
-    torch.cuda.synchronize()
+    for _ in range(args.reps):
+        c0 = ctx.counters()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x, rep = pk.block_gmres(sysb, rhs, pk.PrecondSpec(inner=4), rtol=1e-15,
+                                maxit=args.restart, restart=args.restart)
+        torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     c1 = ctx.counters()
     by = c1["cgs_bytes"] - c0["cgs_bytes"]
