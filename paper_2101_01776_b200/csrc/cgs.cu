@@ -6,10 +6,12 @@
 //     DOT       c1 = V^T w, ||w||^2
 //     UPD_DOT   w1 = w - V c1 (written back), c2 = V^T w1      (V tile read once)
 //     UPD_NORM  s_{j+1} = w1 - V c2, ||s_{j+1}||^2; last CTA finishes the column
-// Each CTA streams row tiles of all (j+1) basis slots + w into shared memory
-// with 1-D TMA bulk copies (cp.async.bulk + mbarrier, 2-stage pipeline; one
-// lane of every warp issues a share of the copies); the tile is read once from HBM for both the update and the dots.  Per-CTA partials are
-// folded by the last CTA in fixed order (deterministic, no fp atomics).
+// Each CTA streams row tiles of all (j+1) basis slots + w into a shared-memory
+// ring of up to CGS_MAXST tiles (one mbarrier each) with TMA bulk copies:
+// 2-D tensor-map boxes for tiles of <= 256 rows, else one 1-D copy per slot.
+// The tile is read once from HBM for both the update and the dots.  Per-CTA
+// partials are folded by the last CTA in fixed order (deterministic, no fp
+// atomics).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -133,7 +135,8 @@ constexpr int VM_B = 9;   // ... and slot boxes 1, 2, ..., 256
 constexpr int CGS_BS = 256;
 constexpr int CGS_NW = CGS_BS / 32;
 constexpr int CGS_Q = (MAXR + 2 + CGS_NW - 1) / CGS_NW;  // slots per warp (<= 33)
-constexpr int CGS_STAGE_MAX = (MAXR + 2) * 32;             // doubles per stage, upper bound
+constexpr int CGS_STAGE_MAX = (MAXR + 2) * 32;  // ring/2 upper bound: max doubles per tile
+constexpr int CGS_MAXST = 8;                    // max tiles in flight per CTA
 
 enum { CGS_DOT = 0, CGS_UPD_DOT = 1, CGS_UPD_NORM = 2 };
 
@@ -143,7 +146,8 @@ struct TileArgs {
   long long pitch;
   const double *win;
   double *out;
-  double *stage0, *stage1;
+  double *ring;      // NST tiles of (L+1) x TRC doubles
+  int nst;
   uint64_t *bars;
   const double *cs;
   double *red;
@@ -195,7 +199,7 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
   constexpr int K = TRC / 32;                       // rows per lane in phase B
   constexpr int RPP = TRC < CGS_BS ? TRC : CGS_BS;  // rows per pass in phase A
   constexpr int PARTS = CGS_BS / RPP;
-  // a stage holds at most CGS_STAGE_MAX doubles, so a tile of TRC rows has at
+  // a tile holds at most CGS_STAGE_MAX doubles, so a tile of TRC rows has at
   // most CGS_STAGE_MAX/TRC slots: unroll only that many slot bodies per warp
   // (short launches at small j run from a cold instruction cache)
   constexpr int QMAX_ = (CGS_STAGE_MAX / TRC + CGS_NW - 1) / CGS_NW;
@@ -207,7 +211,7 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
 
   auto tile_full = [&](int t) { return (long long)(t + 1) * TRC <= (long long)A.n; };
   auto issue = [&](int t, int s) {
-    double *dst = s ? A.stage1 : A.stage0;
+    double *dst = A.ring + (size_t)s * (L + 1) * TRC;
     if (A.maps) {
       if (tid == 0) issue_boxed(dst, A.maps, A.win, t * TRC, TRC, L, &A.bars[s]);
     } else {
@@ -217,17 +221,18 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
   };
 
   const int t0 = blockIdx.x;
-  if (t0 < ntiles && tile_full(t0)) issue(t0, 0);
-  if (t0 + G < ntiles && tile_full(t0 + G)) issue(t0 + G, 1);
+  const int NST = A.nst;
+  for (int i = 0; i < NST; ++i)
+    if (t0 + i * G < ntiles && tile_full(t0 + i * G)) issue(t0 + i * G, i);
 
-  int it = 0;
+  int it = 0, s = 0;
+  uint32_t phase = 0;
   for (int t = t0; t < ntiles; t += G, ++it) {
-    const int s = it & 1;
     const int r0 = t * TRC;
     const int rows = min(TRC, A.n - r0);
-    double *buf = s ? A.stage1 : A.stage0;
+    double *buf = A.ring + (size_t)s * (L + 1) * TRC;
     if (tile_full(t)) {
-      while (!mbar_try_wait(&A.bars[s], (uint32_t)((it >> 1) & 1))) {
+      while (!mbar_try_wait(&A.bars[s], phase)) {
       }
     } else {  // partial tail tile (only the globally last one): generic loads
       for (int l = 0; l <= L; ++l) {
@@ -313,21 +318,25 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
     if (MODE != CGS_DOT) fence_proxy_async();  // wt was written via the generic proxy
     __syncthreads();  // stage s consumed
     {
-      const int tn = t + 2 * G;
+      const int tn = t + NST * G;
       if (tn < ntiles && tile_full(tn)) issue(tn, s);
+    }
+    if (++s == NST) {
+      s = 0;
+      phase ^= 1u;
     }
   }
 }
 
-// Stage layout: (L+1) x TR doubles; rows [0, L) are basis slots, row L is w.
+// Tile layout: (L+1) x TR doubles; rows [0, L) are basis slots, row L is w.
 template <int MODE>
 __global__ void __launch_bounds__(CGS_BS, 2)
     k_cgs(int n, double *__restrict__ V, long long pitch, GWork W, const double *cin,
           const double *win, double *wout, double *part, int G, unsigned *counter,
-          int stage_doubles, int use_cond, cudaGraphConditionalHandle cond,
+          int ring_doubles, int use_cond, cudaGraphConditionalHandle cond,
           const char *__restrict__ vmaps, int trmax) {
   extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bars[CGS_MAXST];
   __shared__ double cs[MAXR + 1];
   __shared__ double red[CGS_BS];
   __shared__ bool is_last;
@@ -344,9 +353,12 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   double *out = (MODE == CGS_UPD_NORM) ? V + (size_t)L * pitch : wout;
   // tile rows: largest power of two with (L+1)*TR <= stage, within [32, 1024]
   int TR = trmax;
-  while (TR > 32 && (L + 1) * TR > stage_doubles) TR >>= 1;
+  while (TR > 32 && 2 * (L + 1) * TR > ring_doubles) TR >>= 1;
+  // as many tiles in flight as the ring holds (short tiles at mid j would
+  // otherwise leave most of the shared memory idle)
+  int nst = ring_doubles / ((L + 1) * TR);
+  nst = nst > CGS_MAXST ? CGS_MAXST : nst;
   const int ntiles = (n + TR - 1) / TR;
-  double *stage0 = sm, *stage1 = sm + stage_doubles;
   const int nd = (MODE == CGS_DOT) ? L + 1 : L;  // dot entries (DOT: + ||w||^2)
   if (TR <= 256 && vmaps) vmaps += (size_t)(__ffs(TR) - 6) * VM_B * sizeof(CUtensorMap);
 
@@ -354,13 +366,12 @@ __global__ void __launch_bounds__(CGS_BS, 2)
     if (MODE != CGS_DOT) cs[l] = W.alpha[l] * cin[l];
   }
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int i = 0; i < nst; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  TileArgs A{n, L, G, ntiles, V, pitch, win, out, stage0, stage1, bars, cs, red,
+  TileArgs A{n, L, G, ntiles, V, pitch, win, out, sm, nst, bars, cs, red,
              TR <= 256 ? vmaps : nullptr};
   double nrm = 0.0;
   double acc[CGS_Q];
@@ -498,17 +509,19 @@ static int cgs_trmax() {
   return v;
 }
 
+// Shared-memory ring per CTA, in doubles: 2 x 52 KB (2 CTAs per SM) unless
+// the restart length needs two 32-row tiles of more slots.
 int Engine::cgs_stage_doubles() const {
-  static_assert(6144 <= CGS_STAGE_MAX, "stage floor above the unroll bound");
+  static_assert(6656 <= CGS_STAGE_MAX, "ring floor above the unroll bound");
   int st = (vcap + 2) * 32;  // <= CGS_STAGE_MAX (vcap <= MAXR)
-  return st < 6144 ? 6144 : st;
+  return 2 * (st < 6656 ? 6656 : st);
 }
 
 // One Arnoldi orthogonalisation: 3 fused sweeps; the last also finishes the
 // Hessenberg column (Givens, estimate, exit test) in its final CTA.
 void Engine::cgs(long long n) {
   const int stage = cgs_stage_doubles();
-  const size_t smem = 2 * (size_t)stage * sizeof(double);
+  const size_t smem = (size_t)stage * sizeof(double);
   if (cgs_smem_set < smem) {
     check(cudaFuncSetAttribute(k_cgs<CGS_DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem), "smem attr");
@@ -536,7 +549,7 @@ void Engine::cgs(long long n) {
 // finished (k_arnoldi_finish) from the global ||w||.  j is known on the host.
 void Engine::cgs_slab(long long n, int j) {
   const int stage = cgs_stage_doubles();
-  const size_t smem = 2 * (size_t)stage * sizeof(double);
+  const size_t smem = (size_t)stage * sizeof(double);
   if (cgs_smem_set < smem) {
     check(cudaFuncSetAttribute(k_cgs<CGS_DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem), "smem attr");

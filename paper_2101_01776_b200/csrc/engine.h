@@ -166,7 +166,7 @@ struct Engine {
   CycleGraph &cycle_graph(const BlockSpec &B, long long n);
   void arnoldi_iteration(const BlockSpec &B, long long n);
   void drop_graphs();
-  int cgs_stage_doubles() const;
+  int cgs_stage_doubles() const;  // CGS shared-memory ring per CTA (doubles)
   void cgs(long long n);  // cgs.cu
   // stencil.cu (register-sliding 2-D / 3-D kernels)
   dim3 slide_grid(int &span) const;
