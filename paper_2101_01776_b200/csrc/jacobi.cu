@@ -175,6 +175,230 @@ __global__ void __launch_bounds__(JW * 32)
   if (zero_diag && flag_ctrl) flag_ctrl->zero_diag = 1;
 }
 
+// ---------------------------------------------------------------------------
+// Column-pair variant (nx even, nx >= 64): lane l owns the aligned column pair
+// (c, c+1), c = strip start + 2l, so a warp covers a 64-column strip and emits
+// 64 - 2*HS columns (HS = halo rounded up to even, keeping the pairs 16-byte
+// aligned for double2 loads/stores).  Against the one-column kernel: twice the
+// independent work per lane (the sweep chain is latency-bound), one shuffle
+// per neighbour per pair instead of per point, no per-row reciprocal when the
+// diagonal is constant (Burgers), and sweep m skips the rows outside the band
+// it must supply to sweep m+1 ([y0-(K-m), y1+(K-m))) -- all warp-uniform.
+// The input rows (a, r, coupling field) stream through a per-warp ring of
+// JRING rows in shared memory filled with cp.async, so the loads run JRING
+// rows ahead without holding registers (the sweep chain is load-latency bound).
+constexpr int JPW = 4;   // warps per CTA
+constexpr int JRING = 8; // rows in flight per warp (cp.async ring in shared memory)
+
+namespace {
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int KIND>
+__device__ __forceinline__ void lx_pair(const Grid &g, const KindParams &kp, double sigma,
+                                        const double *am, const double *ac, const double *ap,
+                                        const double *xm, const double *xc, const double *xp,
+                                        double *lx) {
+  // same expression order as lx_col (left + right - 2 centre) for each column
+  if (KIND == KIND_NLDIFF) {
+    const double ax0 = ac[0] * xc[0], ax1 = ac[1] * xc[1];
+    const double axl = shfl_up1(ax1), axr = shfl_dn1(ax0);
+    lx[0] = g.ih2[0] * (axl + ax1 - 2.0 * ax0) + g.ih2[1] * (am[0] * xm[0] + ap[0] * xp[0] - 2.0 * ax0);
+    lx[1] = g.ih2[0] * (ax0 + axr - 2.0 * ax1) + g.ih2[1] * (am[1] * xm[1] + ap[1] * xp[1] - 2.0 * ax1);
+  } else if (KIND == KIND_BURGERS) {
+    const double ax0 = ac[0] * xc[0], ax1 = ac[1] * xc[1];
+    const double axl = shfl_up1(ax1), axr = shfl_dn1(ax0);
+    const double xl = shfl_up1(xc[1]), xr = shfl_dn1(xc[0]);
+    const double adv0 = g.i2h[0] * (ax1 - axl) + g.i2h[1] * (ap[0] * xp[0] - am[0] * xm[0]);
+    const double adv1 = g.i2h[0] * (axr - ax0) + g.i2h[1] * (ap[1] * xp[1] - am[1] * xm[1]);
+    const double lap0 = g.ih2[0] * (xl + xc[1] - 2.0 * xc[0]) + g.ih2[1] * (xm[0] + xp[0] - 2.0 * xc[0]);
+    const double lap1 = g.ih2[0] * (xc[0] + xr - 2.0 * xc[1]) + g.ih2[1] * (xm[1] + xp[1] - 2.0 * xc[1]);
+    lx[0] = -adv0 + sigma * kp.nu * lap0;
+    lx[1] = -adv1 + sigma * kp.nu * lap1;
+  } else {
+    const double xl = shfl_up1(xc[1]), xr = shfl_dn1(xc[0]);
+    const double lap0 = g.ih2[0] * (xl + xc[1] - 2.0 * xc[0]) + g.ih2[1] * (xm[0] + xp[0] - 2.0 * xc[0]);
+    const double lap1 = g.ih2[0] * (xc[0] + xr - 2.0 * xc[1]) + g.ih2[1] * (xm[1] + xp[1] - 2.0 * xc[1]);
+    const double ds0 = g.i2h[0] * (xc[1] - xl) + g.i2h[1] * (xp[0] - xm[0]);
+    const double ds1 = g.i2h[0] * (xr - xc[0]) + g.i2h[1] * (xp[1] - xm[1]);
+    lx[0] = sigma * (kp.nu * lap0 + kp.c * ds0) + ac[0] * xc[0];
+    lx[1] = sigma * (kp.nu * lap1 + kp.c * ds1) + ac[1] * xc[1];
+  }
+}
+
+}  // namespace
+
+template <int KIND, int K>
+__global__ void __launch_bounds__(JPW * 32)
+    k_jacobi_pair2d(Grid g, KindParams kp, Op L, double alpha, double dt, VecIn vin, int in_off,
+                    FRef zcr, double cpl, double *__restrict__ x_out, int span, int strips,
+                    int nwarps, GCtrl *flag_ctrl, const GCtrl *skip) {
+  if (skip && skip->cycle_done) return;
+  constexpr int H = K - 1;
+  constexpr int HS = (H + 1) & ~1;
+  constexpr int WC = 64 - 2 * HS;
+  constexpr bool CONST_D = (KIND == KIND_BURGERS);
+  const int gw = blockIdx.x * JPW + (threadIdx.x >> 5);
+  if (gw >= nwarps) return;  // whole warp idle
+  const int strip = gw % strips, band = gw / strips;
+  double scale;
+  const FRef inr = vin_resolve(vin, in_off, scale);
+  const FRef ar = fref(L);
+  const bool has_zc = zcr.base != nullptr;
+  const int lane = threadIdx.x & 31;
+  const int nx = g.nx, ny = g.ny;
+  const int x0 = strip * WC;
+  const int li = 2 * lane;  // strip-local index of the pair's first column
+  int c0 = x0 - HS + li;
+  c0 = c0 < 0 ? c0 + nx : (c0 >= nx ? c0 - nx : c0);
+  const bool valid = li >= HS && li < 64 - HS && x0 - HS + li < nx;
+  const int y0 = band * span;
+  const int y1 = min(ny, y0 + span);
+  const double sig = L.sigma;
+
+  double A[K + 1][2];               // a rows t-K .. t
+  double ID[K + 1][2];              // 1/D rows t-K .. t (unused if CONST_D)
+  double R[K][2];                   // r rows t-K+1 .. t
+  double X[K][3][2];                // sweep m (1..K-1): rows rho_m-2 .. rho_m
+#pragma unroll
+  for (int i = 0; i <= K; ++i) A[i][0] = A[i][1] = 0.0;
+#pragma unroll
+  for (int i = 0; i <= K; ++i) ID[i][0] = ID[i][1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) R[i][0] = R[i][1] = 0.0;
+#pragma unroll
+  for (int m = 0; m < K; ++m)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) X[m][i][0] = X[m][i][1] = 0.0;
+  bool zero_diag = false;
+  double idc = 0.0;
+  if (CONST_D) {
+    const double D = alpha - dt * diag_of<KIND>(g, kp, 0.0, sig);
+    zero_diag = (D == 0.0);
+    idc = 1.0 / D;
+  }
+
+  const int t0 = y0 - H, t1 = y1 + H;  // input rows [t0, t1)
+  auto rowp = [&](const FRef &f, int t) -> const double * {
+    if (!g.slab) {
+      const int s = t < 0 ? t + ny : (t >= ny ? t - ny : t);
+      return f.base + (size_t)s * nx;
+    }
+    return plane_ptr(f, t, ny, nx, 1);
+  };
+  // ring slot layout per warp: [JRING][3 fields][64 columns]
+  extern __shared__ __align__(16) double jring[];
+  double *ring = jring + (size_t)(threadIdx.x >> 5) * JRING * 3 * 64;
+  const int nf = has_zc ? 3 : 2;
+  auto issue_row = [&](int t, int slot) {
+    if (t < t1) {
+      double *d = ring + slot * 3 * 64 + 2 * lane;
+      cp_async16(d, rowp(ar, t) + c0);
+      cp_async16(d + 64, rowp(inr, t) + c0);
+      if (nf == 3) cp_async16(d + 128, rowp(zcr, t) + c0);
+    }
+    cp_async_commit();  // (empty groups past the end keep the count uniform)
+  };
+  auto read_row = [&](int slot, double2 &av, double2 &rv) {
+    const double *d = ring + slot * 3 * 64 + 2 * lane;
+    av = *reinterpret_cast<const double2 *>(d);
+    const double2 in = *reinterpret_cast<const double2 *>(d + 64);
+    double r0 = scale * in.x, r1 = scale * in.y;
+    if (nf == 3) {
+      const double2 z = *reinterpret_cast<const double2 *>(d + 128);
+      r0 = r0 + cpl * z.x;
+      r1 = r1 + cpl * z.y;
+    }
+    rv = make_double2(r0, r1);
+  };
+#pragma unroll
+  for (int i = 0; i < JRING; ++i) issue_row(t0 + i, i);
+
+  auto step = [&](int t, double2 a_in, double2 r_in) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      A[i][0] = A[i + 1][0];
+      A[i][1] = A[i + 1][1];
+      if (!CONST_D) {
+        ID[i][0] = ID[i + 1][0];
+        ID[i][1] = ID[i + 1][1];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < K - 1; ++i) {
+      R[i][0] = R[i + 1][0];
+      R[i][1] = R[i + 1][1];
+    }
+    A[K][0] = a_in.x;
+    A[K][1] = a_in.y;
+    R[K - 1][0] = r_in.x;
+    R[K - 1][1] = r_in.y;
+    if (!CONST_D) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const double D = alpha - dt * diag_of<KIND>(g, kp, A[K][c], sig);
+        zero_diag |= (D == 0.0);
+        ID[K][c] = 1.0 / D;
+      }
+    }
+    // sweep 1 at row t (pointwise from x_0 = 0)
+    double xn[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) xn[c] = OMEGA * ((CONST_D ? idc : ID[K][c]) * R[K - 1][c]);
+    // sweeps 2..K: sweep m at row rho = t - m + 1
+#pragma unroll
+    for (int m = 2; m <= K; ++m) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        X[m - 1][0][c] = X[m - 1][1][c];
+        X[m - 1][1][c] = X[m - 1][2][c];
+        X[m - 1][2][c] = xn[c];
+      }
+      const int rho = t - m + 1;
+      if (rho >= y0 - (K - m) && rho < y1 + (K - m)) {  // warp-uniform
+        double lx[2];
+        lx_pair<KIND>(g, kp, sig, A[K - m], A[K - m + 1], A[K - m + 2], X[m - 1][0], X[m - 1][1],
+                      X[m - 1][2], lx);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double xc = X[m - 1][1][c];
+          const double sx = alpha * xc - dt * lx[c];
+          const double id = CONST_D ? idc : ID[K - m + 1][c];
+          xn[c] = xc + OMEGA * (id * (R[K - m][c] - sx));
+        }
+      } else {
+        xn[0] = xn[1] = 0.0;
+      }
+    }
+    const int yo = t - H;
+    if (valid && yo >= y0 && yo < y1)
+      *reinterpret_cast<double2 *>(x_out + (size_t)yo * nx + c0) = make_double2(xn[0], xn[1]);
+  };
+  int slot = 0;
+  for (int t = t0; t < t1; ++t) {
+    cp_async_wait<JRING - 1>();  // row t (the oldest group) has landed
+    double2 av, rv;
+    read_row(slot, av, rv);
+    issue_row(t + JRING, slot);  // refill the slot just read (own lane only)
+    slot = slot + 1 == JRING ? 0 : slot + 1;
+    step(t, av, rv);
+  }
+  cp_async_wait<0>();
+  if (zero_diag && flag_ctrl) flag_ctrl->zero_diag = 1;
+}
+
 // launcher: returns false when the fused path does not apply
 bool Engine::jacobi_chain_fused(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
                                 int in_off, const double *zc, double cpl, double *x_out,
@@ -182,6 +406,53 @@ bool Engine::jacobi_chain_fused(const Op &L, double alpha, double dt, int inner,
   if (!fused_jacobi || ndim != 2 || inner < 1 || inner > 6 || grid.nx < 32 ||
       grid.ny < 2 * inner)
     return false;
+  if (pair_jacobi && grid.nx % 2 == 0 && grid.nx >= 64) {
+    const int wc = 64 - 2 * (inner & ~1);  // 64 - 2*HS, HS = (H+1) & ~1 with H = inner-1
+    const int strips = (grid.nx + wc - 1) / wc;
+    long long target = (long long)sms * jwarps_per_sm;
+    long long bands = target / strips;
+    bands = bands < 1 ? 1 : bands;
+    int span = (int)((grid.ny + bands - 1) / bands);
+    span = span < 8 ? 8 : (span > 128 ? 128 : span);
+    if (jspan_override > 0) span = jspan_override;
+    if (span > grid.ny) span = grid.ny;
+    const int nb = (grid.ny + span - 1) / span;
+    const int nwarps = strips * nb;
+    const int blocks = (nwarps + JPW - 1) / JPW;
+    auto go2 = [&](auto KD, auto KK) {
+      static bool attr = false;  // one per instantiation
+      if (!attr) {
+        check(cudaFuncSetAttribute(
+                  (const void *)k_jacobi_pair2d<decltype(KD)::value, decltype(KK)::value>,
+                  cudaFuncAttributeMaxDynamicSharedMemorySize, JPW * JRING * 3 * 64 * 8),
+              "jacobi ring smem");
+        attr = true;
+      }
+      k_jacobi_pair2d<decltype(KD)::value, decltype(KK)::value>
+          <<<blocks, JPW * 32, JPW * JRING * 3 * 64 * sizeof(double), stream>>>(
+          grid, kp, opref(L), alpha, dt, vin, in_off,
+          zc ? ref(zc) : FRef{nullptr, nullptr, nullptr}, cpl, x_out, span, strips, nwarps,
+          ctrl_dev, skip);
+    };
+    auto with_k2 = [&](auto KD) {
+      switch (inner) {
+        case 1: go2(KD, std::integral_constant<int, 1>{}); break;
+        case 2: go2(KD, std::integral_constant<int, 2>{}); break;
+        case 3: go2(KD, std::integral_constant<int, 3>{}); break;
+        case 4: go2(KD, std::integral_constant<int, 4>{}); break;
+        case 5: go2(KD, std::integral_constant<int, 5>{}); break;
+        default: go2(KD, std::integral_constant<int, 6>{}); break;
+      }
+    };
+    switch (prob.kind) {
+      case KIND_NLDIFF: with_k2(std::integral_constant<int, KIND_NLDIFF>{}); break;
+      case KIND_BURGERS: with_k2(std::integral_constant<int, KIND_BURGERS>{}); break;
+      default: with_k2(std::integral_constant<int, KIND_RAD>{}); break;
+    }
+    count(1);
+    counters.precond_bytes += 8.0 * N * (zc ? 4.0 : 3.0);
+    return true;
+  }
   const int H = inner - 1;
   const int wcols = 32 - 2 * H;
   const int xt = (grid.nx + wcols - 1) / wcols;

@@ -560,7 +560,12 @@ int Engine::grid_for(long long n) const {
   return (int)b;
 }
 
-void Engine::count(int k) { counters.kernel_launches += k; }
+// every launcher reports here: a failed launch (bad configuration, shared
+// memory over the limit) surfaces immediately instead of as a stalled solve
+void Engine::count(int k) {
+  counters.kernel_launches += k;
+  check(cudaPeekAtLastError(), "kernel launch");
+}
 
 double Engine::norm2(const double *x, long long n, const GCtrl *skip) {
   k_norm2<256><<<G, 256, 0, stream>>>((int)n, x, part, G, &scal_dev[0], counter, skip);

@@ -8,6 +8,8 @@
 // row from L2).  Used by the Jacobi sweeps (ShiftedSolver inner solves,
 // src/irk_core.py:117-123), the block operators (src/irk_core.py:126-140,
 // 216-219) and the stage residual (src/nonlinear.py:145-152).
+#include <cstdlib>
+
 #include "engine.h"
 
 namespace irkg {
@@ -100,9 +102,10 @@ __device__ __forceinline__ double wsum2(double v) {
 }
 
 // fold one value per CTA through the last-CTA ticket (deterministic order)
+template <int NWARP = SBX / 32>
 __device__ void cta_reduce_store(double v, double *part, int nblk, unsigned *counter,
                                  double *out) {
-  __shared__ double red[SBX / 32];
+  __shared__ double red[NWARP];
   __shared__ bool last;
   const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   v = wsum2(v);
@@ -110,7 +113,7 @@ __device__ void cta_reduce_store(double v, double *part, int nblk, unsigned *cou
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < SBX / 32; ++w) t += red[w];
+    for (int w = 0; w < NWARP; ++w) t += red[w];
     part[bid] = t;
     __threadfence();
     last = (atomicAdd(counter, 1u) == (unsigned)(nblk - 1));
@@ -127,6 +130,20 @@ __device__ void cta_reduce_store(double v, double *part, int nblk, unsigned *cou
       *counter = 0u;
     }
   }
+}
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 }  // namespace
@@ -297,6 +314,163 @@ __global__ void __launch_bounds__(SBX)
   }
 }
 
+// ------------------------------------------- block operator, 2-D strips
+// Same operator as k_block_op_s (identical lx_nb arithmetic), laid out for
+// memory-level parallelism: a warp owns a 64-column strip of aligned column
+// pairs (60 valid; x-neighbours by shuffle) and slides along y through a
+// band of rows; every input row (z1 [, z2], a1 [, a2, c12, c21]) streams
+// through a per-warp ring of BRING rows in shared memory filled by cp.async,
+// BRING-2 rows ahead of the row being computed.  (The one-column slide keeps
+// only one row in flight per thread and is load-latency bound.)
+constexpr int BPW = 2;    // warps per CTA
+constexpr int BRING = 8;  // ring rows per warp
+constexpr int BWC = 60;   // valid columns per strip (halo 2 keeps pairs aligned)
+
+template <int SIZE>
+constexpr int bop_nf() {
+  return SIZE == 1 ? 2 : 6;  // ring fields: z1, a1 [, z2, a2, c12, c21]
+}
+
+template <int KIND, int SIZE>
+__global__ void __launch_bounds__(BPW * 32)
+    k_block_op_strip(Grid g, KindParams kp, double eta, double beta, double phi, double dt,
+                     Op l1, Op l2, Op c12, Op c21, FRef z1r, FRef z2r, double *__restrict__ w,
+                     const double *__restrict__ b, int span, int strips, int nwarps,
+                     double *part, unsigned *counter, double *out_norm, const GCtrl *skip) {
+  if (skip && skip->cycle_done) return;
+  constexpr int NF = bop_nf<SIZE>();
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * BPW + (threadIdx.x >> 5);
+  double nrm = 0.0;
+  if (gw < nwarps) {
+    const int nx = g.nx, ny = g.ny, n = g.n;
+    const int strip = gw % strips, band = gw / strips;
+    const int x0 = strip * BWC;
+    const int li = 2 * lane;
+    int c0 = x0 - 2 + li;
+    c0 = c0 < 0 ? c0 + nx : (c0 >= nx ? c0 - nx : c0);
+    const bool valid = li >= 2 && li < 62 && x0 - 2 + li < nx;
+    const int y0 = band * span, y1 = min(ny, y0 + span);
+    const bool h12 = SIZE == 2 && c12.present, h21 = SIZE == 2 && c21.present;
+    FRef fr[NF];
+    fr[0] = z1r;
+    fr[1] = fref(l1);
+    if (SIZE == 2) {
+      fr[2] = z2r;
+      fr[3] = fref(l2);
+      fr[4] = fref(c12);
+      fr[5] = fref(c21);
+    }
+    bool have[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) have[f] = true;
+    if (SIZE == 2) {
+      have[4] = h12;
+      have[5] = h21;
+    }
+    extern __shared__ __align__(16) double bring[];
+    double *ring = bring + (size_t)(threadIdx.x >> 5) * BRING * NF * 64 + li;
+    auto rowp = [&](const FRef &f, int t) -> const double * {
+      if (!g.slab) {
+        const int s = t < 0 ? t + ny : (t >= ny ? t - ny : t);
+        return f.base + (size_t)s * nx;
+      }
+      return plane_ptr(f, t, ny, nx, 1);
+    };
+    auto issue_row = [&](int t) {
+      if (t <= y1) {  // rows y0-1 .. y1 feed the band
+        double *d = ring + (t & (BRING - 1)) * NF * 64;
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+          if (have[f]) cp_async16(d + f * 64, rowp(fr[f], t) + c0);
+      }
+      cp_async_commit();  // (empty groups past the end keep the count uniform)
+    };
+    // pair values of field f at row t (from the ring)
+    auto rd = [&](int f, int t) {
+      return *reinterpret_cast<const double2 *>(ring + ((t & (BRING - 1)) * NF + f) * 64);
+    };
+    // neighbourhoods of the two columns from rows (m, c, p) of one field
+    auto nb2 = [&](double2 m, double2 c, double2 p, Nb &n0, Nb &n1) {
+      n0.c = c.x;
+      n0.v[0] = __shfl_sync(0xffffffffu, c.y, (lane + 31) & 31);
+      n0.v[1] = c.y;
+      n0.v[2] = m.x;
+      n0.v[3] = p.x;
+      n0.v[4] = n0.v[5] = 0.0;
+      n1.c = c.y;
+      n1.v[0] = c.x;
+      n1.v[1] = __shfl_sync(0xffffffffu, c.x, (lane + 1) & 31);
+      n1.v[2] = m.y;
+      n1.v[3] = p.y;
+      n1.v[4] = n1.v[5] = 0.0;
+    };
+    auto field_nb = [&](int f, int s, Nb &n0, Nb &n1) {
+      nb2(rd(f, s - 1), rd(f, s), rd(f, s + 1), n0, n1);
+    };
+#pragma unroll
+    for (int i = 0; i < BRING - 1; ++i) issue_row(y0 - 1 + i);  // rows y0-1 .. y0+5
+    for (int s = y0; s < y1; ++s) {
+      cp_async_wait<BRING - 4>();  // rows up to s+1 have landed (s+2 .. s+5 may pend)
+      Nb x1[2], a1n[2];
+      field_nb(0, s, x1[0], x1[1]);
+      field_nb(1, s, a1n[0], a1n[1]);
+      double top[2], bot[2];
+      if (SIZE == 1) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          top[c] = eta * x1[c].c - dt * lx_nb<KIND, 2>(g, kp, a1n[c], l1.sigma, x1[c]);
+      } else {
+        Nb x2[2], a2n[2];
+        field_nb(2, s, x2[0], x2[1]);
+        field_nb(3, s, a2n[0], a2n[1]);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          top[c] = eta * x1[c].c - dt * lx_nb<KIND, 2>(g, kp, a1n[c], l1.sigma, x1[c]) +
+                   phi * x2[c].c;
+          bot[c] = -(beta * beta / phi) * x1[c].c + eta * x2[c].c -
+                   dt * lx_nb<KIND, 2>(g, kp, a2n[c], l2.sigma, x2[c]);
+        }
+        if (h12) {
+          Nb cn[2];
+          field_nb(4, s, cn[0], cn[1]);
+#pragma unroll
+          for (int c = 0; c < 2; ++c) top[c] -= dt * lx_nb<KIND, 2>(g, kp, cn[c], c12.sigma, x2[c]);
+        }
+        if (h21) {
+          Nb cn[2];
+          field_nb(5, s, cn[0], cn[1]);
+#pragma unroll
+          for (int c = 0; c < 2; ++c) bot[c] -= dt * lx_nb<KIND, 2>(g, kp, cn[c], c21.sigma, x1[c]);
+        }
+      }
+      if (valid) {
+        const size_t p = (size_t)s * nx + c0;
+        if (b) {
+          const double2 b1 = *reinterpret_cast<const double2 *>(b + p);
+          top[0] = b1.x - top[0];
+          top[1] = b1.y - top[1];
+          nrm += top[0] * top[0] + top[1] * top[1];
+          if (SIZE == 2) {
+            const double2 b2 = *reinterpret_cast<const double2 *>(b + p + n);
+            bot[0] = b2.x - bot[0];
+            bot[1] = b2.y - bot[1];
+            nrm += bot[0] * bot[0] + bot[1] * bot[1];
+          }
+        }
+        *reinterpret_cast<double2 *>(w + p) = make_double2(top[0], top[1]);
+        if (SIZE == 2) *reinterpret_cast<double2 *>(w + p + n) = make_double2(bot[0], bot[1]);
+      }
+      issue_row(s + BRING - 2);  // into the slot of row s-2 (no longer read)
+    }
+    cp_async_wait<0>();
+  }
+  if (b) {
+    const int nblk = gridDim.x;
+    cta_reduce_store<BPW>(nrm, part, nblk, counter, out_norm);
+  }
+}
+
 // ------------------------------------------------------- stage residual
 // F_i = N(U_i) - K_i, ||F||^2   (src/nonlinear.py:148-152)
 template <int KIND, int NDIM>
@@ -416,16 +590,21 @@ static void dispatch_kd23(int kind, int ndim, F f) {
 
 // grid + slide span for ~8 CTAs per SM
 dim3 Engine::slide_grid(int &span) const {
+  static int cps = -1;
+  if (cps < 0) {
+    const char *e = getenv("IRKG_SLIDE_CPS");
+    cps = e && atoi(e) > 0 ? atoi(e) : 8;
+  }
   if (ndim == 2) {
     const int bx = (grid.nx + SBX - 1) / SBX;
-    long long target = (long long)sms * 8;
+    long long target = (long long)sms * cps;
     int sp = (int)((long long)bx * grid.ny / target);
     sp = sp < 2 ? 2 : (sp > 32 ? 32 : sp);
     span = sp;
     return dim3(bx, (grid.ny + sp - 1) / sp, 1);
   }
   const int bx = (grid.nx + 31) / 32, by = (grid.ny + SBX / 32 - 1) / (SBX / 32);
-  long long target = (long long)sms * 8;
+  long long target = (long long)sms * cps;
   int sp = (int)((long long)bx * by * grid.nz / target);
   sp = sp < 2 ? 2 : (sp > 32 ? 32 : sp);
   span = sp;
@@ -446,6 +625,50 @@ void Engine::jac_sweep_s(const Op &L, double alpha, double dt, const VecIn &vin,
 
 void Engine::block_op_s(const BlockSpec &B, const double *z, double *w, const double *b,
                         double *out_norm, const GCtrl *skip) {
+  if (strip_op && ndim == 2 && grid.nx % 2 == 0 && grid.nx >= 64) {
+    // strips of BWC columns x bands of rows: ~bop_wps resident warps per SM
+    const int strips = (grid.nx + BWC - 1) / BWC;
+    const int wps = B.size == 1 ? 2 * bop_wps : bop_wps;
+    long long bands = (long long)sms * wps / strips;
+    bands = bands < 1 ? 1 : bands;
+    int span = (int)((grid.ny + bands - 1) / bands);
+    span = span < 4 ? 4 : span;
+    if (span > grid.ny) span = grid.ny;
+    const int nwarps = strips * ((grid.ny + span - 1) / span);
+    const int blocks = (nwarps + BPW - 1) / BPW;
+    const FRef z1 = ref(z);
+    auto launch = [&](auto KD) {
+      constexpr int K_ = decltype(KD)::value;
+      // opt in above the 48 KB default (static + dynamic shared memory)
+      static bool attr[2] = {false, false};
+      auto opt_in = [&](const void *fn, int size, int bytes) {
+        if (!attr[size - 1]) {
+          check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                "strip op smem");
+          attr[size - 1] = true;
+        }
+      };
+      opt_in((const void *)k_block_op_strip<K_, 1>, 1, BPW * BRING * bop_nf<1>() * 64 * 8);
+      opt_in((const void *)k_block_op_strip<K_, 2>, 2, BPW * BRING * bop_nf<2>() * 64 * 8);
+      if (B.size == 1)
+        k_block_op_strip<K_, 1><<<blocks, BPW * 32, BPW * BRING * bop_nf<1>() * 64 * 8, stream>>>(
+            grid, kp, B.eta, B.beta, B.phi, B.dt, opref(B.l1), opref(B.l2), opref(B.c12),
+            opref(B.c21), z1, FRef{nullptr, nullptr, nullptr}, w, b, span, strips, nwarps, part,
+            counter, out_norm, skip);
+      else
+        k_block_op_strip<K_, 2><<<blocks, BPW * 32, BPW * BRING * bop_nf<2>() * 64 * 8, stream>>>(
+            grid, kp, B.eta, B.beta, B.phi, B.dt, opref(B.l1), opref(B.l2), opref(B.c12),
+            opref(B.c21), z1, ref(z + N), w, b, span, strips, nwarps, part, counter, out_norm,
+            skip);
+    };
+    switch (prob.kind) {
+      case KIND_NLDIFF: launch(std::integral_constant<int, KIND_NLDIFF>{}); break;
+      case KIND_BURGERS: launch(std::integral_constant<int, KIND_BURGERS>{}); break;
+      default: launch(std::integral_constant<int, KIND_RAD>{}); break;
+    }
+    count(1);
+    return;
+  }
   int span;
   const dim3 gr = slide_grid(span);
   dispatch_kd23(prob.kind, ndim, [&](auto KD, auto ND) {
