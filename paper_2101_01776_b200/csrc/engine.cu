@@ -108,7 +108,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   if (const char *e = getenv("IRKG_PAIR_JACOBI")) pair_jacobi = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_JWPS")) jwarps_per_sm = atoi(e) > 0 ? atoi(e) : 12;
   if (const char *e = getenv("IRKG_STRIP_OP")) strip_op = (atoi(e) != 0);
-  if (const char *e = getenv("IRKG_BOP_WPS")) bop_wps = atoi(e) > 0 ? atoi(e) : 8;
+  if (const char *e = getenv("IRKG_BOP_WPS")) bop_wps = atoi(e) > 0 ? atoi(e) : 12;
   for (int i = 0; i < MAXS; ++i)
     for (int j = 0; j < MAXS; ++j) od_slot[i][j] = -1;
 }

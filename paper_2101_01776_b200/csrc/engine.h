@@ -210,7 +210,7 @@ struct Engine {
   bool pair_jacobi = true;   // column-pair Jacobi kernel (IRKG_PAIR_JACOBI=0: one column per lane)
   int jwarps_per_sm = 12;    // pair kernel: target resident warps per SM (IRKG_JWPS)
   bool strip_op = true;      // 2-D block operator on column-pair strips (IRKG_STRIP_OP=0: slide)
-  int bop_wps = 8;           // strip block operator: target warps per SM (IRKG_BOP_WPS)
+  int bop_wps = 12;          // strip block operator: target warps per SM (IRKG_BOP_WPS)
   bool jacobi_chain_fused(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
                           int in_off, const double *zc, double cpl, double *x_out,
                           const GCtrl *skip);

@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(SBX)
 // BRING-2 rows ahead of the row being computed.  (The one-column slide keeps
 // only one row in flight per thread and is load-latency bound.)
 constexpr int BPW = 2;    // warps per CTA
-constexpr int BRING = 8;  // ring rows per warp
+constexpr int BRING = 6;  // ring rows per warp (rows s-1..s+1 + BRING-3 ahead)
 constexpr int BWC = 60;   // valid columns per strip (halo 2 keeps pairs aligned)
 
 template <int SIZE>
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(BPW * 32)
     };
     auto issue_row = [&](int t) {
       if (t <= y1) {  // rows y0-1 .. y1 feed the band
-        double *d = ring + (t & (BRING - 1)) * NF * 64;
+        double *d = ring + ((t - y0 + 1) % BRING) * NF * 64;
 #pragma unroll
         for (int f = 0; f < NF; ++f)
           if (have[f]) cp_async16(d + f * 64, rowp(fr[f], t) + c0);
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(BPW * 32)
     };
     // pair values of field f at row t (from the ring)
     auto rd = [&](int f, int t) {
-      return *reinterpret_cast<const double2 *>(ring + ((t & (BRING - 1)) * NF + f) * 64);
+      return *reinterpret_cast<const double2 *>(ring + (((t - y0 + 1) % BRING) * NF + f) * 64);
     };
     // neighbourhoods of the two columns from rows (m, c, p) of one field
     auto nb2 = [&](double2 m, double2 c, double2 p, Nb &n0, Nb &n1) {
@@ -409,9 +409,9 @@ __global__ void __launch_bounds__(BPW * 32)
       nb2(rd(f, s - 1), rd(f, s), rd(f, s + 1), n0, n1);
     };
 #pragma unroll
-    for (int i = 0; i < BRING - 1; ++i) issue_row(y0 - 1 + i);  // rows y0-1 .. y0+5
+    for (int i = 0; i < BRING - 1; ++i) issue_row(y0 - 1 + i);  // rows y0-1 .. y0+BRING-3
     for (int s = y0; s < y1; ++s) {
-      cp_async_wait<BRING - 4>();  // rows up to s+1 have landed (s+2 .. s+5 may pend)
+      cp_async_wait<BRING - 4>();  // rows up to s+1 have landed (s+2 .. s+BRING-3 may pend)
       Nb x1[2], a1n[2];
       field_nb(0, s, x1[0], x1[1]);
       field_nb(1, s, a1n[0], a1n[1]);
