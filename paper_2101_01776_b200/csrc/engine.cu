@@ -108,6 +108,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   if (const char *e = getenv("IRKG_PAIR_JACOBI")) pair_jacobi = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_JWPS")) jwarps_per_sm = atoi(e) > 0 ? atoi(e) : 12;
   if (const char *e = getenv("IRKG_STRIP_OP")) strip_op = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_CGS_FUSED")) cgs_fused = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_BOP_WPS")) bop_wps = atoi(e) > 0 ? atoi(e) : 12;
   for (int i = 0; i < MAXS; ++i)
     for (int j = 0; j < MAXS; ++j) od_slot[i][j] = -1;
@@ -117,7 +118,7 @@ Engine::~Engine() {
   cudaStreamSynchronize(stream);
   void *bufs[] = {part, counter, scal_dev, ctrl_dev, W.H, W.cs, W.sn, W.g, W.alpha, W.y,
                   W.c1, W.c2, W.res, V, wbuf, zbuf, ubuf, tmp_x, tmp_t, U, F, Gs, Y, DK,
-                  Kst, RHS, ufield, opA, vmaps};
+                  Kst, RHS, ufield, opA, vmaps, gbar};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (ctrl_host) cudaFreeHost(ctrl_host);

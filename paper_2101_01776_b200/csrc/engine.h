@@ -150,6 +150,10 @@ struct Engine {
   void ensure_res(int maxit);
   int rescap = 0;
   size_t cgs_smem_set = 0;
+  size_t cgs3_smem_set = 0;
+  unsigned *gbar = nullptr;   // fused-CGS grid barrier {count, generation}
+  bool cgs_fused = false;     // one cooperative launch for the 3 CGS sweeps (IRKG_CGS_FUSED=1; measured
+                              // slower than 3 launches on config 1: 755M vs 796M DOF/s)
   // CUDA-graph execution of the Arnoldi loop: one graph per block system,
   // a WHILE conditional node whose condition the last CGS kernel clears.
   struct CycleGraph {
