@@ -685,7 +685,8 @@ static void validate_problem(const irkg_problem *prob, int rank, int nranks) {
     if (planes / nranks < GH)
       throw SolveError(IRKG_ERR_CONFIG, "slabs must hold at least 6 planes per rank");
   }
-  const long long nl = ((long long)(nranks > 1 ? 1 : 1)) * prob->nx * prob->ny * prob->nz / nranks + prob->nx * prob->ny;
+  // local points incl. one plane of slack for the uneven split
+  const long long nl = (long long)prob->nx * prob->ny * prob->nz / nranks + (long long)prob->nx * prob->ny;
   if (2 * nl >= (1LL << 31)) throw SolveError(IRKG_ERR_VALUE, "grid too large for one rank");
 }
 
