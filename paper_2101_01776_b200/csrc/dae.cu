@@ -33,32 +33,49 @@ struct P9 {
   double c, E, W, N, S, NE, NW, SE, SW;
 };
 
-struct Off9 {
-  int dxm, dxp, dym, dyp;
+// rows iy-1, iy, iy+1 of a field: ghost planes in slab mode, periodic wrap
+// otherwise (plane_ptr) -- the same values as flat periodic offsets
+struct R3 {
+  const double *m, *c, *p;
 };
 
-__device__ __forceinline__ Off9 off9(const Grid &g, int ix, int iy) {
-  Off9 o;
-  o.dxm = (ix == 0) ? g.nx - 1 : -1;
-  o.dxp = (ix == g.nx - 1) ? 1 - g.nx : 1;
-  o.dym = (iy == 0) ? (g.ny - 1) * g.nx : -g.nx;
-  o.dyp = (iy == g.ny - 1) ? -(g.ny - 1) * g.nx : g.nx;
-  return o;
+__device__ __forceinline__ R3 rows3(const FRef &f, const Grid &g, int iy) {
+  R3 r;
+  r.c = f.base + (size_t)iy * g.nx;
+  r.m = plane_ptr(f, iy - 1, g.ny, g.nx, g.slab);
+  r.p = plane_ptr(f, iy + 1, g.ny, g.nx, g.slab);
+  return r;
 }
 
-__device__ __forceinline__ P9 load9(const double *__restrict__ f, int p, const Off9 &o) {
+// a column and its periodic x-neighbours
+struct XO {
+  int c, m, p;
+};
+
+__device__ __forceinline__ XO xo_of(const Grid &g, int ix) {
+  return XO{ix, ix == 0 ? g.nx - 1 : ix - 1, ix == g.nx - 1 ? 0 : ix + 1};
+}
+
+__device__ __forceinline__ P9 load9(const R3 &r, const XO &x) {
   P9 v;
-  v.c = f[p];
-  v.E = f[p + o.dxp];
-  v.W = f[p + o.dxm];
-  v.N = f[p + o.dyp];
-  v.S = f[p + o.dym];
-  v.NE = f[p + o.dyp + o.dxp];
-  v.NW = f[p + o.dyp + o.dxm];
-  v.SE = f[p + o.dym + o.dxp];
-  v.SW = f[p + o.dym + o.dxm];
+  v.c = r.c[x.c];
+  v.E = r.c[x.p];
+  v.W = r.c[x.m];
+  v.N = r.p[x.c];
+  v.S = r.m[x.c];
+  v.NE = r.p[x.p];
+  v.NW = r.p[x.m];
+  v.SE = r.m[x.p];
+  v.SW = r.m[x.m];
   return v;
 }
+
+__device__ __forceinline__ P9 load9(const FRef &f, const Grid &g, int iy, const XO &x) {
+  return load9(rows3(f, g, iy), x);
+}
+
+// the pinned constraint row: global point 0 (on the rank that holds it)
+__device__ __forceinline__ bool pinned(const Grid &g, int p) { return g.pin && p == 0; }
 
 // 12 hx hy * J(psi, w): Arakawa's three forms summed
 __device__ __forceinline__ double jac_sum(const P9 &P, const P9 &W) {
@@ -80,9 +97,9 @@ __device__ __forceinline__ double jscale(const Grid &g) {
 }
 
 // L_eff(a, sigma) x = -J(a, x) + sigma nu Lap x
-__device__ __forceinline__ double ara_lx(const Grid &g, double nu, const double *a, double sigma,
-                                         const double *x, int p, const Off9 &o) {
-  const P9 A = load9(a, p, o), X = load9(x, p, o);
+__device__ __forceinline__ double ara_lx(const Grid &g, double nu, const FRef &a, double sigma,
+                                         const FRef &x, int iy, const XO &o) {
+  const P9 A = load9(a, g, iy, o), X = load9(x, g, iy, o);
   return -jscale(g) * jac_sum(A, X) + sigma * nu * lap9(g, X);
 }
 
@@ -143,20 +160,24 @@ constexpr int DBS = 256;
   for (int iy = blockIdx.x; iy < (g).ny; iy += gridDim.x)             \
     for (int ix = threadIdx.x; ix < (g).nx; ix += blockDim.x)
 
+// stage fields U_i, W_i (rows of UW) with their ghost planes
+struct DaeStageRefs {
+  FRef u[MAXS], w[MAXS];
+};
+
 // composite residual per stage: [N(U_i, W_i) - k_i ; G(U_i, W_i)] and ||.||^2
-__global__ void k_dae_residual(Grid g, double nu, double h2, int s, const double *__restrict__ UW,
+__global__ void k_dae_residual(Grid g, double nu, double h2, int s, DaeStageRefs R,
                                const double *__restrict__ K2, double *__restrict__ F2,
                                double *part, unsigned *counter, double *out) {
   const int n = g.n;
   double acc = 0.0;
   ROWS_LOOP(g) {
     const int p = iy * g.nx + ix;
-    const Off9 o = off9(g, ix, iy);
+    const XO o = xo_of(g, ix);
     for (int i = 0; i < s; ++i) {
-      const double *U = UW + (size_t)i * 2 * n, *Wp = U + n;
-      const P9 u = load9(U, p, o), w = load9(Wp, p, o);
+      const P9 u = load9(R.u[i], g, iy, o), w = load9(R.w[i], g, iy, o);
       const double fu = (-jscale(g) * jac_sum(w, u) + nu * lap9(g, u)) - K2[(size_t)i * 2 * n + p];
-      const double fw = (p == 0) ? w.c : h2 * (lap9(g, w) + u.c);
+      const double fw = pinned(g, p) ? w.c : h2 * (lap9(g, w) + u.c);
       F2[(size_t)i * 2 * n + p] = fu;
       F2[(size_t)i * 2 * n + n + p] = fw;
       acc += fu * fu + fw * fw;
@@ -166,15 +187,14 @@ __global__ void k_dae_residual(Grid g, double nu, double h2, int s, const double
 }
 
 // ||G(u, w)||^2 for the state uw = [u; w]
-__global__ void k_dae_gnorm(Grid g, double h2, const double *__restrict__ UW, double *part,
+__global__ void k_dae_gnorm(Grid g, double h2, const double *__restrict__ UW, FRef wr, double *part,
                             unsigned *counter, double *out) {
-  const int n = g.n;
   double acc = 0.0;
   ROWS_LOOP(g) {
     const int p = iy * g.nx + ix;
-    const Off9 o = off9(g, ix, iy);
-    const P9 w = load9(UW + n, p, o);
-    const double fw = (p == 0) ? w.c : h2 * (lap9(g, w) + UW[p]);
+    const XO o = xo_of(g, ix);
+    const P9 w = load9(wr, g, iy, o);
+    const double fw = pinned(g, p) ? w.c : h2 * (lap9(g, w) + UW[p]);
     acc += fw * fw;
   }
   reduce2<DBS>(acc, 0.0, part, gridDim.x, counter, out);
@@ -205,8 +225,10 @@ __global__ void k_dae_opfields(int n, OpWeights W, const double *__restrict__ UW
 // Jacobi on (alpha I - dt L_eff); first sweep from zero when x == nullptr
 __global__ void k_ara_jac(Grid g, double nu, Op L, double alpha, double dt, VecIn vin, int in_off,
                           const double *__restrict__ zc, double cpl, double *__restrict__ t_out,
-                          const double *__restrict__ t_in, const double *__restrict__ x,
+                          const double *__restrict__ t_in, FRef xr,
                           double *__restrict__ x_out, const GCtrl *skip) {
+  const double *x = xr.base;
+  const FRef ar = fref(L);
   if (skip && skip->cycle_done) return;
   double scale = 1.0;
   const double *in = t_in ? nullptr : vin_resolve(vin, in_off, scale).base;
@@ -227,9 +249,9 @@ __global__ void k_ara_jac(Grid g, double nu, Op L, double alpha, double dt, VecI
     if (!x) {
       x_out[p] = OMEGA * (invD * r);
     } else {
-      const Off9 o = off9(g, ix, iy);
+      const XO o = xo_of(g, ix);
       const double xc = x[p];
-      const double sx = alpha * xc - dt * ara_lx(g, nu, L.a, L.sigma, x, p, o);
+      const double sx = alpha * xc - dt * ara_lx(g, nu, ar, L.sigma, xr, iy, o);
       x_out[p] = xc + OMEGA * (invD * (r - sx));
     }
   }
@@ -238,29 +260,31 @@ __global__ void k_ara_jac(Grid g, double nu, Op L, double alpha, double dt, VecI
 // 1x1 / 2x2 block operator with the Arakawa L (apply_block2x2); b != null: residual + norm
 template <int SIZE>
 __global__ void k_ara_block_op(Grid g, double nu, double eta, double beta, double phi, double dt,
-                               Op l1, Op l2, Op c12, Op c21, const double *__restrict__ z,
+                               Op l1, Op l2, Op c12, Op c21, FRef z1r, FRef z2r,
                                double *__restrict__ w, const double *__restrict__ b, double *part,
                                unsigned *counter, double *out_norm, const GCtrl *skip) {
   if (skip && skip->cycle_done) return;
   const int n = g.n;
+  const FRef a1 = fref(l1), a2 = fref(l2), a12 = fref(c12), a21 = fref(c21);
   double nrm = 0.0;
   ROWS_LOOP(g) {
     const int p = iy * g.nx + ix;
-    const Off9 o = off9(g, ix, iy);
+    const XO o = xo_of(g, ix);
     if (SIZE == 1) {
-      double v = eta * z[p] - dt * ara_lx(g, nu, l1.a, l1.sigma, z, p, o);
+      const double *z = z1r.base;
+      double v = eta * z[p] - dt * ara_lx(g, nu, a1, l1.sigma, z1r, iy, o);
       if (b) {
         v = b[p] - v;
         nrm += v * v;
       }
       w[p] = v;
     } else {
-      const double *z1 = z, *z2 = z + n;
-      double top = eta * z1[p] - dt * ara_lx(g, nu, l1.a, l1.sigma, z1, p, o) + phi * z2[p];
+      const double *z1 = z1r.base, *z2 = z2r.base;
+      double top = eta * z1[p] - dt * ara_lx(g, nu, a1, l1.sigma, z1r, iy, o) + phi * z2[p];
       double bot = -(beta * beta / phi) * z1[p] + eta * z2[p] -
-                   dt * ara_lx(g, nu, l2.a, l2.sigma, z2, p, o);
-      if (c12.present) top -= dt * ara_lx(g, nu, c12.a, c12.sigma, z2, p, o);
-      if (c21.present) bot -= dt * ara_lx(g, nu, c21.a, c21.sigma, z1, p, o);
+                   dt * ara_lx(g, nu, a2, l2.sigma, z2r, iy, o);
+      if (c12.present) top -= dt * ara_lx(g, nu, a12, c12.sigma, z2r, iy, o);
+      if (c21.present) bot -= dt * ara_lx(g, nu, a21, c21.sigma, z1r, iy, o);
       if (b) {
         top = b[p] - top;
         bot = b[p + n] - bot;
@@ -281,6 +305,7 @@ struct DaeBacksub {
   int j[MAXS];
   double coef[2][MAXS];
   Op od[2][MAXS];
+  FRef yu[MAXS], yw[MAXS];  // y_u,j / y_w,j with ghost planes
 };
 
 __global__ void k_dae_backsub(Grid g, double nu, double h2, double dt, DaeBacksub T,
@@ -289,20 +314,20 @@ __global__ void k_dae_backsub(Grid g, double nu, double h2, double dt, DaeBacksu
   const int n = g.n;
   ROWS_LOOP(g) {
     const int p = iy * g.nx + ix;
-    const Off9 o = off9(g, ix, iy);
+    const XO o = xo_of(g, ix);
     for (int r = 0; r < T.rows; ++r) {
       double au = G2[(size_t)(T.row0 + r) * 2 * n + p];
       double aw = G2[(size_t)(T.row0 + r) * 2 * n + n + p];
       for (int q = 0; q < T.njs; ++q) {
-        const double *yu = Y2 + (size_t)T.j[q] * 2 * n, *yw = yu + n;
+        const double *yu = T.yu[q].base;
         const double c = T.coef[r][q];
         if (c != 0.0) au -= c * yu[p];
         const Op od = T.od[r][q];
         if (od.present) {
-          au += dt * ara_lx(g, nu, od.a, od.sigma, yu, p, o);
-          const P9 w9 = load9(yw, p, o);
-          const double gu = (p == 0) ? 0.0 : h2 * yu[p];
-          const double gw = (p == 0) ? w9.c : h2 * lap9(g, w9);
+          au += dt * ara_lx(g, nu, fref(od), od.sigma, T.yu[q], iy, o);
+          const P9 w9 = load9(T.yw[q], g, iy, o);
+          const double gu = pinned(g, p) ? 0.0 : h2 * yu[p];
+          const double gw = pinned(g, p) ? w9.c : h2 * lap9(g, w9);
           aw += dt * (od.sigma * gu + od.sigma * gw);
         }
       }
@@ -313,10 +338,11 @@ __global__ void k_dae_backsub(Grid g, double nu, double h2, double dt, DaeBacksu
 }
 
 // constraint rhs c = acc_w + dt * sigma * G_u y_u  (G_u row 0 is zero)
-__global__ void k_dae_crhs(int n, double dt, double sigma_h2, const double *__restrict__ accw,
-                           const double *__restrict__ yu, double *__restrict__ c) {
+__global__ void k_dae_crhs(int n, int pin, double dt, double sigma_h2,
+                           const double *__restrict__ accw, const double *__restrict__ yu,
+                           double *__restrict__ c) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
-    c[p] = (p == 0) ? accw[0] : accw[p] + dt * (sigma_h2 * yu[p]);
+    c[p] = (pin && p == 0) ? accw[0] : accw[p] + dt * (sigma_h2 * yu[p]);
 }
 
 // Poisson step 1: f = c / (sigma h^2) off the pin; f_0 = -sum_{i != 0} f_i
@@ -348,34 +374,36 @@ __global__ void k_pois_scale(int nx, int ny, double ih2x, double ih2y, cufftDoub
   }
 }
 
-// y = yt - yt_0 + c_0 / sigma;  out = post * y
-__global__ void k_pois_fix(int n, double post, double inv_sigma, const double *__restrict__ yt,
-                           const double *__restrict__ c, double *__restrict__ out) {
+// y = yt - yt_0 + c_0 / sigma;  out = post * y  (yt, c global; out = points
+// [off, off + n) of the global vector)
+__global__ void k_pois_fix(int n, long long off, double post, double inv_sigma,
+                           const double *__restrict__ yt, const double *__restrict__ c,
+                           double *__restrict__ out) {
   const double y0 = yt[0], pin = c[0] * inv_sigma;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
-    out[p] = post * ((yt[p] - y0) + pin);
+    out[p] = post * ((yt[off + p] - y0) + pin);
 }
 
 // composite true residual of the reordered 4x4 block (src/dae.py:238-253, 307-314):
 // out[0] = ||rhs - A x||^2, out[1] = ||rhs||^2; rhs = ACC (2 x 2N), x = Y2 rows r0, r0+1
 __global__ void k_dae_block_res(Grid g, double nu, double h2, double eta, double beta, double phi,
                                 double dt, Op l1, Op l2, double sig1, double sig2,
-                                const double *__restrict__ ACC, const double *__restrict__ X1,
-                                const double *__restrict__ X2, double *part, unsigned *counter,
-                                double *out) {
+                                const double *__restrict__ ACC, FRef x1ur, FRef x1wr, FRef x2ur,
+                                FRef x2wr, double *part, unsigned *counter, double *out) {
   const int n = g.n;
+  const FRef a1 = fref(l1), a2 = fref(l2);
   double rr = 0.0, bb = 0.0;
   ROWS_LOOP(g) {
     const int p = iy * g.nx + ix;
-    const Off9 o = off9(g, ix, iy);
-    const double *x1u = X1, *x1w = X1 + n, *x2u = X2, *x2w = X2 + n;
-    const double top1 = eta * x1u[p] - dt * ara_lx(g, nu, l1.a, l1.sigma, x1u, p, o) + phi * x2u[p];
-    const double top2 = eta * x2u[p] - dt * ara_lx(g, nu, l2.a, l2.sigma, x2u, p, o) -
+    const XO o = xo_of(g, ix);
+    const double *x1u = x1ur.base, *x2u = x2ur.base;
+    const double top1 = eta * x1u[p] - dt * ara_lx(g, nu, a1, l1.sigma, x1ur, iy, o) + phi * x2u[p];
+    const double top2 = eta * x2u[p] - dt * ara_lx(g, nu, a2, l2.sigma, x2ur, iy, o) -
                         (beta * beta / phi) * x1u[p];
-    const P9 w1 = load9(x1w, p, o), w2 = load9(x2w, p, o);
-    const double gu1 = (p == 0) ? 0.0 : h2 * x1u[p], gu2 = (p == 0) ? 0.0 : h2 * x2u[p];
-    const double gw1 = (p == 0) ? w1.c : h2 * lap9(g, w1);
-    const double gw2 = (p == 0) ? w2.c : h2 * lap9(g, w2);
+    const P9 w1 = load9(x1wr, g, iy, o), w2 = load9(x2wr, g, iy, o);
+    const double gu1 = pinned(g, p) ? 0.0 : h2 * x1u[p], gu2 = pinned(g, p) ? 0.0 : h2 * x2u[p];
+    const double gw1 = pinned(g, p) ? w1.c : h2 * lap9(g, w1);
+    const double gw2 = pinned(g, p) ? w2.c : h2 * lap9(g, w2);
     const double bot1 = -dt * (sig1 * gu1) - dt * (sig1 * gw1);
     const double bot2 = -dt * (sig2 * gu2) - dt * (sig2 * gw2);
     const double r[4] = {ACC[p], ACC[n + p], ACC[2 * n + p], ACC[3 * n + p]};
@@ -393,16 +421,20 @@ __global__ void k_dae_block_res(Grid g, double nu, double h2, double eta, double
 
 void Engine::dae_init() {
   if (!dae) return;
+  // the constraint solve runs on the global grid (slab mode: gathered rhs,
+  // solved redundantly on every rank -- see constraint_solve)
+  const int gny = gplanes;
+  const long long ng = (long long)grid.nx * gny;
   dalloc_raw((void **)&ACC, sizeof(double) * 4 * N);
   dalloc_raw((void **)&XU, sizeof(double) * 2 * N);
   dalloc_raw((void **)&CR, sizeof(double) * N);
-  dalloc_raw((void **)&PT, sizeof(double) * N);
-  dalloc_raw((void **)&fft_buf, sizeof(cufftDoubleComplex) * (size_t)grid.ny * (grid.nx / 2 + 1));
-  h2 = (prob.length / grid.nx) *
-       ((prob.length_y > 0.0 ? prob.length_y : prob.length) / grid.ny);
+  dalloc_raw((void **)&PT, sizeof(double) * ng);
+  if (slab()) dalloc_raw((void **)&CG, sizeof(double) * ng);
+  dalloc_raw((void **)&fft_buf, sizeof(cufftDoubleComplex) * (size_t)gny * (grid.nx / 2 + 1));
+  h2 = (prob.length / grid.nx) * ((prob.length_y > 0.0 ? prob.length_y : prob.length) / gny);
   cufftHandle p1, p2;
-  if (cufftPlan2d(&p1, grid.ny, grid.nx, CUFFT_D2Z) != CUFFT_SUCCESS ||
-      cufftPlan2d(&p2, grid.ny, grid.nx, CUFFT_Z2D) != CUFFT_SUCCESS)
+  if (cufftPlan2d(&p1, gny, grid.nx, CUFFT_D2Z) != CUFFT_SUCCESS ||
+      cufftPlan2d(&p2, gny, grid.nx, CUFFT_Z2D) != CUFFT_SUCCESS)
     throw CudaError("cufftPlan2d failed");
   fft_fwd = (int)p1;
   fft_inv = (int)p2;
@@ -411,31 +443,48 @@ void Engine::dae_init() {
 void Engine::dae_fini() {
   if (fft_fwd >= 0) cufftDestroy((cufftHandle)fft_fwd);
   if (fft_inv >= 0) cufftDestroy((cufftHandle)fft_inv);
-  void *bufs[] = {ACC, XU, CR, PT, fft_buf};
+  void *bufs[] = {ACC, XU, CR, PT, CG, fft_buf};
   for (void *b : bufs)
     if (b) cudaFree(b);
 }
 
 int Engine::dae_grid() const { return grid.ny < sms * 8 ? grid.ny : sms * 8; }
 
-// out = post * (sigma G_w)^{-1} c  -- _ConstraintSolver.solve, src/dae.py:122-126
+// out = post * (sigma G_w)^{-1} c  -- _ConstraintSolver.solve, src/dae.py:122-126.
+// Slab mode: the ranks' slabs of c are gathered into the global vector (an
+// all-reduce of the zero-padded slab: exact, transport-agnostic) and every
+// rank runs the same global FFT solve, keeping its own slab of the result.
+// A constraint solve is 2 per 2x2 block per Newton iteration, against
+// hundreds of GMRES iterations, so the redundant O(N_global) FFT is cheap and
+// avoids a distributed transpose; the pinned row stays exactly the global one.
 void Engine::constraint_solve(double sigma, const double *c, double *out, double post) {
   if (sigma == 0.0) throw SolveError(IRKG_ERR_INDEX, "constraint Jacobian is singular");
-  const int n = (int)N;
+  const int gny = gplanes;
+  const long long ng = (long long)grid.nx * gny;
+  const double *cg = c;
+  long long off = 0;
+  if (slab()) {
+    off = (long long)p0 * grid.nx;
+    check(cudaMemsetAsync(CG, 0, sizeof(double) * ng, stream), "gather");
+    check(cudaMemcpyAsync(CG + off, c, sizeof(double) * N, cudaMemcpyDeviceToDevice, stream),
+          "gather");
+    allreduce(CG, (int)ng);
+    cg = CG;
+  }
+  const int n = (int)ng;
   const double inv = 1.0 / (sigma * h2);
-  k_pois_sum<<<dae_grid(), DBS, 0, stream>>>(n, inv, c, part, counter, &scal_dev[4]);
-  k_pois_rhs<<<grid_for(N), 256, 0, stream>>>(n, inv, c, &scal_dev[4], PT);
+  k_pois_sum<<<dae_grid(), DBS, 0, stream>>>(n, inv, cg, part, counter, &scal_dev[4]);
+  k_pois_rhs<<<grid_for(ng), 256, 0, stream>>>(n, inv, cg, &scal_dev[4], PT);
   cufftSetStream((cufftHandle)fft_fwd, stream);
   cufftSetStream((cufftHandle)fft_inv, stream);
   if (cufftExecD2Z((cufftHandle)fft_fwd, PT, (cufftDoubleComplex *)fft_buf) != CUFFT_SUCCESS)
     throw CudaError("cufftExecD2Z failed");
-  k_pois_scale<<<grid_for((long long)grid.ny * (grid.nx / 2 + 1)), 256, 0, stream>>>(
-      grid.nx, grid.ny, grid.ih2[0], grid.ih2[1], (cufftDoubleComplex *)fft_buf);
+  k_pois_scale<<<grid_for((long long)gny * (grid.nx / 2 + 1)), 256, 0, stream>>>(
+      grid.nx, gny, grid.ih2[0], grid.ih2[1], (cufftDoubleComplex *)fft_buf);
   if (cufftExecZ2D((cufftHandle)fft_inv, (cufftDoubleComplex *)fft_buf, PT) != CUFFT_SUCCESS)
     throw CudaError("cufftExecZ2D failed");
-  k_pois_fix<<<grid_for(N), 256, 0, stream>>>(n, post, 1.0 / sigma, PT, c, out);
+  k_pois_fix<<<grid_for(N), 256, 0, stream>>>((int)N, off, post, 1.0 / sigma, PT, cg, out);
   count(4);
-
 }
 
 void Engine::ara_jacobi_chain(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
@@ -444,12 +493,14 @@ void Engine::ara_jacobi_chain(const Op &L, double alpha, double dt, int inner, c
   const int gb = dae_grid();
   double *tbuf = zc ? tmp_t : nullptr;
   auto dst = [&](int i) { return ((inner - i) % 2 == 0) ? x_out : tmp_x; };
-  k_ara_jac<<<gb, DBS, 0, stream>>>(grid, kp.nu, L, alpha, dt, vin, in_off, zc, cpl, tbuf, nullptr,
-                                    nullptr, dst(1), skip);
+  const Op Lr = opref(L);
+  k_ara_jac<<<gb, DBS, 0, stream>>>(grid, kp.nu, Lr, alpha, dt, vin, in_off, zc, cpl, tbuf, nullptr,
+                                    FRef{nullptr, nullptr, nullptr}, dst(1), skip);
   count(1);
   for (int i = 2; i <= inner; ++i) {
-    k_ara_jac<<<gb, DBS, 0, stream>>>(grid, kp.nu, L, alpha, dt, vin, in_off, nullptr, 0.0, nullptr,
-                                      tbuf, dst(i - 1), dst(i), skip);
+    if (slab()) exchange(R_JX, dst(i - 1), 1);
+    k_ara_jac<<<gb, DBS, 0, stream>>>(grid, kp.nu, Lr, alpha, dt, vin, in_off, nullptr, 0.0, nullptr,
+                                      tbuf, ref(dst(i - 1)), dst(i), skip);
     count(1);
   }
 }
@@ -457,19 +508,39 @@ void Engine::ara_jacobi_chain(const Op &L, double alpha, double dt, int inner, c
 void Engine::ara_block_op(const BlockSpec &B, const double *z, double *w, const double *b,
                           double *out_norm, const GCtrl *skip) {
   const int gb = dae_grid();
+  if (slab()) {
+    exchange(R_X0, z, 1);
+    if (B.size == 2) exchange(R_X1, z + N, 1);
+  }
+  const FRef z1 = ref(z), z2 = B.size == 2 ? ref(z + N) : FRef{nullptr, nullptr, nullptr};
+  const Op l1 = opref(B.l1), l2 = opref(B.l2), c12 = opref(B.c12), c21 = opref(B.c21);
   if (B.size == 1)
-    k_ara_block_op<1><<<gb, DBS, 0, stream>>>(grid, kp.nu, B.eta, B.beta, B.phi, B.dt, B.l1, B.l2,
-                                              B.c12, B.c21, z, w, b, part, counter, out_norm, skip);
+    k_ara_block_op<1><<<gb, DBS, 0, stream>>>(grid, kp.nu, B.eta, B.beta, B.phi, B.dt, l1, l2,
+                                              c12, c21, z1, z2, w, b, part, counter, out_norm,
+                                              skip);
   else
-    k_ara_block_op<2><<<gb, DBS, 0, stream>>>(grid, kp.nu, B.eta, B.beta, B.phi, B.dt, B.l1, B.l2,
-                                              B.c12, B.c21, z, w, b, part, counter, out_norm, skip);
+    k_ara_block_op<2><<<gb, DBS, 0, stream>>>(grid, kp.nu, B.eta, B.beta, B.phi, B.dt, l1, l2,
+                                              c12, c21, z1, z2, w, b, part, counter, out_norm,
+                                              skip);
   count(1);
+  if (b) allreduce(out_norm, 1);
 }
 
 double Engine::dae_residual(const double *UW, const double *K2, double *F2) {
-  k_dae_residual<<<dae_grid(), DBS, 0, stream>>>(grid, kp.nu, h2, s, UW, K2, F2, part, counter,
+  DaeStageRefs R{};
+  for (int i = 0; i < s; ++i) {
+    const double *u = UW + (size_t)i * 2 * N, *w = u + N;
+    if (slab()) {
+      exchange(R_STAGE + i, u, 1);
+      exchange(R_DW + i, w, 1);
+    }
+    R.u[i] = ref(u);
+    R.w[i] = ref(w);
+  }
+  k_dae_residual<<<dae_grid(), DBS, 0, stream>>>(grid, kp.nu, h2, s, R, K2, F2, part, counter,
                                                  &scal_dev[0]);
   count(1);
+  allreduce(&scal_dev[0], 1);
   double v = 0.0;
   check(cudaMemcpyAsync(&v, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost, stream));
   check(cudaStreamSynchronize(stream));
@@ -477,8 +548,11 @@ double Engine::dae_residual(const double *UW, const double *K2, double *F2) {
 }
 
 double Engine::dae_gnorm(const double *UW) {
-  k_dae_gnorm<<<dae_grid(), DBS, 0, stream>>>(grid, h2, UW, part, counter, &scal_dev[0]);
+  if (slab()) exchange(R_DG, UW + N, 1);
+  k_dae_gnorm<<<dae_grid(), DBS, 0, stream>>>(grid, h2, UW, ref(UW + N), part, counter,
+                                              &scal_dev[0]);
   count(1);
+  allreduce(&scal_dev[0], 1);
   double v = 0.0;
   check(cudaMemcpyAsync(&v, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost, stream));
   check(cudaStreamSynchronize(stream));
@@ -506,10 +580,19 @@ void Engine::dae_transformed_solve(double dt, const double *rhs, double *dk,
     for (int j = off + 2; j < s; ++j) {
       int q = T.njs++;
       T.j[q] = j;
+      bool any_od = false;
       for (int r = 0; r < 2; ++r) {
         T.coef[r][q] = tab.r[(off + r) * IRKG_MAX_STAGES + j];
-        T.od[r][q] = op_of(od_slot[off + r][j]);
+        T.od[r][q] = opref(op_of(od_slot[off + r][j]));
+        any_od |= T.od[r][q].present != 0;
       }
+      const double *yu = Y + (size_t)j * n2, *yw = yu + N;
+      if (slab() && any_od) {
+        exchange(R_Y + j, yu, 1);
+        exchange(R_DYW + j, yw, 1);
+      }
+      T.yu[q] = any_od ? ref(yu) : FRef{yu, nullptr, nullptr};
+      T.yw[q] = any_od ? ref(yw) : FRef{yw, nullptr, nullptr};
     }
     k_dae_backsub<<<dae_grid(), DBS, 0, stream>>>(grid, kp.nu, h2, dt, T, Gs, Y, ACC);
     count(1);
@@ -534,9 +617,10 @@ void Engine::dae_transformed_solve(double dt, const double *rhs, double *dk,
     check(cudaMemcpyAsync(Y1, XU, N * sizeof(double), cudaMemcpyDeviceToDevice, stream));
     check(cudaMemcpyAsync(Y2r, XU + N, N * sizeof(double), cudaMemcpyDeviceToDevice, stream));
     const double sig1 = op_sigma[diag_slot[off]], sig2 = op_sigma[diag_slot[off + 1]];
-    k_dae_crhs<<<grid_for(N), 256, 0, stream>>>((int)N, dt, sig1 * h2, ACC + N, XU, CR);
+    k_dae_crhs<<<grid_for(N), 256, 0, stream>>>((int)N, grid.pin, dt, sig1 * h2, ACC + N, XU, CR);
     constraint_solve(sig1, CR, Y1 + N, -1.0 / dt);
-    k_dae_crhs<<<grid_for(N), 256, 0, stream>>>((int)N, dt, sig2 * h2, ACC + n2 + N, XU + N, CR);
+    k_dae_crhs<<<grid_for(N), 256, 0, stream>>>((int)N, grid.pin, dt, sig2 * h2, ACC + n2 + N,
+                                                XU + N, CR);
     constraint_solve(sig2, CR, Y2r + N, -1.0 / dt);
     count(2);
     if (stats) {
@@ -567,10 +651,18 @@ void Engine::dae_transformed_solve(double dt, const double *rhs, double *dk,
       throw SolveError(IRKG_ERR_STAGE_SOLVE, msg);
     }
     // composite true-residual recheck (src/dae.py:307-314)
+    if (slab()) {
+      exchange(R_DB + 0, Y1, 1);
+      exchange(R_DB + 1, Y1 + N, 1);
+      exchange(R_DB + 2, Y2r, 1);
+      exchange(R_DB + 3, Y2r + N, 1);
+    }
     k_dae_block_res<<<dae_grid(), DBS, 0, stream>>>(grid, kp.nu, h2, B.eta, B.beta, B.phi, dt,
-                                                    B.l1, B.l2, sig1, sig2, ACC, Y1, Y2r, part,
-                                                    counter, &scal_dev[6]);
+                                                    opref(B.l1), opref(B.l2), sig1, sig2, ACC,
+                                                    ref(Y1), ref(Y1 + N), ref(Y2r), ref(Y2r + N),
+                                                    part, counter, &scal_dev[6]);
     count(1);
+    allreduce(&scal_dev[6], 2);
     double rb[2];
     check(cudaMemcpyAsync(rb, &scal_dev[6], 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
     check(cudaStreamSynchronize(stream));
@@ -624,6 +716,9 @@ void Engine::dae_newton(const double *uw, double *K2, double t, double dt, irkg_
       build_weights();
       k_dae_opfields<<<grid_for(N), 256, 0, stream>>>((int)N, weights, U, opA);
       count(1);
+      if (slab())  // operator fields feed the 9-point stencils
+        for (int o = 0; o < nops; ++o)
+          if (!op_zero[o]) exchange(R_OP + o, opA + (size_t)o * N, 1);
       stats->jacobian_assemblies += s;
       have_ops = true;
     }

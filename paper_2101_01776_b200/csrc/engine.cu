@@ -51,6 +51,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
     grid.nz = ndim == 3 ? nl : p.nz;
   }
   grid.slab = slab() ? 1 : 0;
+  grid.pin = p0 == 0 ? 1 : 0;
   grid.nxy = grid.nx * grid.ny;
   grid.n = grid.nx * grid.ny * grid.nz;
   double lapdiag = 0.0;
@@ -679,8 +680,8 @@ static void validate_problem(const irkg_problem *prob, int rank, int nranks) {
   if (nranks > 1) {
     const int nd = (prob->nz > 1) ? 3 : (prob->ny > 1 ? 2 : 1);
     if (nd == 1) throw SolveError(IRKG_ERR_CONFIG, "slab partition needs a 2-D or 3-D grid");
-    if (prob->kind == IRKG_KIND_ARAKAWA)
-      throw SolveError(IRKG_ERR_CONFIG, "the DAE path runs on one rank in this version");
+    if (prob->kind == IRKG_KIND_ARAKAWA && nd != 2)
+      throw SolveError(IRKG_ERR_CONFIG, "the vorticity DAE is 2-D");
     const int planes = nd == 3 ? prob->nz : prob->ny;
     if (planes / nranks < GH)
       throw SolveError(IRKG_ERR_CONFIG, "slabs must hold at least 6 planes per rank");

@@ -53,7 +53,13 @@ void nccl_unique_id(void *out128);
 // ghost-buffer roles (one ghost pair per role, re-pointed by exchange())
 enum GhostRole {
   R_VIN0 = 0, R_VIN1 = 1, R_Z0 = 2, R_Z1 = 3, R_X0 = 4, R_X1 = 5, R_JX = 6,
-  R_STAGE = 16, R_Y = 32, R_OP = 64
+  R_DG = 7,      // DAE: psi of the state (constraint norm)
+  R_DB = 8,      // DAE: 4 fields of the composite block residual (8..11)
+  R_STAGE = 16,  // stage values U_i (16..23)
+  R_DW = 24,     // DAE: stage values W_i (24..31)
+  R_Y = 32,      // back-substitution y_j (DAE: y_u,j) (32..39)
+  R_DYW = 40,    // DAE back-substitution y_w,j (40..47)
+  R_OP = 64      // operator fields
 };
 
 struct KrylovOut {
@@ -185,6 +191,7 @@ struct Engine {
   bool dae = false;
   double h2 = 0.0;
   double *ACC = nullptr, *XU = nullptr, *CR = nullptr, *PT = nullptr;
+  double *CG = nullptr;  // slab mode: the gathered global constraint rhs (PT is global then)
   void *fft_buf = nullptr;
   int fft_fwd = -1, fft_inv = -1;
   void dae_init();

@@ -33,6 +33,7 @@ struct Grid {
   double i2h[3];   // 1/(2h) per axis, 0 for an axis of extent 1
   double lapdiag;  // diagonal of Lap: -2 * sum ih2
   int slab;        // 1: slab-partitioned (ghost planes), 0: periodic wrap locally
+  int pin;         // 1: this rank holds global point 0 (the DAE constraint's pinned row)
 };
 
 // Depth of the ghost-plane buffers (>= Jacobi halo K-1 for K <= 6, and 1).

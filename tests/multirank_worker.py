@@ -41,9 +41,35 @@ def main():
     backend = "gloo" if args.transport == "callback" else "nccl"
     dist.init_process_group(backend)
     shape = tuple(int(x) for x in args.shape.split(","))
-    params = {"burgers": dict(nu=1e-2), "nldiff": {}, "rad": dict(nu=0.01, c=0.3, lam=-0.2)}
-    prob = pk.GridProblem(args.kind, shape, **params[args.kind])
-    u0 = pk.fourier_u0(shape, 1, 4, 0.5 if args.kind == "burgers" else 0.1, 0)
+    dae = args.kind == "arakawa"
+    if dae:
+        # vorticity/streamfunction DAE (configs[4] form): state [omega; psi],
+        # each slab-partitioned; the constraint solve gathers across ranks
+        prob = pk.VorticityProblem(shape, nu=1e-3)
+        w0, p0 = pk.vorticity_initial_state(prob, seed=3)
+        u0 = np.concatenate([w0, p0])
+    else:
+        params = {"burgers": dict(nu=1e-2), "nldiff": {}, "rad": dict(nu=0.01, c=0.3, lam=-0.2)}
+        prob = pk.GridProblem(args.kind, shape, **params[args.kind])
+        u0 = pk.fourier_u0(shape, 1, 4, 0.5 if args.kind == "burgers" else 0.1, 0)
+    n_glob = int(np.prod(shape))
+
+    def local_of(vec):
+        if not dae:
+            return scatter(vec, shape, rank, ws)
+        return np.concatenate([scatter(vec[:n_glob], shape, rank, ws),
+                               scatter(vec[n_glob:], shape, rank, ws)])
+
+    def global_of(parts):
+        if not dae:
+            return gather(parts, shape)
+        halves = [np.split(p, 2) for p in parts]
+        return np.concatenate([gather([h[0] for h in halves], shape),
+                               gather([h[1] for h in halves], shape)])
+
+    def advance(c, x, t):
+        return c.dae_step_device(x, t, args.dt) if dae else c.step_device(x, t, args.dt)
+
     tab = pk.make_tableau(args.family, args.stages)
     prep = pk.prepare_stages(tab)
     cfg = pk.SolverConfig(krylov_maxit=5000, precond=pk.PrecondSpec(inner=4))
@@ -51,10 +77,10 @@ def main():
     ctx = SlabContext(prob, rank, ws, transport=args.transport)
     ctx.set_prep(prep)
     ctx.set_config(cfg)
-    u = torch.from_numpy(np.ascontiguousarray(scatter(u0, shape, rank, ws))).cuda()
+    u = torch.from_numpy(np.ascontiguousarray(local_of(u0))).cuda()
     stats = []
     for j in range(args.nsteps):
-        st = ctx.step_device(u, j * args.dt, args.dt)
+        st = advance(ctx, u, j * args.dt)
         stats.append([st.newton_iterations, st.krylov_iterations,
                       {str(k): v for k, v in st.block_iterations.items()}])
     local = u.cpu().numpy()
@@ -63,7 +89,7 @@ def main():
     halos = ctx.counters()["halo_exchanges"]
     ctx.close()
     if rank == 0:
-        uglob = gather(parts, shape)
+        uglob = global_of(parts)
         from paper_2101_01776_b200.engine import Context
 
         single = Context(prob)
@@ -72,7 +98,7 @@ def main():
         us = torch.from_numpy(u0).cuda()
         sstats = []
         for j in range(args.nsteps):
-            st = single.step_device(us, j * args.dt, args.dt)
+            st = advance(single, us, j * args.dt)
             sstats.append([st.newton_iterations, st.krylov_iterations,
                            {str(k): v for k, v in st.block_iterations.items()}])
         ref = us.cpu().numpy()

@@ -192,3 +192,63 @@ def test_two_rank_gloo_decomposition_is_p_independent(kind, shape):
     assert conv and conv_ref
     assert abs(its - its_ref) <= 1, (its, its_ref)
     assert rel <= 1e-8, rel
+
+
+def _dae_worker(rank, nranks, port, shape, queue):
+    """The multi-rank DAE path (csrc/dae.cu) restated: the Arakawa 9-point
+    differential operator on slabs with one full ghost plane each side (the
+    corners come with the planes), and the constraint solve on the gathered
+    right-hand side -- each rank's slab zero-padded into the global vector and
+    all-reduced (exact), solved globally, own slab kept."""
+    import scipy.sparse.linalg as spla
+
+    from oracle.problems import DaeProblemDef
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=nranks)
+    try:
+        pd = DaeProblemDef(shape, 1e-3)
+        rng = np.random.default_rng(7)
+        u = rng.standard_normal(pd.dim)
+        w = rng.standard_normal(pd.dim)
+        lu, _, gu, gw = pd.blocks_csr(u, w, 0.0)
+        # the engine's slab axis is y (x fastest): shape (nx, ny) -> planes = ny
+        sshape = (shape[0], shape[1])
+        x = rng.standard_normal(pd.dim)
+        ok_lu = np.allclose(SlabOperator(lu, sshape, rank, nranks)(scatter(x, sshape, rank,
+                                                                          nranks).copy()),
+                            scatter(lu @ x, sshape, rank, nranks), atol=1e-10)
+        ok_gw = np.allclose(SlabOperator(gw, sshape, rank, nranks)(scatter(x, sshape, rank,
+                                                                          nranks).copy()),
+                            scatter(gw @ x, sshape, rank, nranks), atol=1e-12)
+        c = rng.standard_normal(pd.dim)
+        p0, nl = slab_range(shape[1], rank, nranks)
+        padded = np.zeros(pd.dim)
+        padded[p0 * shape[0]:(p0 + nl) * shape[0]] = scatter(c, sshape, rank, nranks)
+        cg = _allreduce(padded)
+        exact_gather = bool(np.array_equal(cg, c))
+        y_loc = scatter(spla.spsolve(gw.tocsc(), cg), sshape, rank, nranks)
+        parts = [None] * nranks
+        dist.all_gather_object(parts, y_loc)
+        if rank == 0:
+            y_ref = spla.spsolve(gw.tocsc(), c)
+            rel = float(np.linalg.norm(gather(parts, sshape) - y_ref) / np.linalg.norm(y_ref))
+            queue.put((bool(ok_lu), bool(ok_gw), exact_gather, rel))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_dae_slabs_and_gathered_constraint_solve():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dae_worker, args=(r, 2, port, (12, 14), q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    ok_lu, ok_gw, exact_gather, rel = res
+    assert ok_lu and ok_gw
+    assert exact_gather
+    assert rel <= 1e-13, rel

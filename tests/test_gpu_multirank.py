@@ -43,6 +43,11 @@ def _run(tmp_path, nproc, *args, env=None):
          "--dt", "2e-4"]),
     (3, ["--kind", "nldiff", "--shape", "16,14,24", "--family", "gauss", "--stages", "2",
          "--dt", "1e-3"]),
+    # the vorticity DAE: 9-point stencils on slabs + the gathered constraint solve
+    (2, ["--kind", "arakawa", "--shape", "40,40", "--family", "gauss", "--stages", "2",
+         "--dt", "2e-3"]),
+    (3, ["--kind", "arakawa", "--shape", "32,36", "--family", "gauss", "--stages", "4",
+         "--dt", "2e-3"]),
 ])
 def test_slab_partition_matches_single_rank(tmp_path, nproc, args):
     r = _run(tmp_path, nproc, *args)
