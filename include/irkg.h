@@ -173,6 +173,12 @@ int irkg_set_tableau(irkg_ctx *ctx, const irkg_tableau *tab);
 int irkg_set_solver(irkg_ctx *ctx, const irkg_solver *cfg);
 int irkg_set_timing(irkg_ctx *ctx, int on);
 int irkg_get_counters(irkg_ctx *ctx, irkg_counters *out);
+/* Diagnostics (no reference counterpart): average device time in us of one
+ * hot-path phase replayed `reps` times on the state the last block solve left
+ * (0 precond, 1/2 first/second Jacobi chain, 3 block operator, 6 CGS2 sweeps,
+ * 7 index pin alone, 8 whole Arnoldi step, 10 x += V y).  Destroys the Krylov
+ * state. */
+int irkg_probe_phase(irkg_ctx *ctx, int phase, int j, int reps, double *us);
 
 /* stage_residual (src/nonlinear.py:145-152): F = N(u + dt A0 K) - K.
  * u_dev (N), k_dev (s,N), f_dev (s,N) out; *norm = ||F||_F. */

@@ -171,8 +171,10 @@ struct TileArgs {
 // TR <= 256: one thread moves the L basis segments with 2-D TMA boxes of 2^b
 // slots (popcount(L) copies, one tensor map per box shape) and w with a 1-D
 // copy.
+// with_w = false: the basis part only (issued before pdl_wait(); the w
+// segment follows with issue_w once the predecessor has finished)
 __device__ __noinline__ void issue_boxed(double *dst, const char *maps, const double *win, int r0,
-                                         int TR, int L, uint64_t *bar) {
+                                         int TR, int L, uint64_t *bar, bool with_w) {
   const uint32_t bytes = TR * 8u;
   mbar_expect_tx(bar, bytes * (uint32_t)(L + 1));
   int l0 = 0;
@@ -183,7 +185,7 @@ __device__ __noinline__ void issue_boxed(double *dst, const char *maps, const do
       l0 += 1 << b;
     }
   }
-  tma_load_1d(dst + L * TR, win + r0, bytes, bar);
+  if (with_w) tma_load_1d(dst + L * TR, win + r0, bytes, bar);
 }
 
 // Taller tiles (small j): one 1-D copy per slot, lane 0 of warp w issuing
@@ -193,10 +195,10 @@ __device__ __noinline__ void issue_boxed(double *dst, const char *maps, const do
 // negative); the phase cannot flip before its arrival.
 __device__ __noinline__ void issue_slots(double *dst, const double *V, long long pitch,
                                          const double *win, int r0, int TR, int L, int warp,
-                                         uint64_t *bar) {
+                                         uint64_t *bar, bool with_w) {
   const uint32_t bytes = TR * 8u;
 #pragma unroll 1
-  for (int l = warp; l <= L; l += CGS_NW) {
+  for (int l = warp; l <= L - (with_w ? 0 : 1); l += CGS_NW) {
     const double *src = (l < L) ? V + (size_t)l * pitch + r0 : win + r0;
     tma_load_1d(dst + l * TR, src, bytes, bar);
   }
@@ -257,7 +259,7 @@ __device__ __forceinline__ void tile_compute(const TileArgs &A, double *buf, int
         } else {
           v = 0.0;
         }
-        wt[r] = v;
+        if (MODE == CGS_UPD_DOT) wt[r] = v;  // the second-pass dots read w1
       }
       if (PARTS > 1) __syncthreads();
     }
@@ -304,15 +306,24 @@ __device__ __forceinline__ bool tile_full(const TileArgs &A, int t) {
 }
 
 template <int TRC>
-__device__ __forceinline__ void tile_issue(const TileArgs &A, int t, int s) {
+__device__ __forceinline__ void tile_issue(const TileArgs &A, int t, int s, bool with_w = true) {
   const int tid = threadIdx.x;
   double *dst = A.ring + (size_t)s * (A.L + 1) * TRC;
   if (A.maps) {
-    if (tid == 0) issue_boxed(dst, A.maps, A.win, t * TRC, TRC, A.L, &A.bars[s]);
+    if (tid == 0) issue_boxed(dst, A.maps, A.win, t * TRC, TRC, A.L, &A.bars[s], with_w);
   } else {
     if (tid == 0) mbar_expect_tx(&A.bars[s], TRC * 8u * (uint32_t)(A.L + 1));
     if ((tid & 31) == 0)
-      issue_slots(dst, A.V, A.pitch, A.win, t * TRC, TRC, A.L, tid >> 5, &A.bars[s]);
+      issue_slots(dst, A.V, A.pitch, A.win, t * TRC, TRC, A.L, tid >> 5, &A.bars[s], with_w);
+  }
+}
+
+// the w segment of a tile whose basis part went out before pdl_wait()
+template <int TRC>
+__device__ __forceinline__ void tile_issue_w(const TileArgs &A, int t, int s) {
+  if (threadIdx.x == 0) {
+    double *dst = A.ring + (size_t)s * (A.L + 1) * TRC;
+    tma_load_1d(dst + A.L * TRC, A.win + t * TRC, TRC * 8u, &A.bars[s]);
   }
 }
 
@@ -328,12 +339,25 @@ __device__ __forceinline__ void tile_load_tail(const TileArgs &A, double *buf, i
 
 // One sweep's tile loop (grid-stride over row tiles, NST tiles in flight).
 template <int MODE, int TRC>
-__device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q], double &nrm) {
+__device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q], double &nrm,
+                                          const GWork &W, const double *cin) {
   const int G = A.G, ntiles = A.ntiles;
   const int t0 = blockIdx.x;
   const int NST = A.nst;
+  // PDL prologue: the basis slots were written >= 2 launches back, so their
+  // part of the first NST tiles goes out while the predecessor drains; w
+  // (and the coefficients) only after pdl_wait()
   for (int i = 0; i < NST; ++i)
-    if (t0 + i * G < ntiles && tile_full<TRC>(A, t0 + i * G)) tile_issue<TRC>(A, t0 + i * G, i);
+    if (t0 + i * G < ntiles && tile_full<TRC>(A, t0 + i * G))
+      tile_issue<TRC>(A, t0 + i * G, i, false);
+  pdl_wait();
+  fence_proxy_async_global();  // w was written through the generic proxy
+  for (int i = 0; i < NST; ++i)
+    if (t0 + i * G < ntiles && tile_full<TRC>(A, t0 + i * G)) tile_issue_w<TRC>(A, t0 + i * G, i);
+  if (MODE != CGS_DOT)
+    for (int l = threadIdx.x; l < A.L; l += CGS_BS) const_cast<double *>(A.cs)[l] = W.alpha[l] * cin[l];
+  __syncthreads();
+  pdl_trigger();
 
   int s = 0;
   uint32_t phase = 0;
@@ -348,7 +372,7 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
       tile_load_tail<TRC>(A, buf, r0, rows);
     }
     tile_compute<MODE, TRC>(A, buf, r0, rows, acc, nrm);
-    if (MODE != CGS_DOT) fence_proxy_async();  // wt was written via the generic proxy
+    if (MODE == CGS_UPD_DOT) fence_proxy_async();  // wt was written via the generic proxy
     __syncthreads();  // stage s consumed
     {
       const int tn = t + NST * G;
@@ -395,9 +419,6 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   const int nd = (MODE == CGS_DOT) ? L + 1 : L;  // dot entries (DOT: + ||w||^2)
   if (TR <= 256 && vmaps) vmaps += (size_t)(__ffs(TR) - 6) * VM_B * sizeof(CUtensorMap);
 
-  for (int l = tid; l < L; l += CGS_BS) {
-    if (MODE != CGS_DOT) cs[l] = W.alpha[l] * cin[l];
-  }
   if (tid == 0) {
     for (int i = 0; i < nst; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -411,12 +432,12 @@ __global__ void __launch_bounds__(CGS_BS, 2)
 #pragma unroll
   for (int q = 0; q < CGS_Q; ++q) acc[q] = 0.0;
   switch (TR) {
-    case 32: cgs_tiles<MODE, 32>(A, acc, nrm); break;
-    case 64: cgs_tiles<MODE, 64>(A, acc, nrm); break;
-    case 128: cgs_tiles<MODE, 128>(A, acc, nrm); break;
-    case 256: cgs_tiles<MODE, 256>(A, acc, nrm); break;
-    case 512: cgs_tiles<MODE, 512>(A, acc, nrm); break;
-    default: cgs_tiles<MODE, 1024>(A, acc, nrm); break;
+    case 32: cgs_tiles<MODE, 32>(A, acc, nrm, W, cin); break;
+    case 64: cgs_tiles<MODE, 64>(A, acc, nrm, W, cin); break;
+    case 128: cgs_tiles<MODE, 128>(A, acc, nrm, W, cin); break;
+    case 256: cgs_tiles<MODE, 256>(A, acc, nrm, W, cin); break;
+    case 512: cgs_tiles<MODE, 512>(A, acc, nrm, W, cin); break;
+    default: cgs_tiles<MODE, 1024>(A, acc, nrm, W, cin); break;
   }
 
   // per-CTA partials -> part[l * G + cta]
@@ -530,238 +551,6 @@ void Engine::build_vmaps() {
         "tensor maps");
 }
 
-// ---------------------------------------------------------------------------
-// Fused CGS2: the three sweeps in ONE persistent launch of G co-resident CTAs
-// (cooperative launch), separated by grid barriers.  Every sweep assigns the
-// same row tiles to the same CTA, so the tile stream runs straight through
-// the sweep boundaries: sweep 2 reads the unchanged V and w (prefetched
-// across the first barrier), sweep 3 reads only the w1 rows this CTA wrote
-// in sweep 2 (issued as soon as that sweep ends, before the second barrier).
-// Saves two launches, ramps and cold starts per Arnoldi step and hides the
-// barrier behind the tile stream.  The last CTA to arrive folds the partials
-// (fixed order) and publishes c1 / c2 before releasing the barrier.
-
-// per-CTA partials of a dot sweep -> part[l * G + cta]
-__device__ __forceinline__ void write_partials(const double (&acc)[CGS_Q], int nd, double *part,
-                                               int G) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nq = (nd + CGS_NW - 1) / CGS_NW;
-#pragma unroll
-  for (int q = 0; q < CGS_Q; ++q) {
-    if (q >= nq) break;
-    const int l = warp + CGS_NW * q;
-    if (l < nd) {
-      const double v = wsum(acc[q]);
-      if (lane == 0) part[(size_t)l * G + blockIdx.x] = v;
-    }
-  }
-}
-
-// fold part[l * G + c] over c for l < nfold (all threads of one CTA) and
-// publish through store(l, v)
-template <class F>
-__device__ __forceinline__ void fold_partials(const double *part, int G, int nfold, F store) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int l = warp; l < nfold; l += CGS_NW) {
-    const double *pl = part + (size_t)l * G;
-    double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;
-    int c = lane;
-    for (; c + 96 < G; c += 128) {
-      f0 += __ldcg(pl + c);
-      f1 += __ldcg(pl + c + 32);
-      f2 += __ldcg(pl + c + 64);
-      f3 += __ldcg(pl + c + 96);
-    }
-    for (; c < G; c += 32) f0 += __ldcg(pl + c);
-    const double v = wsum((f0 + f1) + (f2 + f3));
-    if (lane == 0) store(l, v);
-  }
-}
-
-template <int TRC>
-__device__ __forceinline__ void cgs3_body(TileArgs &A, GWork W, double *part, unsigned *gbar,
-                                          unsigned *counter, double *cs, double *wout,
-                                          double *vout, bool &is_last, int use_cond,
-                                          cudaGraphConditionalHandle cond) {
-  const int tid = threadIdx.x;
-  const int L = A.L, G = A.G, ntiles = A.ntiles, NST = A.nst;
-  const int cta = blockIdx.x;
-  const int nk = cta < ntiles ? (ntiles - cta + G - 1) / G : 0;  // tiles per sweep
-  GCtrl *ctrl = W.ctrl;
-  // ring state (identical in every thread): next virtual tile to issue, and
-  // per slot the expected mbarrier parity / whether the slot's tile was armed
-  int issued = 0, consumed = 0;
-  uint32_t parity = 0, armed = 0;
-  auto pump = [&](int limit) {
-    while (issued < limit && issued < consumed + NST) {
-      const int t = cta + (issued % nk) * G;
-      const int slot = issued % NST;
-      if (tile_full<TRC>(A, t)) {
-        tile_issue<TRC>(A, t, slot);
-        armed |= 1u << slot;
-      } else {
-        armed &= ~(1u << slot);
-      }
-      ++issued;
-    }
-  };
-  // grid barrier: arrive (partials written), the last CTA folds + publishes
-  // and releases; everyone waits for the release
-  auto barrier_fold = [&](int nfold, auto store) {
-    __threadfence();
-    __syncthreads();
-    unsigned gen0 = 0;
-    if (tid == 0) {
-      gen0 = ld_acquire(gbar + 1);
-      is_last = atomicAdd(gbar, 1u) == (unsigned)(G - 1);
-    }
-    __syncthreads();
-    if (is_last) {
-      __threadfence();
-      fold_partials(part, G, nfold, store);
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) {
-        gbar[0] = 0u;
-        __threadfence();
-        atomicAdd(gbar + 1, 1u);
-      }
-    } else if (tid == 0) {
-      // bounded: a broken barrier traps (launch error) instead of hanging
-      unsigned long long spins = 0;
-      while (ld_acquire(gbar + 1) == gen0) {
-        __nanosleep(64);  // back off: 296 pollers on one line slow the folding CTA
-        if (++spins > (1ull << 26)) __trap();
-      }
-    }
-    __syncthreads();
-  };
-
-  double acc[CGS_Q];
-#pragma unroll
-  for (int q = 0; q < CGS_Q; ++q) acc[q] = 0.0;
-  double nrm = 0.0;
-  if (nk > 0) pump(2 * nk);  // sweeps 1 and 2 read unchanged data: prefetch freely
-
-  for (int sw = 0; sw < 3; ++sw) {
-    if (sw > 0) {
-      const double *cin = sw == 1 ? W.c1 : W.c2;
-      for (int l = tid; l < L; l += CGS_BS) cs[l] = W.alpha[l] * __ldcg(cin + l);
-      __syncthreads();
-    }
-    A.out = sw == 2 ? vout : wout;
-    for (int k = 0; k < nk; ++k) {
-      const int slot = consumed % NST;
-      const int t = cta + k * G;
-      const int r0 = t * TRC;
-      const int rows = min(TRC, A.n - r0);
-      double *buf = A.ring + (size_t)slot * (L + 1) * TRC;
-      if (armed & (1u << slot)) {
-        while (!mbar_try_wait(&A.bars[slot], (parity >> slot) & 1u)) {
-        }
-        parity ^= 1u << slot;
-      } else {
-        tile_load_tail<TRC>(A, buf, r0, rows);
-      }
-      if (sw == 0)
-        tile_compute<CGS_DOT, TRC>(A, buf, r0, rows, acc, nrm);
-      else if (sw == 1)
-        tile_compute<CGS_UPD_DOT, TRC>(A, buf, r0, rows, acc, nrm);
-      else
-        tile_compute<CGS_UPD_NORM, TRC>(A, buf, r0, rows, acc, nrm);
-      if (sw > 0) fence_proxy_async();  // wt was written via the generic proxy
-      __syncthreads();                  // slot consumed
-      ++consumed;
-      if (nk > 0) pump(sw < 2 ? 2 * nk : 3 * nk);
-    }
-    if (sw == 0) {
-      write_partials(acc, L + 1, part, G);
-#pragma unroll
-      for (int q = 0; q < CGS_Q; ++q) acc[q] = 0.0;
-      barrier_fold(L + 1, [&](int l, double v) {
-        if (l == L)
-          ctrl->wn2 = v;
-        else
-          W.c1[l] = W.alpha[l] * v;
-      });
-    } else if (sw == 1) {
-      write_partials(acc, L, part, G);
-      // w1 (global, generic proxy) -> the sweep-3 tiles read it through TMA
-      fence_proxy_async_global();
-      __syncthreads();
-      if (nk > 0) pump(3 * nk);
-      barrier_fold(L, [&](int l, double v) { W.c2[l] = W.alpha[l] * v; });
-    }
-  }
-  // sweep 3: ||s_{j+1}||^2 through the last-CTA ticket, then the column finish
-  {
-    const int lane = tid & 31, warp = tid >> 5;
-    double v = wsum(nrm);
-    if (lane == 0) A.red[warp] = v;
-    __syncthreads();
-    if (tid == 0) {
-      double tot = 0.0;
-      for (int w = 0; w < CGS_NW; ++w) tot += A.red[w];
-      part[cta] = tot;
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) is_last = (atomicAdd(counter, 1u) == (unsigned)(G - 1));
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-    fold_partials(part, G, 1, [&](int, double v2) { ctrl->hn2 = v2; });
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      arnoldi_finish_dev(W);
-      if (use_cond > 0) cudaGraphSetConditional(cond, ctrl->cycle_done ? 0u : 1u);
-      *counter = 0u;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(CGS_BS, 2)
-    k_cgs3(int n, double *__restrict__ V, long long pitch, GWork W, double *w, double *part,
-           int G, unsigned *gbar, unsigned *counter, int ring_doubles, int use_cond,
-           cudaGraphConditionalHandle cond, const char *__restrict__ vmaps, int trmax) {
-  extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) uint64_t bars[CGS_MAXST];
-  __shared__ double cs[MAXR + 1];
-  __shared__ double red[CGS_BS];
-  __shared__ bool is_last;
-
-  GCtrl *ctrl = W.ctrl;
-  if (ctrl->cycle_done) {
-    // inside the graph WHILE body: make sure the loop terminates
-    if (use_cond > 0 && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
-    return;
-  }
-  const int L = ctrl->j + 1;
-  const int tid = threadIdx.x;
-  int TR = trmax;
-  while (TR > 32 && 2 * (L + 1) * TR > ring_doubles) TR >>= 1;
-  int nst = ring_doubles / ((L + 1) * TR);
-  nst = nst > CGS_MAXST ? CGS_MAXST : nst;
-  const int ntiles = (n + TR - 1) / TR;
-  if (TR <= 256 && vmaps) vmaps += (size_t)(__ffs(TR) - 6) * VM_B * sizeof(CUtensorMap);
-  if (tid == 0) {
-    for (int i = 0; i < nst; ++i) mbar_init(&bars[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  TileArgs A{n, L, G, ntiles, V, pitch, w, w, sm, nst, bars, cs, red, TR <= 256 ? vmaps : nullptr};
-  double *vout = V + (size_t)L * pitch;
-  switch (TR) {
-    case 32: cgs3_body<32>(A, W, part, gbar, counter, cs, w, vout, is_last, use_cond, cond); break;
-    case 64: cgs3_body<64>(A, W, part, gbar, counter, cs, w, vout, is_last, use_cond, cond); break;
-    case 128: cgs3_body<128>(A, W, part, gbar, counter, cs, w, vout, is_last, use_cond, cond); break;
-    case 256: cgs3_body<256>(A, W, part, gbar, counter, cs, w, vout, is_last, use_cond, cond); break;
-    case 512: cgs3_body<512>(A, W, part, gbar, counter, cs, w, vout, is_last, use_cond, cond); break;
-    default: cgs3_body<1024>(A, W, part, gbar, counter, cs, w, vout, is_last, use_cond, cond); break;
-  }
-}
-
 static const char *cgs_maps(const void *vmaps) {
   static int nobox = -1;
   if (nobox < 0) nobox = getenv("IRKG_CGS_NOBOX") ? 1 : 0;
@@ -784,7 +573,7 @@ int Engine::cgs_stage_doubles() const {
 
 // One Arnoldi orthogonalisation: 3 fused sweeps; the last also finishes the
 // Hessenberg column (Givens, estimate, exit test) in its final CTA.
-void Engine::cgs(long long n) {
+void Engine::cgs(long long n, int nsweeps) {
   const int stage = cgs_stage_doubles();
   const size_t smem = (size_t)stage * sizeof(double);
   if (cgs_smem_set < smem) {
@@ -797,42 +586,26 @@ void Engine::cgs(long long n) {
     cgs_smem_set = smem;
   }
   const int uc = cond_active ? 1 : 0;
-  if (cgs_fused) {
-    if (!gbar) {
-      dalloc_raw((void **)&gbar, 2 * sizeof(unsigned));
-      check(cudaMemset(gbar, 0, 2 * sizeof(unsigned)), "grid barrier");
-    }
-    if (cgs3_smem_set < smem) {
-      check(cudaFuncSetAttribute(k_cgs3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-            "smem attr");
-      cgs3_smem_set = smem;
-    }
-    // cooperative: the grid barriers need all G CTAs resident (2 per SM)
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(G);
-    lc.blockDim = dim3(CGS_BS);
-    lc.dynamicSmemBytes = smem;
-    lc.stream = stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    check(cudaLaunchKernelEx(&lc, k_cgs3, (int)n, V, vpitch, W, wbuf, part, G, gbar, counter,
-                             stage, uc, cond_handle, cgs_maps(vmaps), cgs_trmax()),
-          "fused CGS launch");
+  const char *maps = cgs_maps(vmaps);
+  const int trm = cgs_trmax();
+  const double *cnull = nullptr;
+  double *dnull = nullptr;
+  launch_pdl(k_cgs<CGS_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W, cnull,
+             (const double *)wbuf, dnull, part, G, counter, stage, 0, cond_handle, maps, trm);
+  if (nsweeps < 2) {  // (phase probe)
     count(1);
     return;
   }
-  k_cgs<CGS_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, nullptr, wbuf, nullptr, part,
-                                              G, counter, stage, 0, cond_handle,
-      cgs_maps(vmaps), cgs_trmax());
-  k_cgs<CGS_UPD_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c1, wbuf, wbuf, part, G,
-                                                  counter, stage, 0, cond_handle,
-      cgs_maps(vmaps), cgs_trmax());
-  k_cgs<CGS_UPD_NORM><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c2, wbuf, nullptr,
-                                                   part, G, counter, stage, uc, cond_handle,
-      cgs_maps(vmaps), cgs_trmax());
+  launch_pdl(k_cgs<CGS_UPD_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
+             (const double *)W.c1, (const double *)wbuf, wbuf, part, G, counter, stage, 0,
+             cond_handle, maps, trm);
+  if (nsweeps < 3) {
+    count(2);
+    return;
+  }
+  launch_pdl(k_cgs<CGS_UPD_NORM>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
+             (const double *)W.c2, (const double *)wbuf, dnull, part, G, counter, stage, uc,
+             cond_handle, maps, trm);
   count(3);
 }
 

@@ -107,9 +107,11 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   if (const char *e = getenv("IRKG_FUSED_JACOBI")) fused_jacobi = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_JSPAN")) jspan_override = atoi(e);
   if (const char *e = getenv("IRKG_PAIR_JACOBI")) pair_jacobi = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_JACOBI_SPLIT")) jacobi_split = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_PDL")) use_pdl = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_CARVEOUT")) use_carveout = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_JWPS")) jwarps_per_sm = atoi(e) > 0 ? atoi(e) : 12;
   if (const char *e = getenv("IRKG_STRIP_OP")) strip_op = (atoi(e) != 0);
-  if (const char *e = getenv("IRKG_CGS_FUSED")) cgs_fused = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_BOP_WPS")) bop_wps = atoi(e) > 0 ? atoi(e) : 12;
   for (int i = 0; i < MAXS; ++i)
     for (int j = 0; j < MAXS; ++j) od_slot[i][j] = -1;
@@ -119,7 +121,7 @@ Engine::~Engine() {
   cudaStreamSynchronize(stream);
   void *bufs[] = {part, counter, scal_dev, ctrl_dev, W.H, W.cs, W.sn, W.g, W.alpha, W.y,
                   W.c1, W.c2, W.res, V, wbuf, zbuf, ubuf, tmp_x, tmp_t, U, F, Gs, Y, DK,
-                  Kst, RHS, ufield, opA, vmaps, gbar};
+                  Kst, RHS, ufield, opA, vmaps};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (ctrl_host) cudaFreeHost(ctrl_host);
@@ -285,6 +287,8 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
   if (!(rtol > 0.0 && rtol < 1.0)) throw SolveError(IRKG_ERR_VALUE, "rtol must lie in (0, 1)");
   ensure_basis(restart);
   ensure_res(maxit);
+  last_block = B;
+  have_last_block = true;
   const long long n = (long long)B.size * N;
   const int spa = B.size;
   KrylovOut out;
@@ -595,6 +599,64 @@ void Engine::transformed_solve(double dt, const double *rhs, double *dk, irkg_st
   stage_mix(qr.data(), Y, dk, false);
 }
 
+// ------------------------------------------------------------ phase probe
+// Diagnostic: device time of one hot-path phase, replayed `reps` times
+// back to back on the engine stream against the state the last gmres() call
+// left (its block system, basis and fields).  Arnoldi index j is pinned by a
+// one-thread kernel before each replay (its own time is probed as phase 7 and
+// subtracted by the caller).  Destroys the Krylov state; diagnostics only.
+__global__ void k_probe_setj(GCtrl *c, int j, int m) {
+  c->j = j;
+  c->m = m;
+  c->k = j + 1;
+  c->cycle_done = 0;
+  c->converged = 0;
+}
+
+double Engine::probe_phase(int phase, int j, int reps) {
+  if (!have_last_block) throw SolveError(IRKG_ERR_CONFIG, "probe: run a block solve first");
+  const BlockSpec &B = last_block;
+  const long long n = (long long)B.size * N;
+  if (j < 0 || j + 1 >= vcap) throw SolveError(IRKG_ERR_VALUE, "probe: j out of range");
+  VecIn vslot{V, vpitch, ctrl_dev, W.alpha};
+  max_carveout((const void *)k_probe_setj);
+  auto one = [&]() {
+    k_probe_setj<<<1, 1, 0, stream>>>(ctrl_dev, j, vcap);
+    switch (phase) {
+      case 0: precond(B, &vslot, zbuf, ctrl_dev); break;
+      case 1: jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vslot, 0, nullptr, 0.0, zbuf, ctrl_dev); break;
+      case 2:
+        jacobi_chain(B.size == 2 ? B.l2 : B.l1, B.size == 2 ? B.gamma : B.eta, B.dt, B.inner,
+                     &vslot, B.size == 2 ? (int)N : 0, B.size == 2 ? zbuf : nullptr,
+                     B.size == 2 ? B.beta * B.beta / B.phi : 0.0, zbuf + (B.size == 2 ? N : 0),
+                     ctrl_dev);
+        break;
+      case 3: block_op(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev); break;
+      case 4: case 5: case 6: cgs(n, phase - 3); break;  // the first 1 / 2 / 3 sweeps
+      case 7: break;
+      case 8: arnoldi_iteration(B, n); break;
+      case 9: {
+        std::vector<double> eye(s * s, 0.0);
+        for (int i = 0; i < s; ++i) eye[i * s + i] = 1.0;
+        stage_mix(eye.data(), F, Gs, false);
+        break;
+      }
+      case 10: vcombine(n, W.c1, ubuf); break;
+      case 11: backsolve(); break;
+      default: throw SolveError(IRKG_ERR_VALUE, "probe: unknown phase");
+    }
+  };
+  for (int i = 0; i < 2; ++i) one();  // warm
+  check(cudaStreamSynchronize(stream), "probe sync");
+  check(cudaEventRecord(ev0, stream));
+  for (int i = 0; i < reps; ++i) one();
+  check(cudaEventRecord(ev1, stream));
+  check(cudaEventSynchronize(ev1), "probe sync");
+  float ms = 0.f;
+  check(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
+  return 1e3 * (double)ms / reps;
+}
+
 // -------------------------------------------------------------- Newton
 // src/nonlinear.py:186-236.  K (s,N) in/out.
 void Engine::newton(const double *u, double *K, double t, double dt, irkg_step_stats *stats) {
@@ -753,6 +815,9 @@ int irkg_set_tableau(irkg_ctx *ctx, const irkg_tableau *tab) { IRKG_GUARD(ctx->e
 int irkg_set_solver(irkg_ctx *ctx, const irkg_solver *cfg) { IRKG_GUARD(ctx->eng->set_solver(*cfg)); }
 int irkg_set_timing(irkg_ctx *ctx, int on) { IRKG_GUARD(ctx->eng->timing = (on != 0)); }
 int irkg_get_counters(irkg_ctx *ctx, irkg_counters *out) { IRKG_GUARD(*out = ctx->eng->counters); }
+int irkg_probe_phase(irkg_ctx *ctx, int phase, int j, int reps, double *us) {
+  IRKG_GUARD(*us = ctx->eng->probe_phase(phase, j, reps));
+}
 
 int irkg_stage_residual(irkg_ctx *ctx, const double *u_dev, const double *k_dev, double t, double dt,
                         double *f_dev, double *norm) {

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <set>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -156,10 +158,6 @@ struct Engine {
   void ensure_res(int maxit);
   int rescap = 0;
   size_t cgs_smem_set = 0;
-  size_t cgs3_smem_set = 0;
-  unsigned *gbar = nullptr;   // fused-CGS grid barrier {count, generation}
-  bool cgs_fused = false;     // one cooperative launch for the 3 CGS sweeps (IRKG_CGS_FUSED=1; measured
-                              // slower than 3 launches on config 1: 755M vs 796M DOF/s)
   // CUDA-graph execution of the Arnoldi loop: one graph per block system,
   // a WHILE conditional node whose condition the last CGS kernel clears.
   struct CycleGraph {
@@ -177,7 +175,7 @@ struct Engine {
   void arnoldi_iteration(const BlockSpec &B, long long n);
   void drop_graphs();
   int cgs_stage_doubles() const;  // CGS shared-memory ring per CTA (doubles)
-  void cgs(long long n);  // cgs.cu
+  void cgs(long long n, int nsweeps = 3);  // cgs.cu
   // stencil.cu (register-sliding 2-D / 3-D kernels)
   dim3 slide_grid(int &span) const;
   void jac_sweep_s(const Op &L, double alpha, double dt, const VecIn &vin, int in_off,
@@ -218,7 +216,8 @@ struct Engine {
   // jacobi.cu (temporally blocked inner solves, 2-D)
   bool fused_jacobi = true;
   int jspan_override = 0;
-  bool pair_jacobi = true;   // column-pair Jacobi kernel (IRKG_PAIR_JACOBI=0: one column per lane)
+  bool pair_jacobi = true;
+  bool jacobi_split = true;  // split-operator pair kernel (IRKG_JACOBI_SPLIT=0: textbook form)   // column-pair Jacobi kernel (IRKG_PAIR_JACOBI=0: one column per lane)
   int jwarps_per_sm = 12;    // pair kernel: target resident warps per SM (IRKG_JWPS)
   bool strip_op = true;      // 2-D block operator on column-pair strips (IRKG_STRIP_OP=0: slide)
   int bop_wps = 12;          // strip block operator: target warps per SM (IRKG_BOP_WPS)
@@ -226,6 +225,35 @@ struct Engine {
                           int in_off, const double *zc, double cpl, double *x_out,
                           const GCtrl *skip);
 
+  // PDL launch of an Arnoldi-body kernel (IRKG_PDL=0: ordinary launch)
+  bool use_pdl = true;
+  template <typename... KArgs, typename... Args>
+  void launch_pdl(void (*kern)(KArgs...), dim3 grid_, dim3 block_, size_t smem, Args &&...args) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid_;
+    lc.blockDim = block_;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = use_pdl ? 1 : 0;
+    max_carveout((const void *)kern);
+    check(cudaLaunchKernelEx(&lc, kern, std::forward<Args>(args)...), "PDL launch");
+  }
+  // All Arnoldi-body kernels ask for the maximum shared-memory carveout, so
+  // consecutive kernels never force an L1/shared reconfiguration of the SMs
+  // (IRKG_CARVEOUT=0: driver default).
+  bool use_carveout = true;
+  std::set<const void *> carved;
+  void max_carveout(const void *fn) {
+    if (!use_carveout || carved.count(fn)) return;
+    check(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               (int)cudaSharedmemCarveoutMaxShared),
+          "carveout");
+    carved.insert(fn);
+  }
   // launch helpers (kernels.cu)
   int grid_for(long long n) const;
   int row_grid() const {  // CTAs of row-structured stencil kernels
@@ -256,6 +284,9 @@ struct Engine {
   void cycle_end();
 
   // drivers (engine.cu)
+  BlockSpec last_block{};  // block system of the last gmres() call (phase probe)
+  bool have_last_block = false;
+  double probe_phase(int phase, int j, int reps);
   void read_ctrl();
   KrylovOut gmres(const BlockSpec &B, const double *rhs, double *x, double rtol, int maxit,
                   int restart);

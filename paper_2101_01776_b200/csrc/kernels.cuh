@@ -17,6 +17,17 @@
 
 namespace irkg {
 
+// Programmatic dependent launch (PDL).  Kernels of the Arnoldi body are
+// launched with programmatic stream serialisation: a kernel may start while
+// its predecessor drains.  Convention: every PDL kernel calls pdl_wait()
+// before touching anything its predecessor writes, and pdl_trigger() only
+// after its own pdl_wait(), so the code before pdl_wait() may read anything
+// written two or more launches back.  (No-ops for ordinary launches.)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 constexpr int MAXS = 8;       // max stages
 constexpr int MAXR = 256;     // max restart length
 constexpr int MAXOPS = 48;    // max operator fields per linearisation

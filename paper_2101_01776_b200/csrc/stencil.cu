@@ -337,6 +337,8 @@ __global__ void __launch_bounds__(BPW * 32)
                      Op l1, Op l2, Op c12, Op c21, FRef z1r, FRef z2r, double *__restrict__ w,
                      const double *__restrict__ b, int span, int strips, int nwarps,
                      double *part, unsigned *counter, double *out_norm, const GCtrl *skip) {
+  pdl_wait();  // z from the preconditioner
+  pdl_trigger();
   if (skip && skip->cycle_done) return;
   constexpr int NF = bop_nf<SIZE>();
   const int lane = threadIdx.x & 31;
@@ -651,15 +653,16 @@ void Engine::block_op_s(const BlockSpec &B, const double *z, double *w, const do
       opt_in((const void *)k_block_op_strip<K_, 1>, 1, BPW * BRING * bop_nf<1>() * 64 * 8);
       opt_in((const void *)k_block_op_strip<K_, 2>, 2, BPW * BRING * bop_nf<2>() * 64 * 8);
       if (B.size == 1)
-        k_block_op_strip<K_, 1><<<blocks, BPW * 32, BPW * BRING * bop_nf<1>() * 64 * 8, stream>>>(
-            grid, kp, B.eta, B.beta, B.phi, B.dt, opref(B.l1), opref(B.l2), opref(B.c12),
-            opref(B.c21), z1, FRef{nullptr, nullptr, nullptr}, w, b, span, strips, nwarps, part,
-            counter, out_norm, skip);
+        launch_pdl(k_block_op_strip<K_, 1>, dim3(blocks), dim3(BPW * 32),
+                   (size_t)BPW * BRING * bop_nf<1>() * 64 * 8, grid, kp, B.eta, B.beta, B.phi,
+                   B.dt, opref(B.l1), opref(B.l2), opref(B.c12), opref(B.c21), z1,
+                   FRef{nullptr, nullptr, nullptr}, w, b, span, strips, nwarps, part, counter,
+                   out_norm, skip);
       else
-        k_block_op_strip<K_, 2><<<blocks, BPW * 32, BPW * BRING * bop_nf<2>() * 64 * 8, stream>>>(
-            grid, kp, B.eta, B.beta, B.phi, B.dt, opref(B.l1), opref(B.l2), opref(B.c12),
-            opref(B.c21), z1, ref(z + N), w, b, span, strips, nwarps, part, counter, out_norm,
-            skip);
+        launch_pdl(k_block_op_strip<K_, 2>, dim3(blocks), dim3(BPW * 32),
+                   (size_t)BPW * BRING * bop_nf<2>() * 64 * 8, grid, kp, B.eta, B.beta, B.phi,
+                   B.dt, opref(B.l1), opref(B.l2), opref(B.c12), opref(B.c21), z1, ref(z + N), w,
+                   b, span, strips, nwarps, part, counter, out_norm, skip);
     };
     switch (prob.kind) {
       case KIND_NLDIFF: launch(std::integral_constant<int, KIND_NLDIFF>{}); break;
