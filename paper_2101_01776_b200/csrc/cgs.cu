@@ -483,7 +483,9 @@ __global__ void __launch_bounds__(CGS_BS, 2)
     double v = wsum((f0 + f1) + (f2 + f3));
     if (lane == 0) {
       if (MODE == CGS_DOT) {
-        if (l == L)
+        if (l == L && use_cond < 0)
+          W.c1[L] = v;  // multi-rank: all-reduced together with c1, then moved
+        else if (l == L)
           ctrl->wn2 = v;
         else
           W.c1[l] = W.alpha[l] * v;
@@ -610,9 +612,20 @@ void Engine::cgs(long long n, int nsweeps) {
 }
 
 // Multi-rank CGS2: the same sweeps over the local slab with the partial
-// dot products summed across ranks between them; the Hessenberg column is
-// finished (k_arnoldi_finish) from the global ||w||.  j is known on the host.
-void Engine::cgs_slab(long long n, int j) {
+// dot products summed across ranks between them (fixed-length all-reduces,
+// so the sequence is graph-capturable with the Arnoldi index on the device:
+// c1 travels together with ||w||^2 in c1[L]); the Hessenberg column is then
+// finished from the global sums by k_arnoldi_finish_slab.
+__global__ void k_arnoldi_finish_slab(GWork W, int use_cond, cudaGraphConditionalHandle cond) {
+  GCtrl *c = W.ctrl;
+  if (!c->cycle_done) {
+    c->wn2 = W.c1[c->j + 1];
+    arnoldi_finish_dev(W);
+  }
+  if (use_cond > 0) cudaGraphSetConditional(cond, c->cycle_done ? 0u : 1u);
+}
+
+void Engine::cgs_slab(long long n) {
   const int stage = cgs_stage_doubles();
   const size_t smem = (size_t)stage * sizeof(double);
   if (cgs_smem_set < smem) {
@@ -624,22 +637,24 @@ void Engine::cgs_slab(long long n, int j) {
                                (int)smem), "smem attr");
     cgs_smem_set = smem;
   }
-  const int L = j + 1;
-  k_cgs<CGS_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, nullptr, wbuf, nullptr, part,
-                                              G, counter, stage, 0, cond_handle,
-      cgs_maps(vmaps), cgs_trmax());
-  allreduce(W.c1, L);
-  allreduce(&ctrl_dev->wn2, 1);
-  k_cgs<CGS_UPD_DOT><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c1, wbuf, wbuf, part, G,
-                                                  counter, stage, 0, cond_handle,
-      cgs_maps(vmaps), cgs_trmax());
-  allreduce(W.c2, L);
-  k_cgs<CGS_UPD_NORM><<<G, CGS_BS, smem, stream>>>((int)n, V, vpitch, W, W.c2, wbuf, nullptr,
-                                                   part, G, counter, stage, -1, cond_handle,
-      cgs_maps(vmaps), cgs_trmax());
+  const int cnt = vcap + 1;  // >= j + 2 for every j of the cycle
+  const char *maps = cgs_maps(vmaps);
+  const int trm = cgs_trmax();
+  const double *cnull = nullptr;
+  double *dnull = nullptr;
+  launch_pdl(k_cgs<CGS_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W, cnull,
+             (const double *)wbuf, dnull, part, G, counter, stage, -1, cond_handle, maps, trm);
+  allreduce(W.c1, cnt);
+  launch_pdl(k_cgs<CGS_UPD_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
+             (const double *)W.c1, (const double *)wbuf, wbuf, part, G, counter, stage, -1,
+             cond_handle, maps, trm);
+  allreduce(W.c2, cnt);
+  launch_pdl(k_cgs<CGS_UPD_NORM>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
+             (const double *)W.c2, (const double *)wbuf, dnull, part, G, counter, stage, -1,
+             cond_handle, maps, trm);
   allreduce(&ctrl_dev->hn2, 1);
-  count(3);
-  arnoldi_finish();
+  k_arnoldi_finish_slab<<<1, 1, 0, stream>>>(W, cond_active ? 1 : 0, cond_handle);
+  count(4);
 }
 
 }  // namespace irkg

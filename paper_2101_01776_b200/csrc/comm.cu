@@ -108,6 +108,18 @@ struct NcclComm : Comm {
     g_nccl.ck(g_nccl.Recv(recv_lo, count, ncclFloat64, prev, comm, st), "ncclRecv");
     g_nccl.ck(g_nccl.GroupEnd(), "ncclGroupEnd");
   }
+  void halo_batch(int nx, const Xfer *x, cudaStream_t st) override {
+    const int prev = (rank + nranks - 1) % nranks, next = (rank + 1) % nranks;
+    g_nccl.ck(g_nccl.GroupStart(), "ncclGroupStart");
+    for (int i = 0; i < nx; ++i) {
+      g_nccl.ck(g_nccl.Send(x[i].send_lo, x[i].count, ncclFloat64, prev, comm, st), "ncclSend");
+      g_nccl.ck(g_nccl.Send(x[i].send_hi, x[i].count, ncclFloat64, next, comm, st), "ncclSend");
+      g_nccl.ck(g_nccl.Recv(x[i].recv_hi, x[i].count, ncclFloat64, next, comm, st), "ncclRecv");
+      g_nccl.ck(g_nccl.Recv(x[i].recv_lo, x[i].count, ncclFloat64, prev, comm, st), "ncclRecv");
+    }
+    g_nccl.ck(g_nccl.GroupEnd(), "ncclGroupEnd");
+  }
+  bool capturable() const override { return true; }
 };
 
 struct CallbackComm : Comm {

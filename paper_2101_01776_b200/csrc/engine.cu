@@ -110,6 +110,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   if (const char *e = getenv("IRKG_JACOBI_SPLIT")) jacobi_split = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_PDL")) use_pdl = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_CARVEOUT")) use_carveout = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_SLAB_BATCH")) slab_batch = atoi(e) > 0 ? atoi(e) : 1;
   if (const char *e = getenv("IRKG_JWPS")) jwarps_per_sm = atoi(e) > 0 ? atoi(e) : 12;
   if (const char *e = getenv("IRKG_STRIP_OP")) strip_op = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_BOP_WPS")) bop_wps = atoi(e) > 0 ? atoi(e) : 12;
@@ -197,8 +198,84 @@ void Engine::read_ctrl() {
   check(cudaStreamSynchronize(stream), "sync");
 }
 
+// Boundary planes [0, H) and [nl-H, nl) of both halves of basis slot j
+// (j read on the device) -> halo_pack, laid out [half][lo | hi][H planes].
+__global__ void k_pack_slot_halo(const double *__restrict__ V, long long pitch, const GCtrl *ctrl,
+                                 long long N, int nl, long long P, int H, int halves,
+                                 double *__restrict__ out) {
+  const double *s = V + (size_t)ctrl->j * pitch;
+  const long long HP = (long long)H * P;
+  const long long total = (long long)halves * 2 * HP;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long h = i / (2 * HP), r = i % (2 * HP);
+    const long long q = r % HP;
+    out[i] = s[h * N + (r < HP ? q : (long long)(nl - H) * P + q)];
+  }
+}
+
+// Multi-rank Arnoldi step with the slot index on the device: pack + one
+// NCCL round for the v_j halos, the two inner solves (z1's halo doubles as
+// the block operator's), z2's halo, the block operator, CGS2 with
+// fixed-length all-reduces and the column finish.  Only device work and
+// NCCL calls: captured into the cycle graph like the single-rank step.
+void Engine::arnoldi_iteration_slab(const BlockSpec &B, long long n, int j_host) {
+  if (prob.kind == KIND_ARAKAWA) {
+    // the DAE's 9-point kernels take the slot as a fixed pointer (host loop)
+    if (j_host < 0) throw SolveError(IRKG_ERR_CONFIG, "internal: DAE slab step needs j");
+    VecIn vj{V + (size_t)j_host * vpitch, 0, nullptr, nullptr};
+    vj.scale_ptr = W.alpha + j_host;
+    precond(B, &vj, zbuf, nullptr);
+    block_op(B, zbuf, wbuf, nullptr, nullptr, nullptr);
+    if (timing) check(cudaEventRecord(ev0, stream));
+    cgs_slab(n);
+    if (timing) check(cudaEventRecord(ev1, stream));
+    return;
+  }
+  const int H = jhalo();
+  const long long P = plane_size();
+  const int nl = local_planes();
+  const int halves = B.size;
+  if (!halo_pack) dalloc_raw((void **)&halo_pack, sizeof(double) * 4 * GH * (size_t)P);
+  const long long tot = (long long)halves * 2 * H * P;
+  int gb = (int)((tot + 255) / 256);
+  gb = gb > sms * 4 ? sms * 4 : (gb < 1 ? 1 : gb);
+  k_pack_slot_halo<<<gb, 256, 0, stream>>>(V, vpitch, ctrl_dev, N, nl, P, H, halves, halo_pack);
+  count(1);
+  Comm::Xfer xf[2];
+  VecIn vslot{V, vpitch, ctrl_dev, W.alpha};
+  for (int h = 0; h < halves; ++h) {
+    Ghost &g = role(R_VIN0 + h);
+    g.field = nullptr;  // indexed input: consumers get the planes through vslot.lo/hi
+    xf[h] = Comm::Xfer{halo_pack + (size_t)h * 2 * H * P, halo_pack + ((size_t)h * 2 + 1) * H * P,
+                       g.lo + (size_t)(GH - H) * P, g.hi, (long long)H * P};
+    vslot.lo[h] = g.lo;
+    vslot.hi[h] = g.hi;
+  }
+  comm->halo_batch(halves, xf, stream);
+  counters.halo_exchanges += halves;
+  jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vslot, 0, nullptr, 0.0, zbuf, ctrl_dev);
+  if (B.size == 2) {
+    exchange(R_Z0, zbuf, H);  // z1 feeds the second row's rhs (and the operator below)
+    jacobi_chain(B.l2, B.gamma, B.dt, B.inner, &vslot, (int)N, zbuf, B.beta * B.beta / B.phi,
+                 zbuf + N, ctrl_dev);
+    exchange(R_X1, zbuf + N, 1);
+  } else {
+    exchange(R_X0, zbuf, 1);
+  }
+  counters.op_bytes += 8.0 * N * B.size * 3.0;
+  block_op_s(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev);
+  if (timing) check(cudaEventRecord(ev0, stream));
+  cgs_slab(n);
+  if (timing) check(cudaEventRecord(ev1, stream));
+}
+
 // One Arnoldi step: z = M^{-1} v_j, w = A z, CGS2 + column finish.
 void Engine::arnoldi_iteration(const BlockSpec &B, long long n) {
+  if (slab()) {
+    arnoldi_iteration_slab(B, n);
+    return;
+  }
   VecIn vslot{V, vpitch, ctrl_dev, W.alpha};
   precond(B, &vslot, zbuf, ctrl_dev);
   block_op(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev);
@@ -218,13 +295,16 @@ void Engine::drop_graphs() {
 // operator fields); the Arnoldi index and exit state live in the device
 // control block, so the same executable serves every cycle and Newton
 // iteration of that block.
-Engine::CycleGraph &Engine::cycle_graph(const BlockSpec &B, long long n) {
+// loop == false: a plain graph of ONE Arnoldi step, launched once per step
+// by the host (multi-rank: NCCL's captured work is not allowed inside a
+// conditional body).
+Engine::CycleGraph &Engine::cycle_graph(const BlockSpec &B, long long n, bool loop) {
   char key[512];
-  snprintf(key, sizeof key, "%d|%a|%a|%a|%a|%a|%d|%p|%a|%d|%p|%a|%d|%p|%a|%d|%p|%a|%d|%lld|%p|%d",
-           B.size, B.eta, B.beta, B.phi, B.gamma, B.dt, B.inner, (const void *)B.l1.a, B.l1.sigma,
-           B.l1.present, (const void *)B.l2.a, B.l2.sigma, B.l2.present, (const void *)B.c12.a,
-           B.c12.sigma, B.c12.present, (const void *)B.c21.a, B.c21.sigma, B.c21.present, n,
-           (void *)V, vcap);
+  snprintf(key, sizeof key, "%c|%d|%a|%a|%a|%a|%a|%d|%p|%a|%d|%p|%a|%d|%p|%a|%d|%p|%a|%d|%lld|%p|%d",
+           loop ? 'W' : 'S', B.size, B.eta, B.beta, B.phi, B.gamma, B.dt, B.inner,
+           (const void *)B.l1.a, B.l1.sigma, B.l1.present, (const void *)B.l2.a, B.l2.sigma,
+           B.l2.present, (const void *)B.c12.a, B.c12.sigma, B.c12.present,
+           (const void *)B.c21.a, B.c21.sigma, B.c21.present, n, (void *)V, vcap);
   auto it = graphs.find(key);
   if (it != graphs.end()) return it->second;
   if (graphs.size() > 64) drop_graphs();
@@ -232,22 +312,26 @@ Engine::CycleGraph &Engine::cycle_graph(const BlockSpec &B, long long n) {
   check(cudaStreamSynchronize(stream), "sync");
   CycleGraph cg;
   check(cudaGraphCreate(&cg.g, 0), "cudaGraphCreate");
-  check(cudaGraphConditionalHandleCreate(&cg.h, cg.g, 1, cudaGraphCondAssignDefault), "cond handle");
-  cudaGraphNodeParams np = {};
-  np.type = cudaGraphNodeTypeConditional;
-  np.conditional.handle = cg.h;
-  np.conditional.type = cudaGraphCondTypeWhile;
-  np.conditional.size = 1;
-  cudaGraphNode_t node;
-  check(cudaGraphAddNode(&node, cg.g, nullptr, 0, &np), "cond node");
-  cudaGraph_t body = np.conditional.phGraph_out[0];
+  cudaGraph_t body = cg.g;
+  if (loop) {
+    check(cudaGraphConditionalHandleCreate(&cg.h, cg.g, 1, cudaGraphCondAssignDefault),
+          "cond handle");
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cg.h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    check(cudaGraphAddNode(&node, cg.g, nullptr, 0, &np), "cond node");
+    body = np.conditional.phGraph_out[0];
+  }
   cudaStream_t saved = stream;
   stream = cap_stream;
   const long long launches0 = counters.kernel_launches;
   const double pb = counters.precond_bytes, ob = counters.op_bytes;
   check(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0,
                                       cudaStreamCaptureModeRelaxed), "capture");
-  cond_active = true;
+  cond_active = loop;
   cond_handle = cg.h;
   try {
     arnoldi_iteration(B, n);
@@ -320,17 +404,32 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
     int m = std::min(restart, maxit - total_it);
     cycle_init(m);
     if (slab()) {
-      // multi-rank: host-driven Arnoldi loop (slot j resolved on the host,
-      // halo exchanges inside precond/block_op, all-reduces inside cgs_slab)
-      for (int it = 0; it < m; ++it) {
-        VecIn vj{V + (size_t)it * vpitch, 0, nullptr, nullptr};
-        vj.scale_ptr = W.alpha + it;
-        precond(B, &vj, zbuf, nullptr);
-        block_op(B, zbuf, wbuf, nullptr, nullptr, nullptr);
-        if (timing) check(cudaEventRecord(ev0, stream));
-        cgs_slab(n, it);  // includes the all-reduces between the sweeps
+      // multi-rank: host-driven Arnoldi loop; with the NCCL transport each
+      // step is one graph launch (captured NCCL halos + all-reduces)
+      const bool g1 = use_graphs && !timing && comm->capturable() && prob.kind != KIND_ARAKAWA;
+      if (g1) {
+        // steps go out in batches without a host round trip in between; a
+        // step launched after the exit test fired is inert (every kernel
+        // checks cycle_done; the NCCL rounds move stale, unused values)
+        CycleGraph &cg = cycle_graph(B, n, false);
+        int launched = 0;
+        while (launched < m) {
+          const int b = std::min(slab_batch, m - launched);
+          for (int k = 0; k < b; ++k) check(cudaGraphLaunch(cg.ex, stream), "cudaGraphLaunch");
+          launched += b;
+          read_ctrl();
+          if (ctrl_host->cycle_done) break;
+        }
+        const int its = ctrl_host->j + 1;
+        counters.kernel_launches += (long long)cg.body_kernels * launched;
+        counters.cgs_launches += 3LL * its;
+        counters.arnoldi_iterations += its;
+      }
+      for (int it = 0; it < m && !g1; ++it) {
+        {
+          arnoldi_iteration_slab(B, n, it);  // (records ev0/ev1 around CGS2 when timing)
+        }
         if (timing) {
-          check(cudaEventRecord(ev1, stream));
           check(cudaEventSynchronize(ev1), "sync");
           float ms = 0.f;
           check(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
@@ -343,7 +442,7 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
       }
     } else if (use_graphs && !timing) {
       // whole Arnoldi loop of this cycle as one graph launch (device-side WHILE)
-      CycleGraph &cg = cycle_graph(B, n);
+      CycleGraph &cg = cycle_graph(B, n, true);
       check(cudaGraphLaunch(cg.ex, stream), "cudaGraphLaunch");
       read_ctrl();
       const int its = ctrl_host->j + 1;

@@ -47,6 +47,18 @@ struct Comm {
   // rank+1 (periodic); receive rank+1's first into recv_hi, rank-1's last into recv_lo
   virtual void halo(const double *send_lo, const double *send_hi, double *recv_lo,
                     double *recv_hi, long long count, cudaStream_t st) = 0;
+  struct Xfer {
+    const double *send_lo, *send_hi;
+    double *recv_lo, *recv_hi;
+    long long count;
+  };
+  // several halo exchanges in one round (one NCCL group)
+  virtual void halo_batch(int nx, const Xfer *x, cudaStream_t st) {
+    for (int i = 0; i < nx; ++i)
+      halo(x[i].send_lo, x[i].send_hi, x[i].recv_lo, x[i].recv_hi, x[i].count, st);
+  }
+  // enqueues only device work (no host round trip): graph-capturable
+  virtual bool capturable() const { return false; }
 };
 Comm *make_nccl_comm(const void *id128, int rank, int nranks);
 Comm *make_callback_comm(int rank, int nranks, irkg_allreduce_fn a, irkg_halo_fn h, void *u);
@@ -171,7 +183,7 @@ struct Engine {
   bool cond_active = false;
   cudaGraphConditionalHandle cond_handle{};
   cudaStream_t cap_stream = nullptr;
-  CycleGraph &cycle_graph(const BlockSpec &B, long long n);
+  CycleGraph &cycle_graph(const BlockSpec &B, long long n, bool loop);
   void arnoldi_iteration(const BlockSpec &B, long long n);
   void drop_graphs();
   int cgs_stage_doubles() const;  // CGS shared-memory ring per CTA (doubles)
@@ -184,7 +196,10 @@ struct Engine {
                   double *out_norm, const GCtrl *skip);
   double residual_s(const double *U, const double *K, double *F);
   void backsub_s(double dt, BacksubTerms T, const double *gst, const double *y, double *rhs);
-  void cgs_slab(long long n, int j);  // CGS2 with all-reduces between sweeps (multi-rank)
+  void cgs_slab(long long n);  // CGS2 with all-reduces between sweeps (multi-rank)
+  void arnoldi_iteration_slab(const BlockSpec &B, long long n, int j_host = -1);
+  double *halo_pack = nullptr;
+  int slab_batch = 4;  // multi-rank Arnoldi steps launched per host check (IRKG_SLAB_BATCH)  // packed boundary planes of basis slot j (2 halves x lo/hi)
   // dae.cu (vorticity/streamfunction DAE, reordered mode)
   bool dae = false;
   double h2 = 0.0;
