@@ -376,28 +376,14 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
   const long long n = (long long)B.size * N;
   const int spa = B.size;
   KrylovOut out;
-  double bnorm2 = norm2(rhs, n);
-  double bnorm = std::sqrt(bnorm2);
+  // ||b|| and the control block stay on the device: the first host round
+  // trip of a solve is the end of its first restart cycle
+  norm2_dev(rhs, n);
+  gmres_init(maxit, rtol);
   check(cudaMemsetAsync(x, 0, n * sizeof(double), stream));
-  if (bnorm == 0.0) {
-    out.iterations = 0;
-    out.converged = 1;
-    out.residuals = {0.0};
-    return out;
-  }
-  // host-side init of the control block
-  GCtrl c{};
-  c.maxit = maxit;
-  c.bnorm = bnorm;
-  c.beta = bnorm;
-  c.rtol = rtol;
-  c.n_res = 1;
-  double one = 1.0;  // residuals[0] = beta / bnorm
-  check(cudaMemcpyAsync(ctrl_dev, &c, sizeof(GCtrl), cudaMemcpyHostToDevice, stream));
-  check(cudaMemcpyAsync(W.res, &one, sizeof(double), cudaMemcpyHostToDevice, stream));
   check(cudaMemcpyAsync(V, rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
   int total_it = 0;
-  int converged = (1.0 <= rtol);
+  int converged = 0;
   VecIn vslot{V, vpitch, ctrl_dev, W.alpha};
   VecIn vfix{ubuf, 0, nullptr, nullptr};
   while (!converged && total_it < maxit) {
@@ -442,13 +428,10 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
       }
     } else if (use_graphs && !timing) {
       // whole Arnoldi loop of this cycle as one graph launch (device-side WHILE)
+      // (no host read here: the counters are settled after the cycle end)
       CycleGraph &cg = cycle_graph(B, n, true);
       check(cudaGraphLaunch(cg.ex, stream), "cudaGraphLaunch");
-      read_ctrl();
-      const int its = ctrl_host->j + 1;
-      counters.kernel_launches += (long long)cg.body_kernels * its;
-      counters.cgs_launches += 3LL * its;
-      counters.arnoldi_iterations += its;
+      graph_body_kernels = cg.body_kernels;
     } else {
       for (int it = 0; it < m; ++it) {
         if (timing) check(cudaEventRecord(evp[0], stream));
@@ -490,16 +473,27 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
     block_op(B, x, V, rhs, &ctrl_dev->rr, nullptr);
     cycle_end();
     read_ctrl();
+    if (graph_body_kernels > 0) {  // WHILE-graph cycle: its = new iterations
+      const int its = ctrl_host->total_it - total_it;
+      counters.kernel_launches += (long long)graph_body_kernels * std::max(its, 1);
+      counters.cgs_launches += 3LL * its;
+      counters.arnoldi_iterations += its;
+      graph_body_kernels = 0;
+    }
     total_it = ctrl_host->total_it;
     converged = ctrl_host->converged;
     if (ctrl_host->zero_diag)
       throw SolveError(IRKG_ERR_VALUE, "Jacobi inner solver needs a nonzero diagonal");
     if (ctrl_host->err_breakdown) {
       char msg[160];
-      double tr = std::sqrt(ctrl_host->rr) / bnorm;
+      double tr = std::sqrt(ctrl_host->rr) / ctrl_host->bnorm;
       snprintf(msg, sizeof msg, "Arnoldi breakdown with residual %.3e above rtol %.3e", tr, rtol);
       throw SolveError(IRKG_ERR_BREAKDOWN, msg);
     }
+  }
+  if (maxit <= 0) {  // no cycle ran: b = 0 is still converged (set by gmres_init)
+    read_ctrl();
+    converged = ctrl_host->converged;
   }
   out.iterations = total_it;
   out.converged = converged;
@@ -620,7 +614,7 @@ Op Engine::op_of(int slot) const {
 // src/irk_core.py:225-338 (identity mass).
 void Engine::transformed_solve(double dt, const double *rhs, double *dk, irkg_step_stats *stats) {
   // g = Q^T F
-  std::vector<double> qt(s * s), qr(s * s);
+  std::vector<double> qt(s * s);
   for (int i = 0; i < s; ++i)
     for (int k = 0; k < s; ++k) qt[i * s + k] = tab.q[k * IRKG_MAX_STAGES + i];
   stage_mix(qt.data(), rhs, Gs, false);
@@ -689,13 +683,18 @@ void Engine::transformed_solve(double dt, const double *rhs, double *dk, irkg_st
     }
   }
   // dk = (Q R0) y
+  if (dk) stage_mix(qr_matrix().data(), Y, dk, false);
+}
+
+std::vector<double> Engine::qr_matrix() const {
+  std::vector<double> qr(s * s);
   for (int i = 0; i < s; ++i)
     for (int j = 0; j < s; ++j) {
       double acc = 0.0;
       for (int k = 0; k < s; ++k) acc += tab.q[i * IRKG_MAX_STAGES + k] * tab.r[k * IRKG_MAX_STAGES + j];
       qr[i * s + j] = acc;
     }
-  stage_mix(qr.data(), Y, dk, false);
+  return qr;
 }
 
 // ------------------------------------------------------------ phase probe
@@ -760,6 +759,7 @@ double Engine::probe_phase(int phase, int j, int reps) {
 // src/nonlinear.py:186-236.  K (s,N) in/out.
 void Engine::newton(const double *u, double *K, double t, double dt, irkg_step_stats *stats) {
   auto tic = std::chrono::steady_clock::now();
+  const std::vector<double> qrm = qr_matrix();
   stage_values(u, K, dt, U);
   double f0 = std::sqrt(residual(U, K, F));
   stats->n_residuals = 0;
@@ -782,15 +782,9 @@ void Engine::newton(const double *u, double *K, double t, double dt, irkg_step_s
       stats->jacobian_assemblies += s;
       have_ops = true;
     }
-    transformed_solve(dt, F, DK, stats);
-    {
-      // K += dk
-      std::vector<double> eye(s * s, 0.0);
-      for (int i = 0; i < s; ++i) eye[i * s + i] = 1.0;
-      stage_mix(eye.data(), DK, K, true);
-    }
+    transformed_solve(dt, F, nullptr, stats);  // y (s,N) left in Y
+    newton_update(qrm.data(), dt, Y, u, K, U);  // K += (Q R0) y ; U = u + dt A0 K
     stats->newton_iterations += 1;
-    stage_values(u, K, dt, U);
     fn = std::sqrt(residual(U, K, F));
     if (stats->n_residuals <= IRKG_MAX_NEWTON) stats->residual_history[stats->n_residuals++] = fn;
   }

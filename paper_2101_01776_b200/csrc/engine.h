@@ -292,6 +292,10 @@ struct Engine {
   void mupdate(long long n, const double *coef, const double *w, double *out, bool to_next,
                double *out_norm);
   void cycle_init(int m);
+  void gmres_init(int maxit, double rtol);
+  void norm2_dev(const double *x, long long n);
+  void newton_update(const double *QR_rowmajor_s, double dt, const double *Yv, const double *u,
+                     double *K, double *Uo);
   void arnoldi_finish();
   void backsolve();
   void vcombine(long long n, const double *coef, double *out);
@@ -303,11 +307,14 @@ struct Engine {
   bool have_last_block = false;
   double probe_phase(int phase, int j, int reps);
   void read_ctrl();
+  int graph_body_kernels = 0;  // body size of the WHILE graph launched this cycle
+  std::vector<double> qr_matrix() const;  // Q R0, row-major s x s
   KrylovOut gmres(const BlockSpec &B, const double *rhs, double *x, double rtol, int maxit,
                   int restart);
   void build_linearization(const double *U);
   Op op_of(int slot) const;
   double gamma_of(double eta, double beta) const;
+  // dk == nullptr: leave y in Y (the Newton loop fuses dk = (Q R0) y into its update)
   void transformed_solve(double dt, const double *rhs, double *dk, irkg_step_stats *stats);
   void newton(const double *u, double *K, double t, double dt, irkg_step_stats *stats);
 };

@@ -619,6 +619,20 @@ bool Engine::jacobi_chain_fused(const Op &L, double alpha, double dt, int inner,
     bands = bands < 1 ? 1 : bands;
     int span = (int)((grid.ny + bands - 1) / bands);
     span = span < 8 ? 8 : (span > 128 ? 128 : span);
+    if (jacobi_split) {
+      // the split kernel walks span + 2(K-1) input rows in unrolled groups of
+      // JRING: take spans that fill whole groups, the longest (least halo
+      // redundancy) that still leaves ~6 resident warps per SM
+      const int h2 = 2 * (inner - 1);
+      int k = 2;
+      while (k < 16) {
+        const int nxt = JRING * (k + 1) - h2;
+        const long long nw = (long long)strips * ((grid.ny + nxt - 1) / nxt);
+        if (nw < 6LL * sms) break;
+        ++k;
+      }
+      span = JRING * k - h2;
+    }
     if (jspan_override > 0) span = jspan_override;
     if (span > grid.ny) span = grid.ny;
     const int nb = (grid.ny + span - 1) / span;

@@ -74,6 +74,42 @@ __global__ void k_norm2(int n, const double *__restrict__ x, double *part, int G
 // ------------------------------------------------------ stage-space passes
 
 // U_i = u + dt * (A0 K)_i  (src/nonlinear.py:147)
+// Newton update fused with the next stage values (src/nonlinear.py:221,
+// 147): K_i += sum_k (Q R0)_ik y_k ;  U_i = u + dt sum_j A0_ij K_j.
+// Same arithmetic as stage_mix (dk) + stage_mix (K += dk) + stage_values.
+__global__ void k_newton_update(int n, int s, StageConsts QR, StageConsts A, double dt,
+                                const double *__restrict__ Y, const double *__restrict__ u,
+                                double *__restrict__ K, double *__restrict__ U) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    double yv[MAXS], kv[MAXS];
+#pragma unroll
+    for (int k = 0; k < MAXS; ++k)
+      if (k < s) yv[k] = Y[(size_t)k * n + p];
+#pragma unroll
+    for (int i = 0; i < MAXS; ++i) {
+      if (i < s) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < MAXS; ++k)
+          if (k < s) acc += QR.a[i * MAXS + k] * yv[k];
+        kv[i] = K[(size_t)i * n + p] + acc;
+        K[(size_t)i * n + p] = kv[i];
+      }
+    }
+    const double up = u[p];
+#pragma unroll
+    for (int i = 0; i < MAXS; ++i) {
+      if (i < s) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < MAXS; ++j)
+          if (j < s) acc += A.a[i * MAXS + j] * kv[j];
+        U[(size_t)i * n + p] = up + dt * acc;
+      }
+    }
+  }
+}
+
 __global__ void k_stage_values(int n, int s, const double *__restrict__ u,
                                const double *__restrict__ K, StageConsts A, double dt,
                                double *__restrict__ U) {
@@ -424,8 +460,30 @@ __global__ void k_mupdate(int n, double *__restrict__ V, long long pitch,
 // ------------------------------------------------------ scalar control
 
 // Start a restart cycle: v_0 = r / beta  (src/sparsela.py:207-216).
+// Control block of a fresh solve from the device-side ||b||^2 (x0 = 0):
+// no host round trip before the first cycle.  b = 0 is converged at once
+// (src/sparsela.py:193-198); the cycles then run as no-ops.
+__global__ void k_gmres_init(GWork W, const double *bn2, int maxit, double rtol) {
+  GCtrl *c = W.ctrl;
+  const double bnorm = sqrt(*bn2);
+  GCtrl z{};
+  z.maxit = maxit;
+  z.rtol = rtol;
+  z.bnorm = bnorm;
+  z.beta = bnorm;
+  z.n_res = 1;
+  z.converged = (bnorm == 0.0) ? 1 : 0;
+  *c = z;
+  W.res[0] = (bnorm == 0.0) ? 0.0 : 1.0;
+}
+
 __global__ void k_cycle_init(GWork W, int m) {
   GCtrl *c = W.ctrl;
+  if (c->bnorm == 0.0) {  // zero right-hand side: nothing to iterate
+    c->k = 0;
+    c->cycle_done = 1;
+    return;
+  }
   c->j = 0;
   c->m = m;
   c->k = 0;
@@ -485,15 +543,34 @@ __global__ void k_arnoldi_finish(GWork W) {
 
 // y = H(:k,:k)^{-1} g(:k) by back substitution (src/sparsela.py:258-261),
 // then fold alpha into y so that x += V (alpha .* y).
-__global__ void k_backsolve(GWork W) {
-  GCtrl *c = W.ctrl;
+// Column-oriented on MAXR threads: thread l keeps the running r_l = g_l -
+// sum_{i' > l} H(l,i') y_i' in a register; column i-1 of H is fetched while
+// column i is applied, so the k sequential steps cost two barriers each
+// instead of k dependent global loads.
+__global__ void __launch_bounds__(MAXR) k_backsolve(GWork W) {
+  __shared__ double ybc;
+  const GCtrl *c = W.ctrl;
   const int k = c->k;
+  const int t = threadIdx.x;
+  double r = t < k ? W.g[t] : 0.0;
+  double yt = 0.0;
+  double hcol = (k > 0 && t < k) ? W.H[(size_t)(k - 1) * (MAXR + 1) + t] : 0.0;
   for (int i = k - 1; i >= 0; --i) {
-    double dot = 0.0;
-    for (int l = i + 1; l < k; ++l) dot += W.H[(size_t)l * (MAXR + 1) + i] * W.y[l];
-    W.y[i] = (W.g[i] - dot) / W.H[(size_t)i * (MAXR + 1) + i];
+    const double hnext = (i > 0 && t < i) ? W.H[(size_t)(i - 1) * (MAXR + 1) + t] : 0.0;
+    if (t == i) {
+      yt = r / hcol;  // hcol = H(i,i) in thread i
+      ybc = yt;
+    }
+    __syncthreads();
+    const double yi = ybc;
+    if (t < i) r -= hcol * yi;
+    __syncthreads();
+    hcol = hnext;
   }
-  for (int i = 0; i < k; ++i) W.c1[i] = W.alpha[i] * W.y[i];
+  if (t < k) {
+    W.y[t] = yt;
+    W.c1[t] = W.alpha[t] * yt;
+  }
 }
 
 // out = sum_{l<k} s_l * coef_l
@@ -520,6 +597,7 @@ __global__ void k_axpy(int n, double a, const double *__restrict__ x, double *__
 // True residual bookkeeping after x += Z y (src/sparsela.py:263-272).
 __global__ void k_cycle_end(GWork W) {
   GCtrl *c = W.ctrl;
+  if (c->bnorm == 0.0) return;
   double rn = sqrt(c->rr);
   double true_rel = rn / c->bnorm;
   W.res[c->n_res - 1] = true_rel;
@@ -575,6 +653,26 @@ double Engine::norm2(const double *x, long long n, const GCtrl *skip) {
   check(cudaMemcpyAsync(&v, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost, stream));
   check(cudaStreamSynchronize(stream));
   return v;
+}
+
+void Engine::newton_update(const double *QR_rowmajor_s, double dt, const double *Yv,
+                           const double *u, double *K, double *Uo) {
+  StageConsts QR{}, A{};
+  QR.s = A.s = s;
+  for (int i = 0; i < s; ++i)
+    for (int j = 0; j < s; ++j) {
+      QR.a[i * MAXS + j] = QR_rowmajor_s[i * s + j];
+      A.a[i * MAXS + j] = tab.a0[i * IRKG_MAX_STAGES + j];
+    }
+  k_newton_update<<<grid_for(N), 256, 0, stream>>>((int)N, s, QR, A, dt, Yv, u, K, Uo);
+  count(1);
+}
+
+// sum of squares into scal_dev[0] (all ranks), no host round trip
+void Engine::norm2_dev(const double *x, long long n) {
+  k_norm2<256><<<G, 256, 0, stream>>>((int)n, x, part, G, &scal_dev[0], counter, nullptr);
+  count(1);
+  allreduce(&scal_dev[0], 1);
 }
 
 void Engine::stage_values(const double *u, const double *K, double dt, double *U) {
@@ -760,6 +858,10 @@ void Engine::mupdate(long long n, const double *coef, const double *w, double *o
   count(1);
 }
 
+void Engine::gmres_init(int maxit, double rtol) {
+  k_gmres_init<<<1, 1, 0, stream>>>(W, &scal_dev[0], maxit, rtol);
+  count(1);
+}
 void Engine::cycle_init(int m) {
   k_cycle_init<<<1, 1, 0, stream>>>(W, m);
   count(1);
@@ -769,7 +871,7 @@ void Engine::arnoldi_finish() {
   count(1);
 }
 void Engine::backsolve() {
-  k_backsolve<<<1, 1, 0, stream>>>(W);
+  k_backsolve<<<1, MAXR, 0, stream>>>(W);
   count(1);
 }
 void Engine::vcombine(long long n, const double *coef, double *out) {
