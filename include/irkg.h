@@ -192,6 +192,13 @@ int irkg_newton_step(irkg_ctx *ctx, const double *u_dev, double *k_dev, double t
 /* step (src/nonlinear.py:299-314): u_dev (N) in/out, u <- u + dt b0^T K. */
 int irkg_step(irkg_ctx *ctx, double *u_dev, double t, double dt, irkg_step_stats *stats);
 
+/* _dirk_step (src/nonlinear.py:239-296), the stepper the reference's step()
+ * uses for SDIRK tableaux (304-306): sequential stage solves, each a Newton
+ * loop over 1x1 GMRES on (I - dt a_ii L) with the Jacobi-k ShiftedSolver.
+ * The tableau comes through irkg_set_tableau with nblocks = 0 (a0 lower
+ * triangular, b0, c0).  u_dev (N) in/out.  Block records are keyed by stage. */
+int irkg_dirk_step(irkg_ctx *ctx, double *u_dev, double t, double dt, irkg_step_stats *stats);
+
 /* Same as irkg_step with host buffers: H2D copy of u, step, D2H copy
  * (the end-to-end path timed by bench.py's e2e leg). */
 int irkg_step_host(irkg_ctx *ctx, double *u_host, double t, double dt, irkg_step_stats *stats);

@@ -12,6 +12,7 @@ Follows, function by function, the reference package
 * ``stage_residual``          src/nonlinear.py:145-152
 * ``newton_like_step``        src/nonlinear.py:186-236
 * ``step`` / ``integrate``    src/nonlinear.py:299-314, 331-374
+* ``dirk_step``               src/nonlinear.py:239-296 (the SDIRK baseline)
 
 Matrices are scipy CSR; ``mass`` is the identity throughout (all BASELINE
 configurations have M = I).  Exact inner solves use a sparse LU
@@ -439,6 +440,46 @@ def newton_like_step(sys, u, k, t, dt, prep, cfg):
         stats.converged = True
     stats.wall_time = time.perf_counter() - tic
     return k, stats
+
+
+def dirk_step(sys, u, t, dt, tableau, cfg):
+    """src/nonlinear.py:239-296: sequential stage solves of an SDIRK tableau;
+    returns (u_next, k, StepStats) with block_iterations keyed by stage."""
+    s, n = tableau.s, sys.dim
+    k = np.zeros((s, n))
+    stats = StepStats()
+    tic = time.perf_counter()
+    for i in range(s):
+        base = u + dt * (tableau.a0[i, :i] @ k[:i]) if i else u.copy()
+        aii = tableau.a0[i, i]
+        ti = t + tableau.c0[i] * dt
+        ki = np.zeros(n)
+        res = sys.rhs(base + dt * aii * ki, ti) - ki
+        f0 = np.linalg.norm(res)
+        stats.residual_history.append(f0)
+        tol = max(cfg.newton_rtol * f0, cfg.newton_abs_floor)
+        it = 0
+        while np.linalg.norm(res) > tol:
+            if it >= cfg.newton_maxit:
+                stats.wall_time = time.perf_counter() - tic
+                raise StepFailureError(f"DIRK stage {i} stalled", stats=stats)
+            lmat = _csr(sys.linearize(base + dt * aii * ki, ti))
+            stats.jacobian_assemblies += 1
+            solver = ShiftedSolver(1.0, lmat, dt * aii, cfg.inner)
+            dk, rep = gmres(lambda x: x - dt * aii * (lmat @ x), res, n, solver.solve, 1,
+                            cfg.krylov_rtol, cfg.krylov_maxit, cfg.restart)
+            ki += dk
+            it += 1
+            stats.newton_iterations += 1
+            stats.krylov_iterations += rep.iterations
+            stats.precond_applications += rep.precond_applications
+            stats.block_iterations.setdefault(i, []).append(rep.iterations)
+            res = sys.rhs(base + dt * aii * ki, ti) - ki
+            stats.residual_history.append(np.linalg.norm(res))
+        k[i] = ki
+    stats.converged = True
+    stats.wall_time = time.perf_counter() - tic
+    return u + dt * (tableau.b0 @ k), k, stats
 
 
 def step(sys, u, t, dt, prep, cfg):

@@ -94,6 +94,16 @@ def prepare(family, s):
     )
 
 
+def dirk_tableau(family):
+    """SDIRK coefficients (src/tableau.py:283-326, make_tableau 336-341),
+    from the reference's own values."""
+    for key, doc in _load().items():
+        if key.split(":")[0] == family:
+            return Tableau(family=doc["family"], s=int(doc["s"]), order=int(doc["order"]),
+                           a0=_arr(doc["a0"]), b0=_arr(doc["b0"]), c0=_arr(doc["c0"]))
+    raise KeyError(family)
+
+
 def gamma_star(eta, beta):
     # src/tableau.py:382-386
     if eta <= 0.0:

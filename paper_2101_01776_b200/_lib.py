@@ -155,6 +155,7 @@ _SIGS = {
     "irkg_set_timing": (_I, [_P, _I]),
     "irkg_get_counters": (_I, [_P, C.POINTER(Counters)]),
     "irkg_probe_phase": (_I, [_P, _I, _I, _I, C.POINTER(C.c_double)]),
+    "irkg_dirk_step": (_I, [_P, _P, C.c_double, C.c_double, C.POINTER(StepStatsC)]),
     "irkg_stage_residual": (_I, [_P, _P, _P, _D, _D, _P, C.POINTER(_D)]),
     "irkg_newton_step": (_I, [_P, _P, _P, _D, _D, C.POINTER(StepStatsC)]),
     "irkg_step": (_I, [_P, _P, _D, _D, C.POINTER(StepStatsC)]),

@@ -209,10 +209,11 @@ Op Engine::opref(const Op &o) const {
   return r;
 }
 
-StageGhosts Engine::stage_ghosts(const double *Ub, long long stride) const {
+StageGhosts Engine::stage_ghosts(const double *Ub, long long stride, int nst) const {
   StageGhosts sg{};
   if (!slab()) return sg;
-  for (int i = 0; i < s; ++i) {
+  if (nst < 0) nst = s;
+  for (int i = 0; i < nst; ++i) {
     FRef f = ref(Ub + (size_t)i * stride);
     sg.lo[i] = f.lo;
     sg.hi[i] = f.hi;

@@ -952,6 +952,19 @@ int irkg_step(irkg_ctx *ctx, double *u_dev, double t, double dt, irkg_step_stats
   });
 }
 
+int irkg_dirk_step(irkg_ctx *ctx, double *u_dev, double t, double dt, irkg_step_stats *stats) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    if (!e.have_tab || !e.have_cfg) throw SolveError(IRKG_ERR_CONFIG, "tableau/solver not set");
+    if (e.dae) throw SolveError(IRKG_ERR_CONFIG, "DIRK tableaux are not supported on DAE systems");
+    irkg_krylov_report fr = stats->fail_report;
+    memset(stats, 0, offsetof(irkg_step_stats, fail_report));
+    stats->fail_report = fr;
+    e.dirk_step(u_dev, t, dt, stats);
+    check(cudaStreamSynchronize(e.stream));
+  });
+}
+
 int irkg_step_host(irkg_ctx *ctx, double *u_host, double t, double dt, irkg_step_stats *stats) {
   IRKG_GUARD({
     Engine &e = *ctx->eng;

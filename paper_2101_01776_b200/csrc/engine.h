@@ -155,7 +155,7 @@ struct Engine {
   void allreduce(double *dev, int count);
   FRef ref(const double *p) const;
   Op opref(const Op &o) const;
-  StageGhosts stage_ghosts(const double *Ub, long long stride) const;
+  StageGhosts stage_ghosts(const double *Ub, long long stride, int nst = -1) const;
   void free_ghosts();
   int jhalo() const { return cfg.inner > 1 ? cfg.inner - 1 : 1; }
 
@@ -194,7 +194,7 @@ struct Engine {
                    const double *t_in, const double *x, double *x_out, const GCtrl *skip);
   void block_op_s(const BlockSpec &B, const double *z, double *w, const double *b,
                   double *out_norm, const GCtrl *skip);
-  double residual_s(const double *U, const double *K, double *F);
+  double residual_s(const double *U, const double *K, double *F, int nst);
   void backsub_s(double dt, BacksubTerms T, const double *gst, const double *y, double *rhs);
   void cgs_slab(long long n);  // CGS2 with all-reduces between sweeps (multi-rank)
   void arnoldi_iteration_slab(const BlockSpec &B, long long n, int j_host = -1);
@@ -278,7 +278,7 @@ struct Engine {
   void count(int k);
   double norm2(const double *x, long long n, const GCtrl *skip = nullptr);
   void stage_values(const double *u, const double *K, double dt, double *U);
-  double residual(const double *U, const double *K, double *F);
+  double residual(const double *U, const double *K, double *F, int nst = -1);
   void opfields(const double *U, const OpWeights &W, double *A);
   void stage_mix(const double *M_rowmajor_s, const double *in, double *out, bool accumulate);
   void step_update(double dt, const double *K, double *u);
@@ -317,6 +317,8 @@ struct Engine {
   // dk == nullptr: leave y in Y (the Newton loop fuses dk = (Q R0) y into its update)
   void transformed_solve(double dt, const double *rhs, double *dk, irkg_step_stats *stats);
   void newton(const double *u, double *K, double t, double dt, irkg_step_stats *stats);
+  // dirk.cu: sequential stage solves of an (S)DIRK tableau (src/nonlinear.py:239-296)
+  void dirk_step(double *u, double t, double dt, irkg_step_stats *stats);
 };
 
 }  // namespace irkg

@@ -688,11 +688,12 @@ void Engine::stage_values_n(const double *u, const double *K, double dt, double 
   count(1);
 }
 
-double Engine::residual(const double *U, const double *K, double *F) {
-  if (ndim >= 2) return residual_s(U, K, F);
+double Engine::residual(const double *U, const double *K, double *F, int nst) {
+  if (nst < 0) nst = s;
+  if (ndim >= 2) return residual_s(U, K, F, nst);
   dispatch_kd(prob.kind, ndim, [&](auto KD, auto ND) {
     k_residual<decltype(KD)::value, decltype(ND)::value, 256>
-        <<<G, 256, 0, stream>>>(grid, kp, s, U, K, F, part, G, &scal_dev[0], counter);
+        <<<G, 256, 0, stream>>>(grid, kp, nst, U, K, F, part, G, &scal_dev[0], counter);
   });
   count(1);
   double v = 0.0;

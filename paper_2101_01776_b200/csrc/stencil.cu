@@ -706,14 +706,14 @@ void Engine::backsub_s(double dt, BacksubTerms T, const double *gst, const doubl
   count(1);
 }
 
-double Engine::residual_s(const double *Ust, const double *K, double *Fo) {
+double Engine::residual_s(const double *Ust, const double *K, double *Fo, int nst) {
   int span;
   const dim3 gr = slide_grid(span);
   if (slab())
-    for (int i = 0; i < s; ++i) exchange(R_STAGE + i, Ust + (size_t)i * N, 1);
+    for (int i = 0; i < nst; ++i) exchange(R_STAGE + i, Ust + (size_t)i * N, 1);
   dispatch_kd23(prob.kind, ndim, [&](auto KD, auto ND) {
     k_residual_s<decltype(KD)::value, decltype(ND)::value>
-        <<<gr, SBX, 0, stream>>>(grid, kp, s, Ust, stage_ghosts(Ust, N), K, Fo, span, part,
+        <<<gr, SBX, 0, stream>>>(grid, kp, nst, Ust, stage_ghosts(Ust, N, nst), K, Fo, span, part,
                                  counter, &scal_dev[0]);
   });
   count(1);

@@ -78,6 +78,24 @@ def ptr(t):
     return C.c_void_p(t.data_ptr())
 
 
+def dirk_tableau_struct(tab):
+    """An SDIRK ButcherTableau as irkg_tableau: coefficients only, nblocks = 0."""
+    s = int(tab.s)
+    S = _lib.MAX_STAGES
+    if s > S:
+        raise ConfigurationError(f"s = {s} exceeds {S}")
+    out = _lib.Tableau()
+    out.s = s
+    a0 = np.asarray(tab.a0, dtype=float)
+    for i in range(s):
+        out.b0[i] = float(tab.b0[i])
+        out.c0[i] = float(tab.c0[i])
+        for j in range(s):
+            out.a0[i * S + j] = a0[i, j]
+    out.nblocks = 0
+    return out
+
+
 def tableau_struct(prep):
     """Pack a (reference or mirror) StagePrep into the C irkg_tableau."""
     tab = prep.tableau
@@ -193,6 +211,24 @@ class Context:
             _raise(rc)
         self._prep_key = key
         self._prep_ref = prep
+
+    def set_dirk_tableau(self, tab):
+        key = ("dirk", str(tab.family), np.asarray(tab.a0, dtype=float).tobytes())
+        if key == self._prep_key:
+            return
+        ts = dirk_tableau_struct(tab)
+        rc = self.lib.irkg_set_tableau(self.h, C.byref(ts))
+        if rc != 0:
+            _raise(rc)
+        self._prep_key = key
+        self._prep_ref = tab
+
+    def dirk_step_device(self, u_dev, t, dt):
+        """_dirk_step (src/nonlinear.py:239-296) on a device state, in place."""
+        st = self._new_stats()
+        rc = self.lib.irkg_dirk_step(self.h, ptr(u_dev), float(t), float(dt), C.byref(st))
+        self._check(rc, st)
+        return step_stats_from_c(st)
 
     def set_config(self, cfg):
         key = (cfg.variant, cfg.newton_rtol, cfg.newton_maxit, cfg.newton_abs_floor,

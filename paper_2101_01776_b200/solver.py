@@ -123,7 +123,8 @@ def step(sys, u, t, dt, tableau, cfg=SolverConfig(), prep=None):
     Returns ``(u_next, StepStats)``.
     """
     _check_sys(sys)
-    _sdirk_guard(tableau)
+    if str(tableau.family) in SDIRK_FAMILIES:  # src/nonlinear.py:304-306
+        return _dirk_step(sys, u, t, dt, tableau, cfg)
     prep = _prep_for(tableau, prep)
     ctx = context_for(sys)
     ctx.set_prep(prep)
@@ -135,6 +136,22 @@ def step(sys, u, t, dt, tableau, cfg=SolverConfig(), prep=None):
     uh = np.array(u, dtype=np.float64, copy=True, order="C")
     stats = ctx.step_host(uh, t, dt)
     return uh, stats
+
+
+def _dirk_step(sys, u, t, dt, tableau, cfg):
+    """Sequential stage solves of an SDIRK tableau on the device
+    (src/nonlinear.py:239-296): returns (u_next, StepStats) with
+    ``block_iterations`` keyed by stage."""
+    ctx = context_for(sys)
+    ctx.set_dirk_tableau(tableau)
+    ctx.set_config(cfg)
+    if _is_torch(u):
+        ud = as_device(u).clone()
+        stats = ctx.dirk_step_device(ud, t, dt)
+        return ud, stats
+    ud = as_device(np.asarray(u, dtype=np.float64)).clone()
+    stats = ctx.dirk_step_device(ud, t, dt)
+    return ud.cpu().numpy(), stats
 
 
 def integrate(sys, u0, t0, t_final, dt, tableau, cfg=SolverConfig(), snapshot_every=None):
@@ -150,11 +167,14 @@ def integrate(sys, u0, t0, t_final, dt, tableau, cfg=SolverConfig(), snapshot_ev
     nsteps = int(round(nsteps_f))
     if abs(nsteps_f - nsteps) > 1e-8 * max(1.0, abs(nsteps_f)):
         raise ConfigurationError(f"(t_final - t0)/dt = {nsteps_f} is not an integer step count")
-    _sdirk_guard(tableau)
-    prep = _prep_for(tableau)
+    dirk = str(tableau.family) in SDIRK_FAMILIES  # prep = None (src/nonlinear.py:355)
     ctx = context_for(sys)
-    ctx.set_prep(prep)
+    if dirk:
+        ctx.set_dirk_tableau(tableau)
+    else:
+        ctx.set_prep(_prep_for(tableau))
     ctx.set_config(cfg)
+    advance = ctx.dirk_step_device if dirk else ctx.step_device
     on_dev = _is_torch(u0)
     u = as_device(u0).clone()
     host = (lambda x: x.clone()) if on_dev else (lambda x: x.cpu().numpy())
@@ -164,7 +184,7 @@ def integrate(sys, u0, t0, t_final, dt, tableau, cfg=SolverConfig(), snapshot_ev
     for j in range(nsteps):
         t = t0 + j * dt
         try:
-            stats = ctx.step_device(u, t, dt)
+            stats = advance(u, t, dt)
         except StepFailureError as exc:
             exc.partial = IntegrationResult(times=np.array(times), states=states,
                                             step_stats=step_stats)

@@ -30,6 +30,7 @@ RADAU_IIA = "radau_iia"
 LOBATTO_IIIC = "lobatto_iiic"
 SDIRK_FAMILIES = ("sdirk1", "sdirk2", "sdirk3", "sdirk4")
 COLLOCATION_FAMILIES = (GAUSS, RADAU_IIA, LOBATTO_IIIC)
+_SDIRK_STAGES = {"sdirk1": 1, "sdirk2": 2, "sdirk3": 3, "sdirk4": 5}
 MAX_COLLOCATION_STAGES = 8
 
 _ALIASES = {
@@ -137,14 +138,19 @@ def _entry(family, s):
 def make_tableau(family, s=None):
     """Construct the Butcher tableau for ``(family, s)`` (src/tableau.py:329-361).
 
-    SDIRK baselines (src/tableau.py:283-326) are outside this engine's path
-    (the reference steps them stage by stage, src/nonlinear.py:239-296).
+    SDIRK baselines (src/tableau.py:283-326) have their stage count fixed by
+    the scheme (a mismatching ``s`` is a configuration error, 336-341); they
+    are stepped stage by stage (src/nonlinear.py:239-296, ``irkg_dirk_step``).
     """
     family = canonical_family(family)
     if family in SDIRK_FAMILIES:
-        raise ConfigurationError(
-            f"{family} is an SDIRK baseline; the device stage solver covers the "
-            "collocation families gauss / radau_iia / lobatto_iiic"
+        fixed = _SDIRK_STAGES[family]
+        if s is not None and int(s) != fixed:
+            raise ConfigurationError(f"{family} has s = {fixed}, got s = {s}")
+        doc = _entry(family, fixed)
+        return ButcherTableau(
+            family=doc["family"], s=fixed, a0=_arr(doc["a0"]), b0=_arr(doc["b0"]),
+            c0=_arr(doc["c0"]), order=int(doc["order"]),
         )
     if s is None:
         raise ConfigurationError(f"{family} requires an explicit stage count")
@@ -165,6 +171,11 @@ def prepare_stages(tableau):
     """A0^{-1}, its real Schur form and d[k,l,i] = q[i,k] q[i,l]
     (src/tableau.py:364-379), from the reference's own values."""
     fam = canonical_family(tableau.family)
+    if fam in SDIRK_FAMILIES:
+        raise ConfigurationError(
+            f"{tableau.family} is stepped stage by stage (src/nonlinear.py:239-296); "
+            "it has no prepared Schur data"
+        )
     doc = _entry(fam, int(tableau.s))
     if not np.array_equal(np.asarray(tableau.a0, dtype=float), _arr(doc["a0"])):
         raise ConfigurationError(

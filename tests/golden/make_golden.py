@@ -70,6 +70,18 @@ def dump_tableaux():
             ],
             "d": _hex(prep.d),
         }
+    # SDIRK baselines (src/tableau.py:283-326): coefficients only (the
+    # reference steps them with _dirk_step and never prepares them)
+    for fam in ("sdirk1", "sdirk2", "sdirk3", "sdirk4"):
+        tab = irkit.make_tableau(fam)
+        doc[f"{fam}:{tab.s}"] = {
+            "family": tab.family,
+            "s": tab.s,
+            "order": tab.order,
+            "a0": _hex(tab.a0),
+            "b0": _hex(tab.b0),
+            "c0": _hex(tab.c0),
+        }
     text = json.dumps(doc, indent=1, sort_keys=True)
     for path in (os.path.join(GOLD, "tableaux.json"),
                  os.path.join(ROOT, "paper_2101_01776_b200", "data", "tableaux.json")):
@@ -163,6 +175,20 @@ def run_configs():
     run_case("rad2d_linear", prob, u0, "radau_iia", 3, 0.01, 3, dict(variant=3, inner=4))
 
 
+def run_sdirk():
+    """integrate() with SDIRK tableaux: the reference's _dirk_step path
+    (src/nonlinear.py:239-296) on the config-0 problem and on 2-D Burgers."""
+    sp0 = baseline_config(0)
+    for fam, s in (("sdirk1", 1), ("sdirk2", 2), ("sdirk3", 3), ("sdirk4", 5)):
+        run_case(f"sdirk_cfg0_{fam}", sp0.problem, sp0.u0(), fam, s, sp0.dt, 3,
+                 dict(sp0.solver))
+    prob = GridProblem("burgers", (48, 48), nu=1e-2)
+    u0 = fourier_u0(prob.shape, 1, 6, 0.5, seed=11)
+    for fam, s in (("sdirk2", 2), ("sdirk4", 5)):
+        run_case(f"sdirk_burgers48_{fam}", prob, u0, fam, s, 2e-3, 3,
+                 dict(variant=3, inner=4, krylov_maxit=2000, restart=200))
+
+
 def run_transformed():
     """solve_transformed_system on advdiff-type linear stencils (every variant),
     mirroring tests/test_irk_core.py:152-167 of the reference."""
@@ -240,7 +266,7 @@ def run_dae():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tableaux", "transformed", "configs", "dae"]
+    which = sys.argv[1:] or ["tableaux", "transformed", "configs", "dae", "sdirk"]
     if "dae" in which:
         run_dae()
     if "tableaux" in which:
@@ -249,3 +275,5 @@ if __name__ == "__main__":
         run_transformed()
     if "configs" in which:
         run_configs()
+    if "sdirk" in which:
+        run_sdirk()

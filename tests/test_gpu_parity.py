@@ -312,10 +312,30 @@ def test_step_failure_error_carries_stats_and_partial():
     assert err.value.partial is not None and len(err.value.partial.states) == 1
 
 
-def test_sdirk_and_exact_inner_are_configuration_errors():
-    prob = GridProblem("nldiff", (8, 8))
-    with pytest.raises(pk.ConfigurationError):
-        pk.step(prob, np.zeros(64), 0.0, 1e-3, pk.make_tableau("gauss", 2), pk.SolverConfig())
+SDIRK_CASES = [c for c in case_names() if c.startswith("sdirk_")]
+
+
+@pytest.mark.parametrize("name", SDIRK_CASES)
+def test_sdirk_per_stage_counts_match_reference(name):
+    """The SDIRK baseline (src/nonlinear.py:239-296) on the device: Newton
+    counts per stage equal, Krylov counts per stage solve within +/-1."""
+    meta = load_case(name)
+    prob = grid_problem(meta)
+    tab = pk.make_tableau(meta["family"])
+    u = meta["u0"]
+    for j, want in enumerate(meta["steps"]):
+        u, got = pk.step(prob, u, j * meta["dt"], meta["dt"], tab, _solver(meta["solver"]))
+        assert got.newton_iterations == want["newton_iterations"]
+        assert got.jacobian_assemblies == want["jacobian_assemblies"]
+        assert sorted(got.block_iterations) == sorted(want["block_iterations"])
+        for stage, its in want["block_iterations"].items():
+            g = got.block_iterations[stage]
+            assert len(g) == len(its)
+            assert all(abs(a - b) <= 1 for a, b in zip(g, its)), (stage, g, its)
+        np.testing.assert_allclose(got.residual_history, want["residual_history"], rtol=1e-6,
+                                   atol=1e-9 * max(want["residual_history"]))
+    rel = np.linalg.norm(u - meta["u_final"]) / np.linalg.norm(meta["u_final"])
+    assert rel <= RTOL_U, rel
 
 
 # ------------------------------------------------- full-size properties

@@ -27,7 +27,7 @@ def test_tableau_table_is_the_golden_reference_table():
     with open(os.path.join(ROOT, "paper_2101_01776_b200", "data", "tableaux.json")) as fh:
         prod = json.load(fh)
     assert gold == prod
-    assert len(prod) == 23
+    assert len(prod) == 27  # 23 collocation tableaux + 4 SDIRK baselines
 
 
 @pytest.mark.parametrize("family,s", [("gauss", 2), ("gauss", 3), ("gauss", 5),
@@ -62,6 +62,10 @@ def test_tableau_bit_exact_against_reference_when_available():
         " (a.tableau.c0, b.tableau.c0), (a.a0inv, b.a0inv), (a.schur.q, b.schur.q), (a.schur.r, b.schur.r), (a.d, b.d)))\n"
         "    ok = ok and [(x.offset, x.size, x.eta, x.beta, x.phi) for x in a.blocks] == [(x.offset, x.size, x.eta, x.beta, x.phi) for x in b.blocks]\n"
         "    bad += [] if ok else [(fam, s)]\n"
+        "for fam in ('sdirk1', 'sdirk2', 'sdirk3', 'sdirk4'):\n"
+        "  a = irkit.make_tableau(fam); b = pk.make_tableau(fam)\n"
+        "  ok = a.s == b.s and a.order == b.order and all(np.array_equal(x, y) for x, y in ((a.a0, b.a0), (a.b0, b.b0), (a.c0, b.c0)))\n"
+        "  bad += [] if ok else [(fam, a.s)]\n"
         "print(json.dumps(bad))\n" % (src, ROOT)
     )
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True)
@@ -75,14 +79,32 @@ def test_tableau_errors():
         pk.make_tableau("gauss", 9)
     with pytest.raises(pk.ConfigurationError):
         pk.make_tableau("lobatto", 1)
-    with pytest.raises(pk.ConfigurationError):
-        pk.make_tableau("sdirk2")
+    with pytest.raises(pk.ConfigurationError):  # SDIRK stage counts are fixed
+        pk.make_tableau("sdirk4", 3)
+    with pytest.raises(pk.ConfigurationError):  # stepped stage by stage, never prepared
+        pk.prepare_stages(pk.make_tableau("sdirk2"))
     with pytest.raises(pk.ConfigurationError):
         pk.make_tableau("nope", 2)
     assert pk.gamma_star(3.0, np.sqrt(3.0)) == pytest.approx(4.0)
 
 
 # ----------------------------------------------------------- config
+
+
+def test_sdirk_tableaux_are_the_reference_values():
+    """make_tableau for the SDIRK baselines (src/tableau.py:283-341): fixed
+    stage counts, lower-triangular A0, stiffly accurate rows where the
+    reference builds them so."""
+    for fam, s in (("sdirk1", 1), ("sdirk2", 2), ("sdirk3", 3), ("sdirk4", 5)):
+        tab = pk.make_tableau(fam)
+        assert tab.s == s and tab.is_dirk
+        assert np.all(np.triu(tab.a0, 1) == 0.0)
+        np.testing.assert_allclose(tab.a0.sum(axis=1), tab.c0, atol=1e-14)
+        assert abs(tab.b0.sum() - 1.0) <= 1e-14
+    g = 1.0 - 1.0 / np.sqrt(2.0)
+    assert pk.make_tableau("sdirk2").a0[0, 0] == g
+    tab4 = pk.make_tableau("sdirk4")
+    assert np.array_equal(tab4.b0, tab4.a0[-1])
 
 
 def test_config_mirrors_reference_validation():

@@ -20,8 +20,17 @@ def run_oracle(meta):
     prob = grid_problem(meta)
     pd = build_problem(prob.kind, prob.shape, **prob.oracle_params())
     sysr = irk.OdeSystem(pd.dim, pd.rhs, pd.linearize_csr)
-    prep = otab.prepare(meta["family"], meta["s"])
     cfg = oracle_config(meta["solver"])
+    if meta["family"].startswith("sdirk"):  # the reference's _dirk_step route
+        tab = otab.dirk_tableau(meta["family"])
+        u = np.array(meta["u0"], dtype=float)
+        states, stats = [u.copy()], []
+        for j in range(meta["nsteps"]):
+            u, _, st = irk.dirk_step(sysr, u, j * meta["dt"], meta["dt"], tab, cfg)
+            states.append(u.copy())
+            stats.append(st)
+        return states, stats
+    prep = otab.prepare(meta["family"], meta["s"])
     return irk.integrate(sysr, meta["u0"], 0.0, meta["nsteps"] * meta["dt"], meta["dt"], prep, cfg)
 
 
