@@ -36,6 +36,11 @@ extern "C" {
 #define IRKG_ERR_BREAKDOWN -5      /* KrylovBreakdownError */
 #define IRKG_ERR_CUDA -6           /* CUDA / NCCL runtime failure */
 #define IRKG_ERR_INDEX -7          /* IndexViolationError (singular constraint block) */
+#define IRKG_ERR_SINGULAR -8       /* SingularMatrixError (exact inner solve: singular band) */
+
+/* irkg_solver.inner: damped-Jacobi sweeps (> 0) or IRKG_INNER_EXACT for the
+ * reference's default PrecondSpec(inner="exact") banded LU (1-D / 2-D, one rank) */
+#define IRKG_INNER_EXACT 0
 
 #define IRKG_MAX_STAGES 8
 #define IRKG_MAX_NEWTON 512
@@ -90,7 +95,7 @@ typedef struct {
   int restart;
   int gamma_mode;         /* 0 = star, 1 = eta, 2 = custom */
   double gamma_custom;
-  int inner;              /* damped-Jacobi sweeps (>0) */
+  int inner;              /* damped-Jacobi sweeps (>0), IRKG_INNER_EXACT = banded LU */
   int jacobian_refresh;   /* 0 = every, 1 = frozen */
   int variant0_stage;
 } irkg_solver;

@@ -24,6 +24,8 @@ ERR_STEP_FAILURE = -4
 ERR_BREAKDOWN = -5
 ERR_CUDA = -6
 ERR_INDEX = -7
+ERR_SINGULAR = -8
+INNER_EXACT = 0
 
 
 class Problem(C.Structure):

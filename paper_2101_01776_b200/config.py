@@ -18,10 +18,10 @@ class PrecondSpec:
     """Shift choice and inner-solver policy for the block preconditioners.
 
     ``inner`` is the number of damped-Jacobi sweeps (omega = 2/3) of each
-    ``(gamma*M - dt*L)`` inner solve.  The reference default ``"exact"``
-    (banded LU + SMW, src/sparsela.py:283-359) is accepted by the dataclass
-    for API compatibility but the device engine implements the Jacobi-k
-    mode only (exact LU is infeasible beyond ~256^2); pass an int.
+    ``(gamma*M - dt*L)`` inner solve, or the reference default ``"exact"``:
+    banded LU + SMW wrap correction (src/sparsela.py:283-359), on the device
+    for single-rank 1-D / 2-D grids (csrc/banded.cu; exact LU is
+    infeasible beyond ~256^2, where the parity contract pins ``inner=4``).
     """
 
     gamma_mode: object = "star"
@@ -75,11 +75,9 @@ def gamma_code(spec):
 
 
 def inner_sweeps(spec):
+    """irkg_solver.inner: Jacobi sweeps, or 0 (IRKG_INNER_EXACT) for the
+    reference's default banded-LU inner solves (1-D / 2-D grids, one rank)."""
     inner = spec.inner
     if inner == "exact":
-        raise ConfigurationError(
-            "PrecondSpec(inner='exact') (banded LU) is not implemented on the device; "
-            "use PrecondSpec(inner=k) damped-Jacobi sweeps (SURVEY 8c; the parity "
-            "contract pins inner=4)"
-        )
+        return 0
     return int(inner)

@@ -76,6 +76,20 @@ enum GhostRole {
   R_OP = 64      // operator fields
 };
 
+// Banded LU + SMW factor of one shifted operator (banded.cu)
+struct BandFactor {
+  int n = 0, kl = 0, ku = 0, ldab = 0, nb = 0;
+  double *ab = nullptr;     // ldab x n, column-major (LAPACK band layout)
+  int *piv = nullptr;
+  double *binvu = nullptr;  // n x nb: B^{-1} U
+  double *cap = nullptr;    // nb x nb LU of I + E^T B^{-1} U
+  int *cpiv = nullptr;
+  int *info = nullptr;
+  double *mid = nullptr;    // nb
+  double *wglob = nullptr;  // factor window when it does not fit in shared memory
+  size_t wsmem = 0;
+};
+
 struct KrylovOut {
   int iterations = 0;
   int converged = 0;
@@ -317,6 +331,12 @@ struct Engine {
   // dk == nullptr: leave y in Y (the Newton loop fuses dk = (Q R0) y into its update)
   void transformed_solve(double dt, const double *rhs, double *dk, irkg_step_stats *stats);
   void newton(const double *u, double *K, double t, double dt, irkg_step_stats *stats);
+  // banded.cu: exact inner solves (PrecondSpec(inner="exact"), cfg.inner == 0)
+  BandFactor bfac[2];
+  void band_factor(BandFactor &F, const Op &L, double alpha, double dt);
+  void band_solve(const BandFactor &F, double *b, long long ldb, int nrhs, const GCtrl *skip);
+  void band_apply(const BandFactor &F, double *x, const GCtrl *skip);
+  void precond_exact(const BlockSpec &B, const VecIn &vin, double *z, const GCtrl *skip);
   // dirk.cu: sequential stage solves of an (S)DIRK tableau (src/nonlinear.py:239-296)
   void dirk_step(double *u, double t, double dt, irkg_step_stats *stats);
 };

@@ -792,6 +792,10 @@ void Engine::jacobi_chain(const Op &L, double alpha, double dt, int inner, const
 
 void Engine::precond(const BlockSpec &B, const void *vin_p, double *z, const GCtrl *skip) {
   VecIn vin = *static_cast<const VecIn *>(vin_p);
+  if (B.inner == IRKG_INNER_EXACT) {  // factors prepared by gmres() (banded.cu)
+    precond_exact(B, vin, z, skip);
+    return;
+  }
   if (slab()) {
     // the input must be a fixed pointer here (the multi-rank loop resolves
     // slot j on the host); exchange the halves' boundary planes

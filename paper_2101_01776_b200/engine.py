@@ -16,6 +16,7 @@ import numpy as np
 from . import _lib
 from .config import gamma_code, inner_sweeps
 from .errors import (
+    SingularMatrixError,
     ConfigurationError,
     IndexViolationError,
     KrylovBreakdownError,
@@ -61,6 +62,8 @@ def _raise(rc, stats_c=None, fail_res=None):
         raise KrylovBreakdownError(msg)
     if rc == _lib.ERR_INDEX:
         raise IndexViolationError(msg)
+    if rc == _lib.ERR_SINGULAR:
+        raise SingularMatrixError(msg)
     raise RuntimeError(f"irkg CUDA failure: {msg}")
 
 

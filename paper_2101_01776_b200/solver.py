@@ -273,18 +273,16 @@ def precond_block2x2(sys2: Block2x2System, spec: PrecondSpec, r):
 
 
 class ShiftedSolver:
-    """Applies ``(alpha*I - dt*L)^{-1}`` by k damped-Jacobi sweeps
-    (src/irk_core.py:103-123)."""
+    """Applies ``(alpha*I - dt*L)^{-1}`` exactly (banded LU + SMW, the
+    reference default) or by k damped-Jacobi sweeps (src/irk_core.py:103-123)."""
 
-    def __init__(self, alpha, mass, lmat: OperatorField, dt, inner=4):
+    def __init__(self, alpha, mass, lmat: OperatorField, dt, inner="exact"):
         if mass is not None:
             raise ConfigurationError("identity mass only")
-        if inner == "exact":
-            inner_sweeps(PrecondSpec(inner="exact"))
         self.alpha = float(alpha)
         self.lmat = lmat
         self.dt = float(dt)
-        self.inner = int(inner)
+        self.inner = inner_sweeps(PrecondSpec(inner=inner))
 
     def solve(self, r):
         rd = as_device(r)

@@ -55,6 +55,54 @@ def test_integrate_matches_reference_golden(name):
         assert got.converged
 
 
+def test_config0_exact_inner_mode_matches_reference_golden():
+    """configs[0] in the reference's DEFAULT inner mode, PrecondSpec(inner=
+    "exact") (banded LU + SMW, src/sparsela.py:283-359) on the device
+    (csrc/banded.cu): per-block Krylov counts equal the reference's exactly,
+    final u within 1e-10."""
+    meta = load_case("cfg0_full_exact")
+    prob = grid_problem(meta)
+    tab = pk.make_tableau("gauss", 2)
+    sv = dict(meta["solver"], inner="exact")
+    cfg = pk.SolverConfig(variant=sv["variant"], newton_rtol=sv["newton_rtol"],
+                          newton_maxit=sv["newton_maxit"], krylov_rtol=sv["krylov_rtol"],
+                          krylov_maxit=sv["krylov_maxit"], restart=sv["restart"],
+                          precond=pk.PrecondSpec(inner="exact"))
+    res = pk.integrate(prob, meta["u0"], 0.0, meta["nsteps"] * meta["dt"], meta["dt"], tab, cfg)
+    rel = np.linalg.norm(res.u_final - meta["u_final"]) / np.linalg.norm(meta["u_final"])
+    assert rel <= RTOL_U, rel
+    for got, want in zip(res.step_stats, meta["steps"]):
+        assert got.newton_iterations == want["newton_iterations"]
+        assert got.block_iterations == want["block_iterations"]
+
+
+def test_exact_shifted_solve_is_exact():
+    """ShiftedSolver(inner="exact") on 1-D and 2-D periodic operators (with
+    the out-of-band wrap through SMW): residual at rounding level, against a
+    dense solve of the same operator assembled by the oracle."""
+    from oracle.problems import build_problem
+
+    for kind, shape, kw in (("burgers", (40, 24), dict(nu=1e-2)), ("nldiff", (32, 32), {}),
+                            ("rad", (50,), dict(nu=1e-2, c=0.7, lam=-1.0))):
+        prob = GridProblem(kind, shape, **kw)
+        rng = np.random.default_rng(3)
+        U = rng.standard_normal(prob.dim)
+        f = pk.OperatorField.linearize(prob, U[None, :])
+        r = rng.standard_normal(prob.dim)
+        x = pk.ShiftedSolver(1.7, None, f, 0.05, inner="exact").solve(r)
+        pd = build_problem(prob.kind, prob.shape, **prob.oracle_params())
+        A = 1.7 * np.eye(prob.dim) - 0.05 * pd.linearize_csr(U, 0.0).toarray()
+        xd = np.linalg.solve(A, r)
+        assert np.linalg.norm(x - xd) <= 1e-12 * np.linalg.norm(xd), kind
+
+
+def test_exact_inner_mode_limits_are_configuration_errors():
+    prob = GridProblem("nldiff", (8, 8, 8))
+    f = pk.OperatorField.linearize(prob, np.ones((1, 512)))
+    with pytest.raises(pk.ConfigurationError):
+        pk.ShiftedSolver(2.0, None, f, 1e-2, inner="exact").solve(np.ones(512))
+
+
 def test_config0_counts_exact_per_block():
     meta = load_case("cfg0_full")
     prob = grid_problem(meta)
@@ -266,8 +314,6 @@ def test_block_gmres_maxit_and_zero_rhs():
 def test_transformed_solve_matches_reference_all_variants():
     prob = GridProblem("rad", (24,), nu=0.01, c=1.0)
     for case in load_transformed():
-        if case["inner"] == "exact":
-            continue
         s = case["s"]
         tab = pk.make_tableau(case["family"], s)
         prep = pk.prepare_stages(tab)
@@ -275,8 +321,8 @@ def test_transformed_solve_matches_reference_all_variants():
         rhs = rng.standard_normal((s, 24))
         lin = pk.StageLinearization(prob, np.zeros(24), np.zeros((s, 24)), 0.05)
         k, stats = pk.solve_transformed_system(
-            prep, lin, case["variant"], case["dt"], rhs, precond=pk.PrecondSpec(inner=4),
-            krylov_rtol=1e-12, krylov_maxit=400)
+            prep, lin, case["variant"], case["dt"], rhs,
+            precond=pk.PrecondSpec(inner=case["inner"]), krylov_rtol=1e-12, krylov_maxit=400)
         got = [[o, r.iterations] for o, r in stats.reports]
         assert [g[0] for g in got] == [w[0] for w in case["reports"]]
         for g, w in zip(got, case["reports"]):

@@ -127,11 +127,13 @@ def test_config_mirrors_reference_validation():
             cfg.restart) == (3, 1e-9, 30, 1e-5, 200, 200)
 
 
-def test_exact_inner_is_a_loud_configuration_error():
+def test_inner_mode_codes():
+    """PrecondSpec.inner -> irkg_solver.inner: the reference default "exact"
+    (banded LU, IRKG_INNER_EXACT = 0) or the Jacobi sweep count."""
+    from paper_2101_01776_b200 import _lib
     from paper_2101_01776_b200.config import inner_sweeps
 
-    with pytest.raises(pk.ConfigurationError):
-        inner_sweeps(pk.PrecondSpec())
+    assert inner_sweeps(pk.PrecondSpec()) == _lib.INNER_EXACT == 0
     assert inner_sweeps(pk.PrecondSpec(inner=4)) == 4
 
 
