@@ -41,7 +41,9 @@ def main():
 
     def probe(ph, j):
         out = C.c_double()
+        torch.cuda.nvtx.range_push(f"probe{ph}")  # (ncu --nvtx --nvtx-include "probe6/")
         rc = lib.irkg_probe_phase(h, ph, j, args.reps, C.byref(out))
+        torch.cuda.nvtx.range_pop()
         if rc != 0:
             raise RuntimeError(lib.irkg_last_error().decode())
         return out.value
