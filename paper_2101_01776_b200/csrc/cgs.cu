@@ -163,6 +163,7 @@ struct TileArgs {
   const double *cs;
   double *red;
   const char *maps;  // tensor maps of this tile height (null: 1-D copies)
+  int rev;           // walk the row tiles last-to-first (L2 reuse between sweeps)
 };
 
 // Tile issue, out of line: one copy of the code for every tile height and
@@ -344,16 +345,21 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
   const int G = A.G, ntiles = A.ntiles;
   const int t0 = blockIdx.x;
   const int NST = A.nst;
+  // logical tile t -> row tile; consecutive sweeps walk the rows in opposite
+  // directions so each starts on the tiles the previous one touched last
+  // (still in L2) instead of the ones LRU evicted first
+  auto ph = [&](int t) { return A.rev ? ntiles - 1 - t : t; };
   // PDL prologue: the basis slots were written >= 2 launches back, so their
   // part of the first NST tiles goes out while the predecessor drains; w
   // (and the coefficients) only after pdl_wait()
   for (int i = 0; i < NST; ++i)
-    if (t0 + i * G < ntiles && tile_full<TRC>(A, t0 + i * G))
-      tile_issue<TRC>(A, t0 + i * G, i, false);
+    if (t0 + i * G < ntiles && tile_full<TRC>(A, ph(t0 + i * G)))
+      tile_issue<TRC>(A, ph(t0 + i * G), i, false);
   pdl_wait();
   fence_proxy_async_global();  // w was written through the generic proxy
   for (int i = 0; i < NST; ++i)
-    if (t0 + i * G < ntiles && tile_full<TRC>(A, t0 + i * G)) tile_issue_w<TRC>(A, t0 + i * G, i);
+    if (t0 + i * G < ntiles && tile_full<TRC>(A, ph(t0 + i * G)))
+      tile_issue_w<TRC>(A, ph(t0 + i * G), i);
   if (MODE != CGS_DOT)
     for (int l = threadIdx.x; l < A.L; l += CGS_BS) const_cast<double *>(A.cs)[l] = W.alpha[l] * cin[l];
   __syncthreads();
@@ -362,10 +368,10 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
   int s = 0;
   uint32_t phase = 0;
   for (int t = t0; t < ntiles; t += G) {
-    const int r0 = t * TRC;
+    const int r0 = ph(t) * TRC;
     const int rows = min(TRC, A.n - r0);
     double *buf = A.ring + (size_t)s * (A.L + 1) * TRC;
-    if (tile_full<TRC>(A, t)) {
+    if (tile_full<TRC>(A, ph(t))) {
       while (!mbar_try_wait(&A.bars[s], phase)) {
       }
     } else {
@@ -376,7 +382,7 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
     __syncthreads();  // stage s consumed
     {
       const int tn = t + NST * G;
-      if (tn < ntiles && tile_full<TRC>(A, tn)) tile_issue<TRC>(A, tn, s);
+      if (tn < ntiles && tile_full<TRC>(A, ph(tn))) tile_issue<TRC>(A, ph(tn), s);
     }
     if (++s == NST) {
       s = 0;
@@ -406,6 +412,8 @@ __global__ void __launch_bounds__(CGS_BS, 2)
     return;
   }
   const int L = ctrl->j + 1;
+  const int cgs_rev_mask = trmax >> 16;
+  trmax &= 0xffff;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double *out = (MODE == CGS_UPD_NORM) ? V + (size_t)L * pitch : wout;
   // tile rows: largest power of two with (L+1)*TR <= stage, within [32, 1024]
@@ -426,7 +434,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   __syncthreads();
 
   TileArgs A{n, L, G, ntiles, V, pitch, win, out, sm, nst, bars, cs, red,
-             TR <= 256 ? vmaps : nullptr};
+             TR <= 256 ? vmaps : nullptr, (cgs_rev_mask >> MODE) & 1};
   double nrm = 0.0;
   double acc[CGS_Q];
 #pragma unroll
@@ -561,7 +569,13 @@ static const char *cgs_maps(const void *vmaps) {
 
 static int cgs_trmax() {
   static int v = -1;
-  if (v < 0) { const char *e = getenv("IRKG_CGS_TRMAX"); v = e ? atoi(e) : 1024; }
+  if (v < 0) {
+    const char *e = getenv("IRKG_CGS_TRMAX");
+    v = e ? atoi(e) : 1024;
+    // bit m: sweep m (DOT, UPD_DOT, UPD_NORM) walks the row tiles backwards
+    const char *r = getenv("IRKG_CGS_REV");
+    v |= (r ? atoi(r) : 2) << 16;
+  }
   return v;
 }
 
