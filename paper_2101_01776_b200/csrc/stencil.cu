@@ -414,36 +414,109 @@ __global__ void __launch_bounds__(BPW * 32)
     for (int i = 0; i < BRING - 1; ++i) issue_row(y0 - 1 + i);  // rows y0-1 .. y0+BRING-3
     for (int s = y0; s < y1; ++s) {
       cp_async_wait<BRING - 4>();  // rows up to s+1 have landed (s+2 .. s+BRING-3 may pend)
-      Nb x1[2], a1n[2];
-      field_nb(0, s, x1[0], x1[1]);
-      field_nb(1, s, a1n[0], a1n[1]);
-      double top[2], bot[2];
-      if (SIZE == 1) {
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-          top[c] = eta * x1[c].c - dt * lx_nb<KIND, 2>(g, kp, a1n[c], l1.sigma, x1[c]);
-      } else {
-        Nb x2[2], a2n[2];
-        field_nb(2, s, x2[0], x2[1]);
-        field_nb(3, s, a2n[0], a2n[1]);
+      // The operator is linear in its coefficient fields, so the four
+      // stencil applications of a 2x2 block collapse into two per row:
+      //   top = eta z1 + phi z2 - dt [ K(q_t) + sig-part(r_t) ],
+      //   q_t = a1 z1 + c12 z2,  r_t = s1 z1 + s12 z2   (bot likewise)
+      // with K the kind's coefficient stencil (Lap for nldiff, -Dsum for
+      // burgers, the centre for rad) and the sigma part nu Lap (+ c Dsum).
+      constexpr bool CP = (KIND != KIND_RAD);  // coefficients enter the stencil
+      const double s1 = l1.sigma, s2 = SIZE == 2 ? l2.sigma : 0.0;
+      const double s12 = h12 ? c12.sigma : 0.0, s21 = h21 ? c21.sigma : 0.0;
+      auto combo = [&](int t, double (&qt)[2], double (&rt)[2], double (&qb)[2],
+                       double (&rb)[2]) {
+        const double2 z1 = rd(0, t), A1 = rd(1, t);
+        const double zz1[2] = {z1.x, z1.y}, aa1[2] = {A1.x, A1.y};
+        double zz2[2] = {0.0, 0.0}, aa2[2] = {0.0, 0.0}, cc12[2] = {0.0, 0.0},
+               cc21[2] = {0.0, 0.0};
+        if (SIZE == 2) {
+          const double2 z2 = rd(2, t), A2 = rd(3, t);
+          zz2[0] = z2.x;
+          zz2[1] = z2.y;
+          aa2[0] = A2.x;
+          aa2[1] = A2.y;
+          if (h12) {
+            const double2 c = rd(4, t);
+            cc12[0] = c.x;
+            cc12[1] = c.y;
+          }
+          if (h21) {
+            const double2 c = rd(5, t);
+            cc21[0] = c.x;
+            cc21[1] = c.y;
+          }
+        }
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          top[c] = eta * x1[c].c - dt * lx_nb<KIND, 2>(g, kp, a1n[c], l1.sigma, x1[c]) +
-                   phi * x2[c].c;
-          bot[c] = -(beta * beta / phi) * x1[c].c + eta * x2[c].c -
-                   dt * lx_nb<KIND, 2>(g, kp, a2n[c], l2.sigma, x2[c]);
+          qt[c] = aa1[c] * zz1[c];
+          rt[c] = s1 * zz1[c];
+          if (SIZE == 2) {
+            if (h12) qt[c] += cc12[c] * zz2[c];
+            rt[c] += s12 * zz2[c];
+            qb[c] = aa2[c] * zz2[c];
+            if (h21) qb[c] += cc21[c] * zz1[c];
+            rb[c] = s2 * zz2[c] + s21 * zz1[c];
+          }
         }
-        if (h12) {
-          Nb cn[2];
-          field_nb(4, s, cn[0], cn[1]);
+      };
+      double qtm[2], rtm[2], qbm[2], rbm[2], qtc[2], rtc[2], qbc[2], rbc[2], qtp[2], rtp[2],
+          qbp[2], rbp[2];
+      combo(s - 1, qtm, rtm, qbm, rbm);
+      combo(s, qtc, rtc, qbc, rbc);
+      combo(s + 1, qtp, rtp, qbp, rbp);
+      // x-neighbours of a row-s combination (lane-1's second / lane+1's first column)
+      auto lap = [&](const double (&m)[2], const double (&c)[2], const double (&p)[2], double out[2]) {
+        const double l = __shfl_sync(0xffffffffu, c[1], (lane + 31) & 31);
+        const double r = __shfl_sync(0xffffffffu, c[0], (lane + 1) & 31);
+        out[0] = g.ih2[0] * (l + c[1] - 2.0 * c[0]) + g.ih2[1] * (m[0] + p[0] - 2.0 * c[0]);
+        out[1] = g.ih2[0] * (c[0] + r - 2.0 * c[1]) + g.ih2[1] * (m[1] + p[1] - 2.0 * c[1]);
+      };
+      auto dsum = [&](const double (&m)[2], const double (&c)[2], const double (&p)[2], double out[2]) {
+        const double l = __shfl_sync(0xffffffffu, c[1], (lane + 31) & 31);
+        const double r = __shfl_sync(0xffffffffu, c[0], (lane + 1) & 31);
+        out[0] = g.i2h[0] * (c[1] - l) + g.i2h[1] * (p[0] - m[0]);
+        out[1] = g.i2h[0] * (r - c[0]) + g.i2h[1] * (p[1] - m[1]);
+      };
+      // L-part of one block row from its two combinations
+      auto lpart = [&](const double (&qm)[2], const double (&qc)[2], const double (&qp)[2],
+                       const double (&rm)[2], const double (&rc)[2], const double (&rp)[2],
+                       double out[2]) {
+        if (KIND == KIND_NLDIFF) {
+          lap(qm, qc, qp, out);
+        } else if (KIND == KIND_BURGERS) {
+          double d[2], l[2];
+          dsum(qm, qc, qp, d);
+          lap(rm, rc, rp, l);
 #pragma unroll
-          for (int c = 0; c < 2; ++c) top[c] -= dt * lx_nb<KIND, 2>(g, kp, cn[c], c12.sigma, x2[c]);
+          for (int c = 0; c < 2; ++c) out[c] = -d[c] + kp.nu * l[c];
+        } else {
+          double d[2], l[2];
+          dsum(rm, rc, rp, d);
+          lap(rm, rc, rp, l);
+#pragma unroll
+          for (int c = 0; c < 2; ++c) out[c] = (kp.nu * l[c] + kp.c * d[c]) + qc[c];
         }
-        if (h21) {
-          Nb cn[2];
-          field_nb(5, s, cn[0], cn[1]);
+        (void)CP;
+      };
+      double top[2], bot[2];
+      {
+        const double2 z1 = rd(0, s);
+        const double zz1[2] = {z1.x, z1.y};
+        double lt[2];
+        lpart(qtm, qtc, qtp, rtm, rtc, rtp, lt);
+        if (SIZE == 1) {
 #pragma unroll
-          for (int c = 0; c < 2; ++c) bot[c] -= dt * lx_nb<KIND, 2>(g, kp, cn[c], c21.sigma, x1[c]);
+          for (int c = 0; c < 2; ++c) top[c] = eta * zz1[c] - dt * lt[c];
+        } else {
+          const double2 z2 = rd(2, s);
+          const double zz2[2] = {z2.x, z2.y};
+          double lb[2];
+          lpart(qbm, qbc, qbp, rbm, rbc, rbp, lb);
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            top[c] = (eta * zz1[c] + phi * zz2[c]) - dt * lt[c];
+            bot[c] = (-(beta * beta / phi) * zz1[c] + eta * zz2[c]) - dt * lb[c];
+          }
         }
       }
       if (valid) {
