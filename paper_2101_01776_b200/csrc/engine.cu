@@ -111,6 +111,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   if (const char *e = getenv("IRKG_PDL")) use_pdl = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_CARVEOUT")) use_carveout = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_SLAB_BATCH")) slab_batch = atoi(e) > 0 ? atoi(e) : 1;
+  if (const char *e = getenv("IRKG_GRAPH_UNROLL")) graph_unroll = atoi(e) > 0 ? atoi(e) : 1;
   if (const char *e = getenv("IRKG_JWPS")) jwarps_per_sm = atoi(e) > 0 ? atoi(e) : 12;
   if (const char *e = getenv("IRKG_STRIP_OP")) strip_op = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_BOP_WPS")) bop_wps = atoi(e) > 0 ? atoi(e) : 12;
@@ -300,8 +301,8 @@ void Engine::drop_graphs() {
 // conditional body).
 Engine::CycleGraph &Engine::cycle_graph(const BlockSpec &B, long long n, bool loop) {
   char key[512];
-  snprintf(key, sizeof key, "%c|%d|%a|%a|%a|%a|%a|%d|%p|%a|%d|%p|%a|%d|%p|%a|%d|%p|%a|%d|%lld|%p|%d",
-           loop ? 'W' : 'S', B.size, B.eta, B.beta, B.phi, B.gamma, B.dt, B.inner,
+  snprintf(key, sizeof key, "%c%d|%d|%a|%a|%a|%a|%a|%d|%p|%a|%d|%p|%a|%d|%p|%a|%d|%p|%a|%d|%lld|%p|%d",
+           loop ? 'W' : 'S', loop ? graph_unroll : 1, B.size, B.eta, B.beta, B.phi, B.gamma, B.dt, B.inner,
            (const void *)B.l1.a, B.l1.sigma, B.l1.present, (const void *)B.l2.a, B.l2.sigma,
            B.l2.present, (const void *)B.c12.a, B.c12.sigma, B.c12.present,
            (const void *)B.c21.a, B.c21.sigma, B.c21.present, n, (void *)V, vcap);
@@ -334,7 +335,10 @@ Engine::CycleGraph &Engine::cycle_graph(const BlockSpec &B, long long n, bool lo
   cond_active = loop;
   cond_handle = cg.h;
   try {
-    arnoldi_iteration(B, n);
+    // the WHILE body holds `graph_unroll` Arnoldi steps: the conditional
+    // re-launch of the body costs several us per trip, and a step after the
+    // exit test fired is inert (every kernel checks cycle_done)
+    for (int u = 0; u < (loop ? graph_unroll : 1); ++u) arnoldi_iteration(B, n);
   } catch (...) {
     cond_active = false;
     stream = saved;
@@ -437,7 +441,7 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
       // (no host read here: the counters are settled after the cycle end)
       CycleGraph &cg = cycle_graph(B, n, true);
       check(cudaGraphLaunch(cg.ex, stream), "cudaGraphLaunch");
-      graph_body_kernels = cg.body_kernels;
+      graph_body_kernels = cg.body_kernels / graph_unroll;  // per Arnoldi step
     } else {
       for (int it = 0; it < m; ++it) {
         if (timing) check(cudaEventRecord(evp[0], stream));
@@ -715,6 +719,10 @@ __global__ void k_probe_setj(GCtrl *c, int j, int m) {
   c->k = j + 1;
   c->cycle_done = 0;
   c->converged = 0;
+  c->total_it = 0;        // (phase 12: the cycle runs to m)
+  c->maxit = 1 << 30;
+  c->rtol = 0.0;
+  c->breakdown = 0;
 }
 
 double Engine::probe_phase(int phase, int j, int reps) {
@@ -725,7 +733,8 @@ double Engine::probe_phase(int phase, int j, int reps) {
   VecIn vslot{V, vpitch, ctrl_dev, W.alpha};
   max_carveout((const void *)k_probe_setj);
   auto one = [&]() {
-    k_probe_setj<<<1, 1, 0, stream>>>(ctrl_dev, j, vcap);
+    // (phase 12: exactly 8 steps j .. j+7 of the WHILE graph)
+    k_probe_setj<<<1, 1, 0, stream>>>(ctrl_dev, j, phase == 12 ? std::min(vcap, j + 8) : vcap);
     switch (phase) {
       case 0: precond(B, &vslot, zbuf, ctrl_dev); break;
       case 1: jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vslot, 0, nullptr, 0.0, zbuf, ctrl_dev); break;
@@ -747,6 +756,11 @@ double Engine::probe_phase(int phase, int j, int reps) {
       }
       case 10: vcombine(n, W.c1, ubuf); break;
       case 11: backsolve(); break;
+      case 12: {  // the WHILE cycle graph from index j to the end of the cycle (m = vcap)
+        CycleGraph &cg = cycle_graph(B, n, true);
+        check(cudaGraphLaunch(cg.ex, stream), "cudaGraphLaunch");
+        break;
+      }
       default: throw SolveError(IRKG_ERR_VALUE, "probe: unknown phase");
     }
   };

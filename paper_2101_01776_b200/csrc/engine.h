@@ -213,7 +213,8 @@ struct Engine {
   void cgs_slab(long long n);  // CGS2 with all-reduces between sweeps (multi-rank)
   void arnoldi_iteration_slab(const BlockSpec &B, long long n, int j_host = -1);
   double *halo_pack = nullptr;
-  int slab_batch = 4;  // multi-rank Arnoldi steps launched per host check (IRKG_SLAB_BATCH)  // packed boundary planes of basis slot j (2 halves x lo/hi)
+  int slab_batch = 4;
+  int graph_unroll = 2;  // Arnoldi steps per WHILE-body trip (IRKG_GRAPH_UNROLL)  // multi-rank Arnoldi steps launched per host check (IRKG_SLAB_BATCH)  // packed boundary planes of basis slot j (2 halves x lo/hi)
   // dae.cu (vorticity/streamfunction DAE, reordered mode)
   bool dae = false;
   double h2 = 0.0;

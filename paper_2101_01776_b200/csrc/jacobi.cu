@@ -421,10 +421,11 @@ struct JacCoef {
   double pym, pyp;
   double xx, xy;      // O x += xx (x_l + x_r) + xy (x_m + x_p)   (symmetric part)
   double xxa, xya;    // O x += xxa (x_r - x_l) + xya (x_p - x_m) (rad: advective)
+  double xym, xyp;    // the y-terms regrouped: xym x_m + xyp x_p
 };
 
 template <int KIND, int K>
-__global__ void __launch_bounds__(JPW * 32)
+__global__ void __launch_bounds__(JPW * 32, 3)
     k_jacobi_sp2d(Grid g, Op L, JacCoef jc, VecIn vin, int in_off, FRef zcr, double cpl,
                   double *__restrict__ x_out, int span, int strips, int nwarps, GCtrl *flag_ctrl,
                   const GCtrl *skip) {
@@ -562,28 +563,33 @@ __global__ void __launch_bounds__(JPW * 32)
       }
       const double *xm = XW[m - 1][0], *xc = XW[m - 1][1], *xp = XW[m - 1][2];
       const double *pm = PW[m - 1][0], *pc = PW[m - 1][1], *pp = PW[m - 1][2];
-      // x-neighbours: lane-1's second column, lane+1's first column
-      double ox[2];
+      // x-neighbours: lane-1's second column, lane+1's first column.  The
+      // rows produced this step (xp, pp: sweep m-1's newest) enter last, so
+      // the per-step dependency chain through the K sweeps is three FMAs and
+      // a multiply per sweep; everything else is off the chain.
+      double off[2] = {0.0, 0.0};
       if (USE_P) {
         const double pl = shfl_up1(pc[1]), pr = shfl_dn1(pc[0]);
-        ox[0] = jc.pxl * pl + jc.pxr * pc[1] + jc.pym * pm[0] + jc.pyp * pp[0];
-        ox[1] = jc.pxl * pc[0] + jc.pxr * pr + jc.pym * pm[1] + jc.pyp * pp[1];
-      } else {
-        ox[0] = ox[1] = 0.0;
+        off[0] = jc.pxl * pl + jc.pxr * pc[1] + jc.pym * pm[0];
+        off[1] = jc.pxl * pc[0] + jc.pxr * pr + jc.pym * pm[1];
       }
       if (USE_XS) {
         const double xl = shfl_up1(xc[1]), xr = shfl_dn1(xc[0]);
-        ox[0] += jc.xx * (xl + xc[1]) + jc.xy * (xm[0] + xp[0]);
-        ox[1] += jc.xx * (xc[0] + xr) + jc.xy * (xm[1] + xp[1]);
+        off[0] += jc.xx * (xl + xc[1]) + jc.xym * xm[0];
+        off[1] += jc.xx * (xc[0] + xr) + jc.xym * xm[1];
         if (KIND == KIND_RAD) {
-          ox[0] += jc.xxa * (xc[1] - xl) + jc.xya * (xp[0] - xm[0]);
-          ox[1] += jc.xxa * (xr - xc[0]) + jc.xya * (xp[1] - xm[1]);
+          off[0] += jc.xxa * (xc[1] - xl);
+          off[1] += jc.xxa * (xr - xc[0]);
         }
       }
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const double cc = CONST_D ? jc.c : CW[K - m][c];
-        xn[c] = (jc.om1 * xc[c] + RW[K - m][c]) - cc * ox[c];
+        const double base = jc.om1 * xc[c] + RW[K - m][c];
+        double ox = off[c];
+        if (USE_XS) ox = fma(jc.xyp, xp[c], ox);
+        if (USE_P) ox = fma(jc.pyp, pp[c], ox);
+        xn[c] = fma(-cc, ox, base);
         pn[c] = (USE_P && m < K) ? AW[K - m][c] * xn[c] : 0.0;
       }
     }
@@ -670,6 +676,8 @@ bool Engine::jacobi_chain_fused(const Op &L, double alpha, double dt, int inner,
         jc.xxa = -dt * sig * kp.c * grid.i2h[0];
         jc.xya = -dt * sig * kp.c * grid.i2h[1];
       }
+      jc.xym = jc.xy - jc.xya;
+      jc.xyp = jc.xy + jc.xya;
       static bool attr = false;  // one per instantiation
       if (!attr) {
         check(cudaFuncSetAttribute((const void *)k_jacobi_sp2d<KIND_, decltype(KK)::value>,

@@ -91,10 +91,6 @@ __device__ __forceinline__ Nb gather(const Win &w, const double *f, int p, const
   return n;
 }
 
-__device__ __forceinline__ int wrap_plane(int s, int NS) {
-  return s < 0 ? s + NS : (s >= NS ? s - NS : s);
-}
-
 __device__ __forceinline__ double wsum2(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -39,10 +39,10 @@ def main():
     torch.cuda.synchronize()
     lib, h = ctx.lib, ctx.h
 
-    def probe(ph, j):
+    def probe(ph, j, reps=None):
         out = C.c_double()
         torch.cuda.nvtx.range_push(f"probe{ph}")  # (ncu --nvtx --nvtx-include "probe6/")
-        rc = lib.irkg_probe_phase(h, ph, j, args.reps, C.byref(out))
+        rc = lib.irkg_probe_phase(h, ph, j, reps or args.reps, C.byref(out))
         torch.cuda.nvtx.range_pop()
         if rc != 0:
             raise RuntimeError(lib.irkg_last_error().decode())
@@ -55,6 +55,11 @@ def main():
     for name, ph in [("precond (2 chains)", 0), ("jacobi chain 1", 1), ("jacobi chain 2", 2),
                      ("block operator", 3), ("stage mix (s,N)", 9), ("backsolve", 11)]:
         print(f"{name:22s} {probe(ph, 4) - pin:8.2f} us")
+    # graph mode: 8 steps j0..j0+7 of the captured WHILE loop (exit test
+    # disabled on the stale probe state), per Arnoldi step
+    for j0 in (0, 8, 16, 32, 100, 180):
+        g = probe(12, j0, reps=5)
+        print(f"graph-mode Arnoldi steps j={j0}..{j0 + 7}: {g / 8:8.2f} us/step")
     print(" j   cgs2(3 sweeps) us   GB/s(alg)   DOT / UPD_DOT / UPD_NORM us   arnoldi step us   x+=Vy us")
     for j in [int(x) for x in args.js.split(",")]:
         c = probe(6, j) - pin
