@@ -41,6 +41,9 @@ extern "C" {
 /* irkg_solver.inner: damped-Jacobi sweeps (> 0) or IRKG_INNER_EXACT for the
  * reference's default PrecondSpec(inner="exact") banded LU (1-D / 2-D, one rank) */
 #define IRKG_INNER_EXACT 0
+/* ... or IRKG_INNER_MG: one geometric-multigrid V-cycle per inner solve
+ * (beyond the reference; 2-D grids, one rank) */
+#define IRKG_INNER_MG -1
 
 #define IRKG_MAX_STAGES 8
 #define IRKG_MAX_NEWTON 512
@@ -95,7 +98,7 @@ typedef struct {
   int restart;
   int gamma_mode;         /* 0 = star, 1 = eta, 2 = custom */
   double gamma_custom;
-  int inner;              /* damped-Jacobi sweeps (>0), IRKG_INNER_EXACT = banded LU */
+  int inner;              /* Jacobi sweeps (>0), IRKG_INNER_EXACT (banded LU), IRKG_INNER_MG */
   int jacobian_refresh;   /* 0 = every, 1 = frozen */
   int variant0_stage;
 } irkg_solver;

@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libirkg.so")
-SOURCES = ["kernels.cu", "cgs.cu", "stencil.cu", "jacobi.cu", "dae.cu", "comm.cu", "dirk.cu", "banded.cu", "engine.cu"]
+SOURCES = ["kernels.cu", "cgs.cu", "stencil.cu", "jacobi.cu", "dae.cu", "comm.cu", "dirk.cu", "banded.cu", "mg.cu", "engine.cu"]
 HEADERS = ["kinds.cuh", "kernels.cuh", "engine.h", os.path.join("..", "..", "include", "irkg.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -26,6 +26,7 @@ ERR_CUDA = -6
 ERR_INDEX = -7
 ERR_SINGULAR = -8
 INNER_EXACT = 0
+INNER_MG = -1
 
 
 class Problem(C.Structure):

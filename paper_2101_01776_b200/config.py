@@ -33,8 +33,9 @@ class PrecondSpec:
                 raise ValueError(f"unknown gamma mode {self.gamma_mode!r}")
         elif not (float(self.gamma_mode) > 0.0):
             raise ValueError("custom gamma must be positive")
-        if self.inner != "exact" and not (isinstance(self.inner, int) and self.inner > 0):
-            raise ValueError("inner must be 'exact' or a positive int")
+        if self.inner not in ("exact", "mg") and not (isinstance(self.inner, int)
+                                                      and self.inner > 0):
+            raise ValueError("inner must be 'exact', 'mg' or a positive int")
 
     def gamma(self, eta, beta):
         if self.gamma_mode == "star":
@@ -80,4 +81,6 @@ def inner_sweeps(spec):
     inner = spec.inner
     if inner == "exact":
         return 0
+    if inner == "mg":
+        return -1
     return int(inner)

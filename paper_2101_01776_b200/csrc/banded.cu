@@ -23,38 +23,6 @@
 
 namespace irkg {
 
-namespace {
-
-// coefficients of L_eff(a, sigma) at point p: centre and neighbours
-// [xm, xp, ym, yp] (2-D) -- the same operators as kinds.cuh / lx_nb
-template <int KIND>
-__device__ __forceinline__ void stencil_row(const Grid &g, const KindParams &kp, const double *a,
-                                            double sig, int p, const int nb[4], double &cc,
-                                            double cn[4]) {
-  const double ih2[2] = {g.ih2[0], g.ih2[1]};
-  const double i2h[2] = {g.i2h[0], g.i2h[1]};
-  if (KIND == KIND_NLDIFF) {  // Lap(a x)
-    cc = g.lapdiag * a[p];
-    for (int d = 0; d < 2; ++d) {
-      cn[2 * d] = ih2[d] * a[nb[2 * d]];
-      cn[2 * d + 1] = ih2[d] * a[nb[2 * d + 1]];
-    }
-  } else if (KIND == KIND_BURGERS) {  // -Dsum(a x) + sigma nu Lap x
-    cc = sig * kp.nu * g.lapdiag;
-    for (int d = 0; d < 2; ++d) {
-      cn[2 * d] = i2h[d] * a[nb[2 * d]] + sig * kp.nu * ih2[d];
-      cn[2 * d + 1] = -i2h[d] * a[nb[2 * d + 1]] + sig * kp.nu * ih2[d];
-    }
-  } else {  // sigma (nu Lap x + c Dsum x) + a x
-    cc = sig * kp.nu * g.lapdiag + a[p];
-    for (int d = 0; d < 2; ++d) {
-      cn[2 * d] = sig * (kp.nu * ih2[d] - kp.c * i2h[d]);
-      cn[2 * d + 1] = sig * (kp.nu * ih2[d] + kp.c * i2h[d]);
-    }
-  }
-}
-
-}  // namespace
 
 // S = alpha I - dt L into band storage (+= so coinciding neighbours of tiny
 // grids add up) and the out-of-band entries into U (n x nb, column-major).
@@ -416,16 +384,18 @@ __global__ void k_vin_rhs(int n, VecIn vin, int in_off, const double *__restrict
 
 // ------------------------------------------------------------------ host
 
-void Engine::band_factor(BandFactor &F, const Op &L, double alpha, double dt) {
-  if (ndim > 2 || slab())
+void Engine::band_factor(BandFactor &F, const Op &L, double alpha, double dt, const Grid *gl) {
+  const Grid &gg = gl ? *gl : grid;  // (a multigrid level, or the engine's grid)
+  const int nd = gg.nz > 1 ? 3 : (gg.ny > 1 ? 2 : 1);
+  if (nd > 2 || slab())
     throw SolveError(IRKG_ERR_CONFIG,
                      "PrecondSpec(inner='exact') covers single-rank 1-D / 2-D grids (banded LU)");
-  const int n = (int)N;
-  const int bw = ndim == 1 ? 1 : grid.nx;
+  const int n = gg.n;
+  const int bw = nd == 1 ? 1 : gg.nx;
   const int kl = std::min(bw, n - 1), ku = kl;
   const int ldab = 2 * kl + ku + 1;
   // out-of-band wrap entries: the first and last grid rows (2-D) / points (1-D)
-  const int lastrow = ndim == 1 ? 1 : grid.nx;
+  const int lastrow = nd == 1 ? 1 : gg.nx;
   const int nb = (n - lastrow > bw) ? 2 * lastrow : 0;
   if (F.n != n || F.ldab != ldab || F.nb != nb) {
     for (void *p : {(void *)F.ab, (void *)F.piv, (void *)F.binvu, (void *)F.cap, (void *)F.cpiv,
@@ -452,10 +422,10 @@ void Engine::band_factor(BandFactor &F, const Op &L, double alpha, double dt) {
   }
   check(cudaMemsetAsync(F.ab, 0, sizeof(double) * (size_t)ldab * n, stream));
   if (nb > 0) check(cudaMemsetAsync(F.binvu, 0, sizeof(double) * (size_t)n * nb, stream));
-  const int gb = grid_for(N);
+  const int gb = grid_for(n);
   auto assemble = [&](auto KD) {
     k_band_assemble<decltype(KD)::value><<<gb, 256, 0, stream>>>(
-        grid, kp, L.a, L.sigma, alpha, dt, F.ab, ldab, kl, ku, F.binvu, nb);
+        gg, kp, L.a, L.sigma, alpha, dt, F.ab, ldab, kl, ku, F.binvu, nb);
   };
   switch (prob.kind) {
     case KIND_NLDIFF: assemble(std::integral_constant<int, KIND_NLDIFF>{}); break;

@@ -180,7 +180,8 @@ void Engine::set_solver(const irkg_solver &c) {
   if (c.variant < 0 || c.variant > 3) throw SolveError(IRKG_ERR_CONFIG, "variant must be 0..3");
   if (!(c.newton_rtol > 0.0 && c.newton_rtol < 1.0) || !(c.krylov_rtol > 0.0 && c.krylov_rtol < 1.0))
     throw SolveError(IRKG_ERR_CONFIG, "tolerance outside (0, 1)");
-  if (c.inner < 0) throw SolveError(IRKG_ERR_VALUE, "inner must be 'exact' or a positive int");
+  if (c.inner < IRKG_INNER_MG)
+    throw SolveError(IRKG_ERR_VALUE, "inner must be 'exact', 'mg' or a positive int");
   if (c.newton_maxit > IRKG_MAX_NEWTON) throw SolveError(IRKG_ERR_CONFIG, "newton_maxit too large");
   cfg = c;
   have_cfg = true;
@@ -382,6 +383,8 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
     // once per block solve (src/irk_core.py:109-110, 155-156)
     band_factor(bfac[0], B.l1, B.eta, B.dt);
     if (B.size == 2) band_factor(bfac[1], B.l2, B.gamma, B.dt);
+  } else if (B.inner == IRKG_INNER_MG) {
+    mg_setup(B);  // restricted fields + coarsest factors, once per block solve
   }
   const long long n = (long long)B.size * N;
   const int spa = B.size;
@@ -1055,7 +1058,8 @@ int irkg_block2x2_precond(irkg_ctx *ctx, double eta, double beta, double phi, do
                           const double *r_dev, double *z_dev) {
   IRKG_GUARD({
     Engine &e = *ctx->eng;
-    if (inner < 0) throw SolveError(IRKG_ERR_VALUE, "inner must be 'exact' or a positive int");
+    if (inner < IRKG_INNER_MG)
+      throw SolveError(IRKG_ERR_VALUE, "inner must be 'exact', 'mg' or a positive int");
     BlockSpec B{};
     B.size = 2;
     B.eta = eta;
@@ -1071,6 +1075,8 @@ int irkg_block2x2_precond(irkg_ctx *ctx, double eta, double beta, double phi, do
     if (inner == IRKG_INNER_EXACT) {
       e.band_factor(e.bfac[0], B.l1, eta, dt);
       e.band_factor(e.bfac[1], B.l2, gamma, dt);
+    } else if (inner == IRKG_INNER_MG) {
+      e.mg_setup(B);
     }
     e.precond(B, &vin, z_dev, nullptr);
     e.read_ctrl();
@@ -1082,17 +1088,21 @@ int irkg_shifted_solve(irkg_ctx *ctx, double alpha, double dt, int inner, const 
                        const double *r_dev, double *x_dev) {
   IRKG_GUARD({
     Engine &e = *ctx->eng;
-    if (inner < 0) throw SolveError(IRKG_ERR_VALUE, "inner must be 'exact' or a positive int");
+    if (inner < IRKG_INNER_MG)
+      throw SolveError(IRKG_ERR_VALUE, "inner must be 'exact', 'mg' or a positive int");
     VecIn vin{r_dev, 0, nullptr, nullptr};
     check(cudaMemsetAsync(e.ctrl_dev, 0, sizeof(GCtrl), e.stream));
-    if (inner == IRKG_INNER_EXACT) {
+    if (inner <= IRKG_INNER_EXACT) {
       BlockSpec B{};
       B.size = 1;
       B.eta = alpha;
       B.dt = dt;
       B.inner = inner;
       B.l1 = to_op(l);
-      e.band_factor(e.bfac[0], B.l1, alpha, dt);
+      if (inner == IRKG_INNER_EXACT)
+        e.band_factor(e.bfac[0], B.l1, alpha, dt);
+      else
+        e.mg_setup(B);
       e.precond(B, &vin, x_dev, nullptr);
     } else {
       e.jacobi_chain(to_op(l), alpha, dt, inner, &vin, 0, nullptr, 0.0, x_dev, nullptr);
@@ -1110,7 +1120,8 @@ int irkg_block_gmres(irkg_ctx *ctx, int size, double eta, double beta, double ph
   IRKG_GUARD({
     Engine &e = *ctx->eng;
     if (size != 1 && size != 2) throw SolveError(IRKG_ERR_VALUE, "block size must be 1 or 2");
-    if (inner < 0) throw SolveError(IRKG_ERR_VALUE, "inner must be 'exact' or a positive int");
+    if (inner < IRKG_INNER_MG)
+      throw SolveError(IRKG_ERR_VALUE, "inner must be 'exact', 'mg' or a positive int");
     BlockSpec B{};
     B.size = size;
     B.eta = eta;

@@ -90,6 +90,24 @@ struct BandFactor {
   size_t wsmem = 0;
 };
 
+// Geometric-multigrid hierarchy of the block's inner operators (mg.cu)
+constexpr int MG_MAXLEV = 16;
+struct MgLevel {
+  Grid g{};
+  double *a[2] = {nullptr, nullptr};  // coefficient field of S1 / S2 on this level
+  double *b = nullptr, *x = nullptr, *t = nullptr;
+};
+struct MgHier {
+  int nlev = 0;
+  MgLevel lev[MG_MAXLEV];
+  BandFactor coarse[2];
+  double alpha[2] = {0.0, 0.0}, sigma[2] = {0.0, 0.0}, dt = 0.0;
+};
+
+// out = scale * in [+ cpl * zc] (an inner solve's right-hand side; banded.cu)
+__global__ void k_vin_rhs(int n, VecIn vin, int in_off, const double *__restrict__ zc, double cpl,
+                          double *__restrict__ out, const GCtrl *skip);
+
 struct KrylovOut {
   int iterations = 0;
   int converged = 0;
@@ -334,10 +352,16 @@ struct Engine {
   void newton(const double *u, double *K, double t, double dt, irkg_step_stats *stats);
   // banded.cu: exact inner solves (PrecondSpec(inner="exact"), cfg.inner == 0)
   BandFactor bfac[2];
-  void band_factor(BandFactor &F, const Op &L, double alpha, double dt);
+  void band_factor(BandFactor &F, const Op &L, double alpha, double dt, const Grid *gl = nullptr);
   void band_solve(const BandFactor &F, double *b, long long ldb, int nrhs, const GCtrl *skip);
   void band_apply(const BandFactor &F, double *x, const GCtrl *skip);
   void precond_exact(const BlockSpec &B, const VecIn &vin, double *z, const GCtrl *skip);
+  // mg.cu: one V-cycle per inner solve (PrecondSpec(inner="mg"), cfg.inner == -1)
+  MgHier mg;
+  double *mg_rhs = nullptr;
+  void mg_setup(const BlockSpec &B);
+  void mg_vcycle(int o, const double *b, double *x, const GCtrl *skip);
+  void precond_mg(const BlockSpec &B, const VecIn &vin, double *z, const GCtrl *skip);
   // dirk.cu: sequential stage solves of an (S)DIRK tableau (src/nonlinear.py:239-296)
   void dirk_step(double *u, double t, double dt, irkg_step_stats *stats);
 };

@@ -796,6 +796,10 @@ void Engine::precond(const BlockSpec &B, const void *vin_p, double *z, const GCt
     precond_exact(B, vin, z, skip);
     return;
   }
+  if (B.inner == IRKG_INNER_MG) {  // hierarchy prepared by gmres() (mg.cu)
+    precond_mg(B, vin, z, skip);
+    return;
+  }
   if (slab()) {
     // the input must be a fixed pointer here (the multi-rank loop resolves
     // slot j on the host); exchange the halves' boundary planes

@@ -260,4 +260,34 @@ __device__ __forceinline__ double ldiag_at(const Grid &g, const KindParams &kp,
   return sigma * kp.nu * g.lapdiag + a[p];
 }
 
+// coefficients of L_eff(a, sigma) at point p: centre and neighbours
+// [xm, xp, ym, yp] (2-D) -- the same operators as kinds.cuh / lx_nb
+template <int KIND>
+__device__ __forceinline__ void stencil_row(const Grid &g, const KindParams &kp, const double *a,
+                                            double sig, int p, const int nb[4], double &cc,
+                                            double cn[4]) {
+  const double ih2[2] = {g.ih2[0], g.ih2[1]};
+  const double i2h[2] = {g.i2h[0], g.i2h[1]};
+  if (KIND == KIND_NLDIFF) {  // Lap(a x)
+    cc = g.lapdiag * a[p];
+    for (int d = 0; d < 2; ++d) {
+      cn[2 * d] = ih2[d] * a[nb[2 * d]];
+      cn[2 * d + 1] = ih2[d] * a[nb[2 * d + 1]];
+    }
+  } else if (KIND == KIND_BURGERS) {  // -Dsum(a x) + sigma nu Lap x
+    cc = sig * kp.nu * g.lapdiag;
+    for (int d = 0; d < 2; ++d) {
+      cn[2 * d] = i2h[d] * a[nb[2 * d]] + sig * kp.nu * ih2[d];
+      cn[2 * d + 1] = -i2h[d] * a[nb[2 * d + 1]] + sig * kp.nu * ih2[d];
+    }
+  } else {  // sigma (nu Lap x + c Dsum x) + a x
+    cc = sig * kp.nu * g.lapdiag + a[p];
+    for (int d = 0; d < 2; ++d) {
+      cn[2 * d] = sig * (kp.nu * ih2[d] - kp.c * i2h[d]);
+      cn[2 * d + 1] = sig * (kp.nu * ih2[d] + kp.c * i2h[d]);
+    }
+  }
+}
+
+
 }  // namespace irkg

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--family", default=None)
     ap.add_argument("--s", type=int, default=None)
     ap.add_argument("--timing", action="store_true", help="per-phase CUDA-event timing")
+    ap.add_argument("--inner", default=None, help="override PrecondSpec.inner (int, exact, mg)")
     args = ap.parse_args()
     import torch
 
@@ -33,7 +34,9 @@ def main():
                           restart=sv["restart"], newton_maxit=sv["newton_maxit"],
                           newton_rtol=sv.get("newton_rtol", 1e-9),
                           krylov_rtol=sv.get("krylov_rtol", 1e-5),
-                          precond=pk.PrecondSpec(inner=sv["inner"]))
+                          precond=pk.PrecondSpec(inner=(sv["inner"] if args.inner is None else
+                                                        (args.inner if args.inner in ("exact", "mg")
+                                                         else int(args.inner)))))
     ctx = Context(spec.problem, 0)
     ctx.set_prep(pk.prepare_stages(tab))
     ctx.set_config(cfg)
