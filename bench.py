@@ -345,7 +345,8 @@ def run_ours(args, spec, ws, rank, local):
             "share_of_step": (cgs_ms * 1e-3) / tr if tr > 0 else None}
 
     # e2e: the public API with host buffers (H2D of u + D2H of u_next per step)
-    uh = u_start.cpu().numpy().copy()
+    # the caller's state in page-locked memory (pk.step returns u_next pinned too)
+    uh = u_start.cpu().pin_memory().numpy()
     t = t_start
     e_stats = []
     barrier(ws)

@@ -49,10 +49,25 @@ def _is_torch(x):
         return False
 
 
+def _pinned(n):
+    """A numpy float64 view of ``n`` page-locked doubles from torch's caching
+    host allocator: host<->device copies of step states run at full DMA speed
+    and the block returns to the cache when the array dies (no per-step
+    cudaHostAlloc)."""
+    return torch().empty(int(n), dtype=torch().float64, pin_memory=True).numpy()
+
+
+def _host_copy(x_dev):
+    """Device vector -> new (pinned) numpy array."""
+    out = _pinned(x_dev.numel()).reshape(tuple(x_dev.shape))
+    torch().from_numpy(out).copy_(x_dev)
+    return out
+
+
 def _out(x_dev, like):
     if _is_torch(like):
         return x_dev
-    return x_dev.cpu().numpy()
+    return _host_copy(x_dev)
 
 
 @dataclass
@@ -133,7 +148,9 @@ def step(sys, u, t, dt, tableau, cfg=SolverConfig(), prep=None):
         ud = as_device(u).clone()
         stats = ctx.step_device(ud, t, dt)
         return ud, stats
-    uh = np.array(u, dtype=np.float64, copy=True, order="C")
+    # u_next lives in page-locked memory: irkg_step_host's H2D/D2H are DMA copies
+    uh = _pinned(sys.dim)
+    np.copyto(uh, np.asarray(u, dtype=np.float64).reshape(-1))
     stats = ctx.step_host(uh, t, dt)
     return uh, stats
 
@@ -151,7 +168,7 @@ def _dirk_step(sys, u, t, dt, tableau, cfg):
         return ud, stats
     ud = as_device(np.asarray(u, dtype=np.float64)).clone()
     stats = ctx.dirk_step_device(ud, t, dt)
-    return ud.cpu().numpy(), stats
+    return _host_copy(ud), stats
 
 
 def integrate(sys, u0, t0, t_final, dt, tableau, cfg=SolverConfig(), snapshot_every=None):
@@ -429,9 +446,11 @@ def dae_step(sys, u, w, t, dt, tableau, cfg=SolverConfig(), prep=None, mode="reo
         uw = torch().cat([as_device(u), as_device(w)]).contiguous()
         stats = ctx.dae_step_device(uw, t, dt)
         return uw[:n].clone(), uw[n:].clone(), stats
-    uw = np.ascontiguousarray(np.concatenate([np.asarray(u, float), np.asarray(w, float)]))
+    uw = _pinned(n + sys.dim_w)
+    uw[:n] = np.asarray(u, float).reshape(-1)
+    uw[n:] = np.asarray(w, float).reshape(-1)
     stats = ctx.dae_step_host(uw, t, dt)
-    return uw[:n].copy(), uw[n:].copy(), stats
+    return uw[:n], uw[n:], stats
 
 
 def dae_integrate(sys, u0, w0, t0, t_final, dt, tableau, cfg=SolverConfig(), mode="reordered"):
