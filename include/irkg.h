@@ -211,6 +211,13 @@ int irkg_dirk_step(irkg_ctx *ctx, double *u_dev, double t, double dt, irkg_step_
  * (the end-to-end path timed by bench.py's e2e leg). */
 int irkg_step_host(irkg_ctx *ctx, double *u_host, double t, double dt, irkg_step_stats *stats);
 
+/* step() with the reference's value semantics on host arrays
+ * (src/nonlinear.py:299-314 returns a new u_next and leaves u untouched):
+ * H2D copy of u_host, step, D2H copy into u_next_host (may equal u_host).
+ * Page-locked buffers make both copies DMA transfers. */
+int irkg_step_host_out(irkg_ctx *ctx, const double *u_host, double *u_next_host, double t,
+                       double dt, irkg_step_stats *stats);
+
 /* ---- operator-level entry points (parity tests; src/irk_core.py) ----
  * An operator "field" is the coefficient field a (device, N) + scalar sigma
  * of the collapsed weighted linearisation sum_k w_k L_k (see problems.py). */

@@ -163,6 +163,7 @@ _SIGS = {
     "irkg_newton_step": (_I, [_P, _P, _P, _D, _D, C.POINTER(StepStatsC)]),
     "irkg_step": (_I, [_P, _P, _D, _D, C.POINTER(StepStatsC)]),
     "irkg_step_host": (_I, [_P, _P, _D, _D, C.POINTER(StepStatsC)]),
+    "irkg_step_host_out": (_I, [_P, _P, _P, _D, _D, C.POINTER(StepStatsC)]),
     "irkg_linearize": (_I, [_P, _P, _I, _P, _P, C.POINTER(_D)]),
     "irkg_block2x2_apply": (
         _I,

@@ -90,49 +90,74 @@ __device__ __forceinline__ double wsum(double v) {
 
 }  // namespace
 
-// Finish Arnoldi column j (src/sparsela.py:227-256); single thread.
-__device__ void arnoldi_finish_dev(GWork W) {
+// Finish Arnoldi column j (src/sparsela.py:227-256), by one whole CTA.
+// The column, the previous rotations and the coefficients are staged into
+// shared memory (scr: >= 3 (MAXR + 2) doubles) by all threads at once, thread
+// 0 applies the j earlier Givens rotations with the running entry in a
+// register (the same operations in the same order as the textbook in-place
+// loop, so H is bit-identical), and the finished column goes back to global
+// memory in parallel.  A single-thread loop over global memory made the
+// finish a chain of dependent L2 round trips that grew with j.
+__device__ void arnoldi_finish_block(GWork W, double *scr) {
   GCtrl *c = W.ctrl;
   const int j = c->j;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double *hs = scr, *css = scr + (MAXR + 2), *sns = scr + 2 * (MAXR + 2);
   double *h = W.H + (size_t)j * (MAXR + 1);
-  for (int i = 0; i <= j; ++i) h[i] = (0.0 + W.c1[i]) + W.c2[i];
-  const double hj = sqrt(c->hn2);
-  const double wnorm0 = sqrt(c->wn2);
-  h[j + 1] = hj;
-  const bool breakdown = hj <= 1e-14 * fmax(wnorm0, 1e-300);
-  if (!breakdown) W.alpha[j + 1] = 1.0 / hj;
-  for (int i = 0; i < j; ++i) {
-    double tmp = W.cs[i] * h[i] + W.sn[i] * h[i + 1];
-    h[i + 1] = -W.sn[i] * h[i] + W.cs[i] * h[i + 1];
-    h[i] = tmp;
+  for (int i = tid; i <= j; i += nt) {
+    hs[i] = (0.0 + W.c1[i]) + W.c2[i];
+    if (i < j) {
+      css[i] = W.cs[i];
+      sns[i] = W.sn[i];
+    }
   }
-  const double denom = hypot(h[j], h[j + 1]);
-  if (denom == 0.0) {  // dead column (src/sparsela.py:239-246)
-    c->breakdown = 1;
-    c->total_it += 1;
-    W.res[c->n_res] = W.res[c->n_res - 1];
-    c->n_res += 1;
-    c->k = j;
-    c->cycle_done = 1;
-    return;
+  __syncthreads();
+  if (tid == 0) {
+    const double hj = sqrt(c->hn2);
+    const double wnorm0 = sqrt(c->wn2);
+    hs[j + 1] = hj;
+    const bool breakdown = hj <= 1e-14 * fmax(wnorm0, 1e-300);
+    if (!breakdown) W.alpha[j + 1] = 1.0 / hj;
+    double hi = hs[0];
+    for (int i = 0; i < j; ++i) {
+      const double hn = hs[i + 1];
+      const double tmp = css[i] * hi + sns[i] * hn;
+      hi = -sns[i] * hi + css[i] * hn;
+      hs[i] = tmp;
+    }
+    hs[j] = hi;
+    const double denom = hypot(hs[j], hs[j + 1]);
+    if (denom == 0.0) {  // dead column (src/sparsela.py:239-246)
+      c->breakdown = 1;
+      c->total_it += 1;
+      W.res[c->n_res] = W.res[c->n_res - 1];
+      c->n_res += 1;
+      c->k = j;
+      c->cycle_done = 1;
+    } else {
+      W.cs[j] = hs[j] / denom;
+      W.sn[j] = hs[j + 1] / denom;
+      hs[j] = denom;
+      hs[j + 1] = 0.0;
+      W.g[j + 1] = -W.sn[j] * W.g[j];
+      W.g[j] = W.cs[j] * W.g[j];
+      c->total_it += 1;
+      const double est = fabs(W.g[j + 1]) / c->bnorm;
+      W.res[c->n_res] = est;
+      c->n_res += 1;
+      if (breakdown) c->breakdown = 1;
+      if (est <= c->rtol || breakdown || c->total_it >= c->maxit || j + 1 >= c->m) {
+        c->k = j + 1;
+        c->cycle_done = 1;
+      } else {
+        c->j = j + 1;
+      }
+    }
   }
-  W.cs[j] = h[j] / denom;
-  W.sn[j] = h[j + 1] / denom;
-  h[j] = denom;
-  h[j + 1] = 0.0;
-  W.g[j + 1] = -W.sn[j] * W.g[j];
-  W.g[j] = W.cs[j] * W.g[j];
-  c->total_it += 1;
-  const double est = fabs(W.g[j + 1]) / c->bnorm;
-  W.res[c->n_res] = est;
-  c->n_res += 1;
-  if (breakdown) c->breakdown = 1;
-  if (est <= c->rtol || breakdown || c->total_it >= c->maxit || j + 1 >= c->m) {
-    c->k = j + 1;
-    c->cycle_done = 1;
-  } else {
-    c->j = j + 1;
-  }
+  __syncthreads();
+  for (int i = tid; i <= j + 1; i += nt) h[i] = hs[i];
+  __threadfence();
+  __syncthreads();
 }
 
 constexpr int VM_TR = 4;  // tensor maps for tile rows 32, 64, 128, 256
@@ -499,15 +524,13 @@ __global__ void __launch_bounds__(CGS_BS, 2)
     }
   }
   __syncthreads();
-  if (tid == 0) {
-    // use_cond < 0: multi-rank -- the column is finished after the all-reduce
-    if (MODE == CGS_UPD_NORM && use_cond >= 0) {
-      __threadfence();
-      arnoldi_finish_dev(W);
-      if (use_cond > 0) cudaGraphSetConditional(cond, ctrl->cycle_done ? 0u : 1u);
-    }
-    *counter = 0u;
+  // use_cond < 0: multi-rank -- the column is finished after the all-reduce
+  if (MODE == CGS_UPD_NORM && use_cond >= 0) {
+    __threadfence();
+    arnoldi_finish_block(W, sm);  // the ring is drained: its memory is scratch now
+    if (tid == 0 && use_cond > 0) cudaGraphSetConditional(cond, ctrl->cycle_done ? 0u : 1u);
   }
+  if (tid == 0) *counter = 0u;
 }
 
 // Tensor maps over the basis V viewed as a 2-D array (rows: vpitch, slots:
@@ -625,12 +648,16 @@ void Engine::cgs(long long n, int nsweeps) {
 // c1 travels together with ||w||^2 in c1[L]); the Hessenberg column is then
 // finished from the global sums by k_arnoldi_finish_slab.
 __global__ void k_arnoldi_finish_slab(GWork W, int use_cond, cudaGraphConditionalHandle cond) {
+  __shared__ double scr[3 * (MAXR + 2)];
   GCtrl *c = W.ctrl;
-  if (!c->cycle_done) {
-    c->wn2 = W.c1[c->j + 1];
-    arnoldi_finish_dev(W);
+  const bool live = !c->cycle_done;  // block-uniform
+  __syncthreads();
+  if (live) {
+    if (threadIdx.x == 0) c->wn2 = W.c1[c->j + 1];
+    __syncthreads();
+    arnoldi_finish_block(W, scr);
   }
-  if (use_cond > 0) cudaGraphSetConditional(cond, c->cycle_done ? 0u : 1u);
+  if (threadIdx.x == 0 && use_cond > 0) cudaGraphSetConditional(cond, c->cycle_done ? 0u : 1u);
 }
 
 void Engine::cgs_slab(long long n) {
@@ -661,7 +688,7 @@ void Engine::cgs_slab(long long n) {
              (const double *)W.c2, (const double *)wbuf, dnull, part, G, counter, stage, -1,
              cond_handle, maps, trm);
   allreduce(&ctrl_dev->hn2, 1);
-  k_arnoldi_finish_slab<<<1, 1, 0, stream>>>(W, cond_active ? 1 : 0, cond_handle);
+  k_arnoldi_finish_slab<<<1, 128, 0, stream>>>(W, cond_active ? 1 : 0, cond_handle);
   count(4);
 }
 

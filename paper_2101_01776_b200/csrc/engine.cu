@@ -988,7 +988,8 @@ int irkg_dirk_step(irkg_ctx *ctx, double *u_dev, double t, double dt, irkg_step_
   });
 }
 
-int irkg_step_host(irkg_ctx *ctx, double *u_host, double t, double dt, irkg_step_stats *stats) {
+int irkg_step_host_out(irkg_ctx *ctx, const double *u_host, double *u_next_host, double t,
+                       double dt, irkg_step_stats *stats) {
   IRKG_GUARD({
     Engine &e = *ctx->eng;
     if (!e.have_tab || !e.have_cfg) throw SolveError(IRKG_ERR_CONFIG, "tableau/solver not set");
@@ -1000,9 +1001,14 @@ int irkg_step_host(irkg_ctx *ctx, double *u_host, double t, double dt, irkg_step
     check(cudaMemsetAsync(e.Kst, 0, (size_t)e.s * e.N * sizeof(double), e.stream));
     e.newton(e.ufield, e.Kst, t, dt, stats);
     e.step_update(dt, e.Kst, e.ufield);
-    check(cudaMemcpyAsync(u_host, e.ufield, e.N * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+    check(cudaMemcpyAsync(u_next_host, e.ufield, e.N * sizeof(double), cudaMemcpyDeviceToHost,
+                          e.stream));
     check(cudaStreamSynchronize(e.stream));
   });
+}
+
+int irkg_step_host(irkg_ctx *ctx, double *u_host, double t, double dt, irkg_step_stats *stats) {
+  return irkg_step_host_out(ctx, u_host, u_host, t, dt, stats);
 }
 
 static Op to_op(const irkg_opfield *f) {

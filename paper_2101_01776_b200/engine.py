@@ -280,6 +280,15 @@ class Context:
         self._check(rc, st)
         return step_stats_from_c(st)
 
+    def step_host_out(self, u_host, u_next_host, t, dt):
+        """u_host -> u_next_host (C-contiguous float64 numpy arrays; u_host untouched)."""
+        st = self._new_stats()
+        rc = self.lib.irkg_step_host_out(self.h, u_host.ctypes.data_as(C.c_void_p),
+                                         u_next_host.ctypes.data_as(C.c_void_p), float(t),
+                                         float(dt), C.byref(st))
+        self._check(rc, st)
+        return step_stats_from_c(st)
+
     def newton(self, u_dev, k_dev, t, dt):
         st = self._new_stats()
         rc = self.lib.irkg_newton_step(self.h, ptr(u_dev), ptr(k_dev), float(t), float(dt),

@@ -148,10 +148,13 @@ def step(sys, u, t, dt, tableau, cfg=SolverConfig(), prep=None):
         ud = as_device(u).clone()
         stats = ctx.step_device(ud, t, dt)
         return ud, stats
-    # u_next lives in page-locked memory: irkg_step_host's H2D/D2H are DMA copies
+    # u_next lives in page-locked memory (and so does u when it came from a
+    # previous step): both copies of irkg_step_host_out are DMA transfers
+    uin = np.ascontiguousarray(u, dtype=np.float64).reshape(-1)
+    if uin.size != sys.dim:
+        raise ValueError(f"u has {uin.size} entries, the system has {sys.dim}")
     uh = _pinned(sys.dim)
-    np.copyto(uh, np.asarray(u, dtype=np.float64).reshape(-1))
-    stats = ctx.step_host(uh, t, dt)
+    stats = ctx.step_host_out(uin, uh, t, dt)
     return uh, stats
 
 
