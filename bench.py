@@ -348,6 +348,9 @@ def run_ours(args, spec, ws, rank, local):
     # the caller's state in page-locked memory (pk.step returns u_next pinned too)
     uh = u_start.cpu().pin_memory().numpy()
     t = t_start
+    if ws == 1:  # untimed: the caching host allocator's first page-locked blocks
+        for _ in range(2):
+            pk.step(prob, uh, t, spec.dt, tab, cfg, prep=prep)
     e_stats = []
     barrier(ws)
     te0 = time.perf_counter()

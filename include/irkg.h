@@ -147,6 +147,11 @@ typedef struct {
   double precond_time_ms; /* device time of the inner solves (if timing on) */
   double op_time_ms;      /* device time of the block operator (if timing on) */
   int64_t halo_exchanges; /* slab-partition halo exchanges issued */
+  /* with IRKG_GRAPH_TIMING=1 (one event pair per restart cycle): device time
+   * of the Arnoldi-loop graphs of 1x1 / 2x2 blocks and of the cycle ends */
+  double arnoldi_ms_1x1;
+  double arnoldi_ms_2x2;
+  double cycle_end_ms;
 } irkg_counters;
 
 /* Host-callback transport for the slab partition (alternative to NCCL):

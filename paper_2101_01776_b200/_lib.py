@@ -127,6 +127,9 @@ class Counters(C.Structure):
         ("precond_time_ms", C.c_double),
         ("op_time_ms", C.c_double),
         ("halo_exchanges", C.c_int64),
+        ("arnoldi_ms_1x1", C.c_double),
+        ("arnoldi_ms_2x2", C.c_double),
+        ("cycle_end_ms", C.c_double),
     ]
 
 

@@ -610,7 +610,7 @@ void Engine::dae_transformed_solve(double dt, const double *rhs, double *dk,
     B.l1 = op_of(diag_slot[off]);
     B.l2 = op_of(diag_slot[off + 1]);
     B.l1.present = B.l2.present = 1;  // reordered drops C12/C21 (src/dae.py:232-233)
-    KrylovOut rep = gmres(B, RHS, XU, cfg.krylov_rtol, cfg.krylov_maxit, cfg.restart);
+    KrylovOut rep = gmres(B, RHS, XU, cfg.krylov_rtol, cfg.krylov_maxit, cfg.restart, false);
     const long long diff_solves = rep.precond_applications;
     // y_u -> Y rows; constraint solves for y_w (src/dae.py:274-278)
     double *Y1 = Y + (size_t)off * n2, *Y2r = Y + (size_t)(off + 1) * n2;

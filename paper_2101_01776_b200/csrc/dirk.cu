@@ -91,7 +91,7 @@ void Engine::dirk_step(double *u, double t, double dt, irkg_step_stats *stats) {
       B.dt = h;
       B.inner = cfg.inner;
       B.l1 = Op{opA, 1.0, 1};
-      KrylovOut rep = gmres(B, F, dk, cfg.krylov_rtol, cfg.krylov_maxit, cfg.restart);
+      KrylovOut rep = gmres(B, F, dk, cfg.krylov_rtol, cfg.krylov_maxit, cfg.restart, false);
       axpy(N, 1.0, dk, ki);
       it += 1;
       stats->newton_iterations += 1;

@@ -103,6 +103,8 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   check(cudaEventCreate(&ev1), "event");
   check(cudaEventCreate(&evp[0]), "event");
   check(cudaEventCreate(&evp[1]), "event");
+  for (auto &e : evg) check(cudaEventCreate(&e), "event");
+  if (const char *e = getenv("IRKG_GRAPH_TIMING")) graph_timing = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_GRAPHS")) use_graphs = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_FUSED_JACOBI")) fused_jacobi = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_JSPAN")) jspan_override = atoi(e);
@@ -129,6 +131,8 @@ Engine::~Engine() {
   if (ctrl_host) cudaFreeHost(ctrl_host);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
+  for (auto e : evg)
+    if (e) cudaEventDestroy(e);
   drop_graphs();
   if (cap_stream) cudaStreamDestroy(cap_stream);
   dae_fini();
@@ -372,7 +376,7 @@ double Engine::gamma_of(double eta, double beta) const {
 // basis Z is not stored: with the fixed linear preconditioner M^{-1}
 // (Jacobi-k), x += Z y == x += M^{-1} (V y).
 KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double rtol, int maxit,
-                        int restart) {
+                        int restart, bool want_residuals) {
   if (!(rtol > 0.0 && rtol < 1.0)) throw SolveError(IRKG_ERR_VALUE, "rtol must lie in (0, 1)");
   ensure_basis(restart);
   ensure_res(maxit);
@@ -443,7 +447,9 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
       // whole Arnoldi loop of this cycle as one graph launch (device-side WHILE)
       // (no host read here: the counters are settled after the cycle end)
       CycleGraph &cg = cycle_graph(B, n, true);
+      if (graph_timing) check(cudaEventRecord(evg[0], stream));
       check(cudaGraphLaunch(cg.ex, stream), "cudaGraphLaunch");
+      if (graph_timing) check(cudaEventRecord(evg[1], stream));
       graph_body_kernels = cg.body_kernels / graph_unroll;  // per Arnoldi step
     } else {
       for (int it = 0; it < m; ++it) {
@@ -485,7 +491,17 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
     axpy(n, 1.0, zbuf, x);
     block_op(B, x, V, rhs, &ctrl_dev->rr, nullptr);
     cycle_end();
+    const bool timed_cycle = graph_timing && graph_body_kernels > 0;
+    if (timed_cycle) check(cudaEventRecord(evg[2], stream));
     read_ctrl();
+    if (timed_cycle) {
+      float ms = 0.f;
+      check(cudaEventSynchronize(evg[2]), "sync");
+      check(cudaEventElapsedTime(&ms, evg[0], evg[1]), "elapsed");
+      (B.size == 2 ? counters.arnoldi_ms_2x2 : counters.arnoldi_ms_1x1) += ms;
+      check(cudaEventElapsedTime(&ms, evg[1], evg[2]), "elapsed");
+      counters.cycle_end_ms += ms;
+    }
     if (graph_body_kernels > 0) {  // WHILE-graph cycle: its = new iterations
       const int its = ctrl_host->total_it - total_it;
       counters.kernel_launches += (long long)graph_body_kernels * std::max(its, 1);
@@ -511,6 +527,7 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
   out.iterations = total_it;
   out.converged = converged;
   out.precond_applications = total_it * spa;
+  if (!want_residuals && converged) return out;
   int nres = ctrl_host->n_res;
   if (total_it == 0 && nres == 0) nres = 1;
   out.residuals.resize(nres);
@@ -668,7 +685,8 @@ void Engine::transformed_solve(double dt, const double *rhs, double *dk, irkg_st
       B.l2.present = 1;
       if (!B.l2.a) B.l2.a = opA + (size_t)diag_slot[off + 1] * N;
     }
-    KrylovOut rep = gmres(B, RHS, Y + (size_t)off * N, cfg.krylov_rtol, cfg.krylov_maxit, cfg.restart);
+    KrylovOut rep = gmres(B, RHS, Y + (size_t)off * N, cfg.krylov_rtol, cfg.krylov_maxit, cfg.restart,
+                          false);
     if (stats) {
       if (stats->n_block_records < IRKG_MAX_BLOCK_RECORDS) {
         stats->block_offset[stats->n_block_records] = off;

@@ -159,6 +159,8 @@ struct Engine {
   int nops_cap = 0;
   GCtrl *ctrl_host = nullptr;   // pinned mirror
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evp[2] = {nullptr, nullptr};
+  cudaEvent_t evg[3] = {nullptr, nullptr, nullptr};  // cycle graph / cycle end (IRKG_GRAPH_TIMING)
+  bool graph_timing = false;
 
   // current linearisation: operator slot per diag row and per offdiag key
   int nops = 0;
@@ -342,8 +344,11 @@ struct Engine {
   void read_ctrl();
   int graph_body_kernels = 0;  // body size of the WHILE graph launched this cycle
   std::vector<double> qr_matrix() const;  // Q R0, row-major s x s
+  // want_residuals = false: the residual history is copied back only when
+  // the solve failed (the stage solves report it in StageSolveError alone),
+  // saving a host round trip per block solve
   KrylovOut gmres(const BlockSpec &B, const double *rhs, double *x, double rtol, int maxit,
-                  int restart);
+                  int restart, bool want_residuals = true);
   void build_linearization(const double *U);
   Op op_of(int slot) const;
   double gamma_of(double eta, double beta) const;
