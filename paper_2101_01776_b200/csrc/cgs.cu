@@ -357,10 +357,26 @@ __device__ __forceinline__ void tile_load_tail(const TileArgs &A, double *buf, i
   __syncthreads();
 }
 
+// Sum of the G per-CTA partials of one entry, by one warp, in a fixed order
+// (identical wherever it runs: the last CTA of a sweep, or every CTA of the
+// next sweep).
+__device__ __forceinline__ double fold_partials(const double *pl, int G, int lane) {
+  double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;
+  int c = lane;
+  for (; c + 96 < G; c += 128) {
+    f0 += __ldcg(pl + c);
+    f1 += __ldcg(pl + c + 32);
+    f2 += __ldcg(pl + c + 64);
+    f3 += __ldcg(pl + c + 96);
+  }
+  for (; c < G; c += 32) f0 += __ldcg(pl + c);
+  return wsum((f0 + f1) + (f2 + f3));
+}
+
 // One sweep's tile loop (grid-stride over row tiles, NST tiles in flight).
 template <int MODE, int TRC>
 __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q], double &nrm,
-                                          const GWork &W, const double *cin) {
+                                          const GWork &W, const double *cin, const double *pin) {
   const int G = A.G, ntiles = A.ntiles;
   const int t0 = blockIdx.x;
   const int NST = A.nst;
@@ -379,8 +395,30 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
   for (int i = 0; i < NST; ++i)
     if (t0 + i * G < ntiles && tile_full<TRC>(A, ph(t0 + i * G)))
       tile_issue_w<TRC>(A, ph(t0 + i * G), i);
-  if (MODE != CGS_DOT)
-    for (int l = threadIdx.x; l < A.L; l += CGS_BS) const_cast<double *>(A.cs)[l] = W.alpha[l] * cin[l];
+  if (MODE != CGS_DOT) {
+    if (pin) {
+      // the previous sweep left only per-CTA partials: every CTA folds them
+      // itself (same order everywhere), off the serial last-CTA path; CTA 0
+      // publishes the coefficients (and DOT's ||w||^2) for the column finish
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      const int nprev = (MODE == CGS_UPD_DOT) ? A.L + 1 : A.L;
+      for (int l = warp; l < nprev; l += CGS_NW) {
+        const double v = fold_partials(pin + (size_t)l * A.G, A.G, lane);
+        if (lane == 0) {
+          if (l < A.L) {
+            const double c = W.alpha[l] * v;
+            const_cast<double *>(A.cs)[l] = W.alpha[l] * c;
+            if (blockIdx.x == 0) const_cast<double *>(cin)[l] = c;
+          } else if (blockIdx.x == 0) {
+            W.ctrl->wn2 = v;
+          }
+        }
+      }
+    } else {
+      for (int l = threadIdx.x; l < A.L; l += CGS_BS)
+        const_cast<double *>(A.cs)[l] = W.alpha[l] * cin[l];
+    }
+  }
   __syncthreads();
   pdl_trigger();
 
@@ -416,7 +454,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
     k_cgs(int n, double *__restrict__ V, long long pitch, GWork W, const double *cin,
           const double *win, double *wout, double *part, int G, unsigned *counter,
           int ring_doubles, int use_cond, cudaGraphConditionalHandle cond,
-          const char *__restrict__ vmaps, int trmax) {
+          const char *__restrict__ vmaps, int trmax, const double *pin, int defer) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bars[CGS_MAXST];
   __shared__ double cs[MAXR + 1];
@@ -459,12 +497,12 @@ __global__ void __launch_bounds__(CGS_BS, 2)
 #pragma unroll
   for (int q = 0; q < CGS_Q; ++q) acc[q] = 0.0;
   switch (TR) {
-    case 32: cgs_tiles<MODE, 32>(A, acc, nrm, W, cin); break;
-    case 64: cgs_tiles<MODE, 64>(A, acc, nrm, W, cin); break;
-    case 128: cgs_tiles<MODE, 128>(A, acc, nrm, W, cin); break;
-    case 256: cgs_tiles<MODE, 256>(A, acc, nrm, W, cin); break;
-    case 512: cgs_tiles<MODE, 512>(A, acc, nrm, W, cin); break;
-    default: cgs_tiles<MODE, 1024>(A, acc, nrm, W, cin); break;
+    case 32: cgs_tiles<MODE, 32>(A, acc, nrm, W, cin, pin); break;
+    case 64: cgs_tiles<MODE, 64>(A, acc, nrm, W, cin, pin); break;
+    case 128: cgs_tiles<MODE, 128>(A, acc, nrm, W, cin, pin); break;
+    case 256: cgs_tiles<MODE, 256>(A, acc, nrm, W, cin, pin); break;
+    case 512: cgs_tiles<MODE, 512>(A, acc, nrm, W, cin, pin); break;
+    default: cgs_tiles<MODE, 1024>(A, acc, nrm, W, cin, pin); break;
   }
 
   // per-CTA partials -> part[l * G + cta]
@@ -489,6 +527,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
       part[blockIdx.x] = tot;
     }
   }
+  if (defer) return;  // the next sweep's CTAs fold these partials themselves
   __threadfence();
   __syncthreads();
   if (tid == 0) is_last = (atomicAdd(counter, 1u) == (unsigned)(G - 1));
@@ -497,17 +536,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   __threadfence();
   const int nfold = (MODE == CGS_UPD_NORM) ? 1 : nd;
   for (int l = warp; l < nfold; l += CGS_NW) {
-    const double *pl = part + (size_t)l * G;
-    double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;
-    int c = lane;
-    for (; c + 96 < G; c += 128) {
-      f0 += __ldcg(pl + c);
-      f1 += __ldcg(pl + c + 32);
-      f2 += __ldcg(pl + c + 64);
-      f3 += __ldcg(pl + c + 96);
-    }
-    for (; c < G; c += 32) f0 += __ldcg(pl + c);
-    double v = wsum((f0 + f1) + (f2 + f3));
+    const double v = fold_partials(part + (size_t)l * G, G, lane);
     if (lane == 0) {
       if (MODE == CGS_DOT) {
         if (l == L && use_cond < 0)
@@ -623,22 +652,26 @@ void Engine::cgs(long long n, int nsweeps) {
   const int trm = cgs_trmax();
   const double *cnull = nullptr;
   double *dnull = nullptr;
+  // DOT and UPD_DOT leave per-CTA partials in their own regions of `part`;
+  // the next sweep folds them in every CTA (no last-CTA fold between sweeps)
+  double *pdot = part + (size_t)(MAXR + 2) * G, *pupd = part + 2 * (size_t)(MAXR + 2) * G;
   launch_pdl(k_cgs<CGS_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W, cnull,
-             (const double *)wbuf, dnull, part, G, counter, stage, 0, cond_handle, maps, trm);
+             (const double *)wbuf, dnull, pdot, G, counter, stage, 0, cond_handle, maps, trm,
+             cnull, 1);
   if (nsweeps < 2) {  // (phase probe)
     count(1);
     return;
   }
   launch_pdl(k_cgs<CGS_UPD_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
-             (const double *)W.c1, (const double *)wbuf, wbuf, part, G, counter, stage, 0,
-             cond_handle, maps, trm);
+             (const double *)W.c1, (const double *)wbuf, wbuf, pupd, G, counter, stage, 0,
+             cond_handle, maps, trm, (const double *)pdot, 1);
   if (nsweeps < 3) {
     count(2);
     return;
   }
   launch_pdl(k_cgs<CGS_UPD_NORM>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
              (const double *)W.c2, (const double *)wbuf, dnull, part, G, counter, stage, uc,
-             cond_handle, maps, trm);
+             cond_handle, maps, trm, (const double *)pupd, 0);
   count(3);
 }
 
@@ -678,15 +711,16 @@ void Engine::cgs_slab(long long n) {
   const double *cnull = nullptr;
   double *dnull = nullptr;
   launch_pdl(k_cgs<CGS_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W, cnull,
-             (const double *)wbuf, dnull, part, G, counter, stage, -1, cond_handle, maps, trm);
+             (const double *)wbuf, dnull, part, G, counter, stage, -1, cond_handle, maps, trm,
+             cnull, 0);
   allreduce(W.c1, cnt);
   launch_pdl(k_cgs<CGS_UPD_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
              (const double *)W.c1, (const double *)wbuf, wbuf, part, G, counter, stage, -1,
-             cond_handle, maps, trm);
+             cond_handle, maps, trm, cnull, 0);
   allreduce(W.c2, cnt);
   launch_pdl(k_cgs<CGS_UPD_NORM>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
              (const double *)W.c2, (const double *)wbuf, dnull, part, G, counter, stage, -1,
-             cond_handle, maps, trm);
+             cond_handle, maps, trm, cnull, 0);
   allreduce(&ctrl_dev->hn2, 1);
   k_arnoldi_finish_slab<<<1, 128, 0, stream>>>(W, cond_active ? 1 : 0, cond_handle);
   count(4);

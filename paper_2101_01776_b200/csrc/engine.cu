@@ -74,7 +74,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   kp.lam = p.lam;
   kp.mu = p.mu;
   N = grid.n;
-  dalloc(&part, (size_t)(MAXR + 2) * G);
+  dalloc(&part, 3 * (size_t)(MAXR + 2) * G);  // 3 regions: CGS sweeps fold across launches
   dalloc(&counter, 1);
   check(cudaMemsetAsync(counter, 0, sizeof(unsigned), stream));
   dalloc(&scal_dev, 16);

@@ -136,7 +136,7 @@ struct Engine {
   int s = 0;
 
   // device buffers
-  double *part = nullptr;       // (MAXR+2) * G reduction partials
+  double *part = nullptr;       // 3 x (MAXR+2) * G reduction partials
   unsigned *counter = nullptr;  // last-CTA ticket
   double *scal_dev = nullptr;   // scalar outputs
   GCtrl *ctrl_dev = nullptr;

@@ -77,56 +77,98 @@ __global__ void k_norm2(int n, const double *__restrict__ x, double *part, int G
 // Newton update fused with the next stage values (src/nonlinear.py:221,
 // 147): K_i += sum_k (Q R0)_ik y_k ;  U_i = u + dt sum_j A0_ij K_j.
 // Same arithmetic as stage_mix (dk) + stage_mix (K += dk) + stage_values.
+// V consecutive points per thread (V = 2: double2 loads/stores when the
+// stage rows are 16-byte aligned); per point the same operations in the same
+// order as the scalar form.
+template <int V>
+struct Vx {
+  static __device__ __forceinline__ void ld(const double *__restrict__ p, double (&o)[V]) {
+    if constexpr (V == 2) {
+      const double2 t = *reinterpret_cast<const double2 *>(p);
+      o[0] = t.x;
+      o[1] = t.y;
+    } else {
+      o[0] = p[0];
+    }
+  }
+  static __device__ __forceinline__ void st(double *__restrict__ p, const double (&o)[V]) {
+    if constexpr (V == 2)
+      *reinterpret_cast<double2 *>(p) = make_double2(o[0], o[1]);
+    else
+      p[0] = o[0];
+  }
+};
+
+template <int V>
 __global__ void k_newton_update(int n, int s, StageConsts QR, StageConsts A, double dt,
                                 const double *__restrict__ Y, const double *__restrict__ u,
                                 double *__restrict__ K, double *__restrict__ U) {
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-    double yv[MAXS], kv[MAXS];
+  const int np = n / V;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < np; q += gridDim.x * blockDim.x) {
+    const size_t p = (size_t)q * V;
+    double yv[MAXS][V], kv[MAXS][V], up[V];
 #pragma unroll
     for (int k = 0; k < MAXS; ++k)
-      if (k < s) yv[k] = Y[(size_t)k * n + p];
+      if (k < s) Vx<V>::ld(Y + (size_t)k * n + p, yv[k]);
 #pragma unroll
     for (int i = 0; i < MAXS; ++i) {
       if (i < s) {
-        double acc = 0.0;
+        Vx<V>::ld(K + (size_t)i * n + p, kv[i]);
 #pragma unroll
-        for (int k = 0; k < MAXS; ++k)
-          if (k < s) acc += QR.a[i * MAXS + k] * yv[k];
-        kv[i] = K[(size_t)i * n + p] + acc;
-        K[(size_t)i * n + p] = kv[i];
+        for (int e = 0; e < V; ++e) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < MAXS; ++k)
+            if (k < s) acc += QR.a[i * MAXS + k] * yv[k][e];
+          kv[i][e] = kv[i][e] + acc;
+        }
+        Vx<V>::st(K + (size_t)i * n + p, kv[i]);
       }
     }
-    const double up = u[p];
+    Vx<V>::ld(u + p, up);
 #pragma unroll
     for (int i = 0; i < MAXS; ++i) {
       if (i < s) {
-        double acc = 0.0;
+        double o[V];
 #pragma unroll
-        for (int j = 0; j < MAXS; ++j)
-          if (j < s) acc += A.a[i * MAXS + j] * kv[j];
-        U[(size_t)i * n + p] = up + dt * acc;
+        for (int e = 0; e < V; ++e) {
+          double acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < MAXS; ++j)
+            if (j < s) acc += A.a[i * MAXS + j] * kv[j][e];
+          o[e] = up[e] + dt * acc;
+        }
+        Vx<V>::st(U + (size_t)i * n + p, o);
       }
     }
   }
 }
 
+template <int V>
 __global__ void k_stage_values(int n, int s, const double *__restrict__ u,
                                const double *__restrict__ K, StageConsts A, double dt,
                                double *__restrict__ U) {
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-    double kv[MAXS];
+  const int np = n / V;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < np; q += gridDim.x * blockDim.x) {
+    const size_t p = (size_t)q * V;
+    double kv[MAXS][V], up[V];
 #pragma unroll
     for (int j = 0; j < MAXS; ++j)
-      if (j < s) kv[j] = K[(size_t)j * n + p];
-    const double up = u[p];
+      if (j < s) Vx<V>::ld(K + (size_t)j * n + p, kv[j]);
+    Vx<V>::ld(u + p, up);
 #pragma unroll
     for (int i = 0; i < MAXS; ++i) {
       if (i < s) {
-        double acc = 0.0;
+        double o[V];
 #pragma unroll
-        for (int j = 0; j < MAXS; ++j)
-          if (j < s) acc += A.a[i * MAXS + j] * kv[j];
-        U[(size_t)i * n + p] = up + dt * acc;
+        for (int e = 0; e < V; ++e) {
+          double acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < MAXS; ++j)
+            if (j < s) acc += A.a[i * MAXS + j] * kv[j][e];
+          o[e] = up[e] + dt * acc;
+        }
+        Vx<V>::st(U + (size_t)i * n + p, o);
       }
     }
   }
@@ -191,24 +233,30 @@ __global__ void k_opfields(int n, KindParams kp, OpWeights W, const double *__re
 
 // out_i = sum_k M[i][k] in_k  (pointwise s x s mix; g = Q^T F, dk = (Q R0) y)
 // mode 0: out = M in; mode 1: out += M in (Newton update K += dk)
+template <int V>
 __global__ void k_stage_mix(int n, int s, StageConsts M, const double *__restrict__ in,
                             double *__restrict__ out, int accumulate) {
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-    double v[MAXS];
+  const int np = n / V;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < np; q += gridDim.x * blockDim.x) {
+    const size_t p = (size_t)q * V;
+    double v[MAXS][V];
 #pragma unroll
     for (int k = 0; k < MAXS; ++k)
-      if (k < s) v[k] = in[(size_t)k * n + p];
+      if (k < s) Vx<V>::ld(in + (size_t)k * n + p, v[k]);
 #pragma unroll
     for (int i = 0; i < MAXS; ++i) {
       if (i < s) {
-        double acc = 0.0;
+        double o[V];
+        if (accumulate) Vx<V>::ld(out + (size_t)i * n + p, o);
 #pragma unroll
-        for (int k = 0; k < MAXS; ++k)
-          if (k < s) acc += M.a[i * MAXS + k] * v[k];
-        if (accumulate)
-          out[(size_t)i * n + p] += acc;
-        else
-          out[(size_t)i * n + p] = acc;
+        for (int e = 0; e < V; ++e) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < MAXS; ++k)
+            if (k < s) acc += M.a[i * MAXS + k] * v[k][e];
+          o[e] = accumulate ? o[e] + acc : acc;
+        }
+        Vx<V>::st(out + (size_t)i * n + p, o);
       }
     }
   }
@@ -630,6 +678,13 @@ static void dispatch_kd(int kind, int ndim, F f) {
   });
 }
 
+// pair (double2) path of the stage-space kernels: even row length and
+// 16-byte-aligned stage rows
+static bool pair_ok(long long n, const void *a, const void *b, const void *c, const void *d) {
+  auto al = [](const void *p) { return ((uintptr_t)p & 15u) == 0; };
+  return n % 2 == 0 && al(a) && al(b) && al(c) && al(d);
+}
+
 int Engine::grid_for(long long n) const {
   long long b = (n + 255) / 256;
   long long cap = (long long)sms * 8;
@@ -664,7 +719,10 @@ void Engine::newton_update(const double *QR_rowmajor_s, double dt, const double 
       QR.a[i * MAXS + j] = QR_rowmajor_s[i * s + j];
       A.a[i * MAXS + j] = tab.a0[i * IRKG_MAX_STAGES + j];
     }
-  k_newton_update<<<grid_for(N), 256, 0, stream>>>((int)N, s, QR, A, dt, Yv, u, K, Uo);
+  if (pair_ok(N, Yv, u, K, Uo))
+    k_newton_update<2><<<grid_for(N / 2), 256, 0, stream>>>((int)N, s, QR, A, dt, Yv, u, K, Uo);
+  else
+    k_newton_update<1><<<grid_for(N), 256, 0, stream>>>((int)N, s, QR, A, dt, Yv, u, K, Uo);
   count(1);
 }
 
@@ -684,7 +742,10 @@ void Engine::stage_values_n(const double *u, const double *K, double dt, double 
   A.s = s;
   for (int i = 0; i < s; ++i)
     for (int j = 0; j < s; ++j) A.a[i * MAXS + j] = tab.a0[i * IRKG_MAX_STAGES + j];
-  k_stage_values<<<grid_for(n), 256, 0, stream>>>((int)n, s, u, K, A, dt, Uo);
+  if (pair_ok(n, u, K, Uo, Uo))
+    k_stage_values<2><<<grid_for(n / 2), 256, 0, stream>>>((int)n, s, u, K, A, dt, Uo);
+  else
+    k_stage_values<1><<<grid_for(n), 256, 0, stream>>>((int)n, s, u, K, A, dt, Uo);
   count(1);
 }
 
@@ -719,7 +780,10 @@ void Engine::stage_mix_n(const double *M_rowmajor_s, const double *in, double *o
   M.s = s;
   for (int i = 0; i < s; ++i)
     for (int k = 0; k < s; ++k) M.a[i * MAXS + k] = M_rowmajor_s[i * s + k];
-  k_stage_mix<<<grid_for(n), 256, 0, stream>>>((int)n, s, M, in, out, accumulate ? 1 : 0);
+  if (pair_ok(n, in, out, out, out))
+    k_stage_mix<2><<<grid_for(n / 2), 256, 0, stream>>>((int)n, s, M, in, out, accumulate ? 1 : 0);
+  else
+    k_stage_mix<1><<<grid_for(n), 256, 0, stream>>>((int)n, s, M, in, out, accumulate ? 1 : 0);
   count(1);
 }
 
