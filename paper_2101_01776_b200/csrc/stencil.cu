@@ -408,6 +408,10 @@ __global__ void __launch_bounds__(BPW * 32)
     };
 #pragma unroll
     for (int i = 0; i < BRING - 1; ++i) issue_row(y0 - 1 + i);  // rows y0-1 .. y0+BRING-3
+    // per-row coefficient combinations of rows s-1, s, s+1 slide down the band
+    // in registers: each row's combination is formed once, not three times
+    double qtm[2], rtm[2], qbm[2], rbm[2], qtc[2], rtc[2], qbc[2], rbc[2], qtp[2], rtp[2],
+        qbp[2], rbp[2];
     for (int s = y0; s < y1; ++s) {
       cp_async_wait<BRING - 4>();  // rows up to s+1 have landed (s+2 .. s+BRING-3 may pend)
       // The operator is linear in its coefficient fields, so the four
@@ -455,10 +459,10 @@ __global__ void __launch_bounds__(BPW * 32)
           }
         }
       };
-      double qtm[2], rtm[2], qbm[2], rbm[2], qtc[2], rtc[2], qbc[2], rbc[2], qtp[2], rtp[2],
-          qbp[2], rbp[2];
-      combo(s - 1, qtm, rtm, qbm, rbm);
-      combo(s, qtc, rtc, qbc, rbc);
+      if (s == y0) {
+        combo(s - 1, qtm, rtm, qbm, rbm);
+        combo(s, qtc, rtc, qbc, rbc);
+      }
       combo(s + 1, qtp, rtp, qbp, rbp);
       // x-neighbours of a row-s combination (lane-1's second / lane+1's first column)
       auto lap = [&](const double (&m)[2], const double (&c)[2], const double (&p)[2], double out[2]) {
@@ -531,6 +535,17 @@ __global__ void __launch_bounds__(BPW * 32)
         }
         *reinterpret_cast<double2 *>(w + p) = make_double2(top[0], top[1]);
         if (SIZE == 2) *reinterpret_cast<double2 *>(w + p + n) = make_double2(bot[0], bot[1]);
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        qtm[c] = qtc[c];
+        rtm[c] = rtc[c];
+        qbm[c] = qbc[c];
+        rbm[c] = rbc[c];
+        qtc[c] = qtp[c];
+        rtc[c] = rtp[c];
+        qbc[c] = qbp[c];
+        rbc[c] = rbp[c];
       }
       issue_row(s + BRING - 2);  // into the slot of row s-2 (no longer read)
     }
