@@ -52,6 +52,7 @@ __device__ __forceinline__ double fold_partials(const double *part, int l, int G
 template <int BS>
 __global__ void k_norm2(int n, const double *__restrict__ x, double *part, int G, double *out,
                         unsigned *counter, const GCtrl *ctrl) {
+  pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
   __shared__ double sm[32];
   if (ctrl && ctrl->cycle_done) return;
   double acc = 0.0;
@@ -103,6 +104,7 @@ template <int V>
 __global__ void k_newton_update(int n, int s, StageConsts QR, StageConsts A, double dt,
                                 const double *__restrict__ Y, const double *__restrict__ u,
                                 double *__restrict__ K, double *__restrict__ U) {
+  pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
   const int np = n / V;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < np; q += gridDim.x * blockDim.x) {
     const size_t p = (size_t)q * V;
@@ -148,6 +150,7 @@ template <int V>
 __global__ void k_stage_values(int n, int s, const double *__restrict__ u,
                                const double *__restrict__ K, StageConsts A, double dt,
                                double *__restrict__ U) {
+  pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
   const int np = n / V;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < np; q += gridDim.x * blockDim.x) {
     const size_t p = (size_t)q * V;
@@ -212,6 +215,7 @@ __global__ void k_residual(Grid g, KindParams kp, int s, const double *__restric
 template <int KIND>
 __global__ void k_opfields(int n, KindParams kp, OpWeights W, const double *__restrict__ U,
                            double *__restrict__ A) {
+  pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
     double f[MAXS];
 #pragma unroll
@@ -236,6 +240,7 @@ __global__ void k_opfields(int n, KindParams kp, OpWeights W, const double *__re
 template <int V>
 __global__ void k_stage_mix(int n, int s, StageConsts M, const double *__restrict__ in,
                             double *__restrict__ out, int accumulate) {
+  pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
   const int np = n / V;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < np; q += gridDim.x * blockDim.x) {
     const size_t p = (size_t)q * V;
@@ -265,6 +270,7 @@ __global__ void k_stage_mix(int n, int s, StageConsts M, const double *__restric
 // u <- u + dt * sum_i b_i K_i  (src/nonlinear.py:313)
 __global__ void k_step_update(int n, int s, StageConsts B, double dt, const double *__restrict__ K,
                               double *__restrict__ u) {
+  pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
     double acc = 0.0;
 #pragma unroll
@@ -512,6 +518,8 @@ __global__ void k_mupdate(int n, double *__restrict__ V, long long pitch,
 // no host round trip before the first cycle.  b = 0 is converged at once
 // (src/sparsela.py:193-198); the cycles then run as no-ops.
 __global__ void k_gmres_init(GWork W, const double *bn2, int maxit, double rtol) {
+  pdl_wait();  // (launched with programmatic stream serialisation)
+  pdl_trigger();
   GCtrl *c = W.ctrl;
   const double bnorm = sqrt(*bn2);
   GCtrl z{};
@@ -526,6 +534,8 @@ __global__ void k_gmres_init(GWork W, const double *bn2, int maxit, double rtol)
 }
 
 __global__ void k_cycle_init(GWork W, int m) {
+  pdl_wait();  // (launched with programmatic stream serialisation)
+  pdl_trigger();
   GCtrl *c = W.ctrl;
   if (c->bnorm == 0.0) {  // zero right-hand side: nothing to iterate
     c->k = 0;
@@ -596,6 +606,8 @@ __global__ void k_arnoldi_finish(GWork W) {
 // column i is applied, so the k sequential steps cost two barriers each
 // instead of k dependent global loads.
 __global__ void __launch_bounds__(MAXR) k_backsolve(GWork W) {
+  pdl_wait();  // (launched with programmatic stream serialisation)
+  pdl_trigger();
   __shared__ double ybc;
   const GCtrl *c = W.ctrl;
   const int k = c->k;
@@ -624,6 +636,7 @@ __global__ void __launch_bounds__(MAXR) k_backsolve(GWork W) {
 // out = sum_{l<k} s_l * coef_l
 __global__ void k_vcombine(int n, const double *__restrict__ V, long long pitch, const GCtrl *ctrl,
                            const double *__restrict__ coef, double *__restrict__ out) {
+  pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
   const int k = ctrl->k;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     double a0 = 0.0, a1 = 0.0;
@@ -638,12 +651,15 @@ __global__ void k_vcombine(int n, const double *__restrict__ V, long long pitch,
 }
 
 __global__ void k_axpy(int n, double a, const double *__restrict__ x, double *__restrict__ y) {
+  pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
     y[r] = y[r] + a * x[r];
 }
 
 // True residual bookkeeping after x += Z y (src/sparsela.py:263-272).
 __global__ void k_cycle_end(GWork W) {
+  pdl_wait();  // (launched with programmatic stream serialisation)
+  pdl_trigger();
   GCtrl *c = W.ctrl;
   if (c->bnorm == 0.0) return;
   double rn = sqrt(c->rr);
@@ -701,7 +717,7 @@ void Engine::count(int k) {
 }
 
 double Engine::norm2(const double *x, long long n, const GCtrl *skip) {
-  k_norm2<256><<<G, 256, 0, stream>>>((int)n, x, part, G, &scal_dev[0], counter, skip);
+  launch_pdl(k_norm2<256>, dim3(G), dim3(256), 0, (int)n, x, part, G, &scal_dev[0], counter, skip);
   count(1);
   allreduce(&scal_dev[0], 1);
   double v = 0.0;
@@ -720,15 +736,18 @@ void Engine::newton_update(const double *QR_rowmajor_s, double dt, const double 
       A.a[i * MAXS + j] = tab.a0[i * IRKG_MAX_STAGES + j];
     }
   if (pair_ok(N, Yv, u, K, Uo))
-    k_newton_update<2><<<grid_for(N / 2), 256, 0, stream>>>((int)N, s, QR, A, dt, Yv, u, K, Uo);
+    launch_pdl(k_newton_update<2>, dim3(grid_for(N / 2)), dim3(256), 0, (int)N, s, QR, A, dt, Yv, u,
+               K, Uo);
   else
-    k_newton_update<1><<<grid_for(N), 256, 0, stream>>>((int)N, s, QR, A, dt, Yv, u, K, Uo);
+    launch_pdl(k_newton_update<1>, dim3(grid_for(N)), dim3(256), 0, (int)N, s, QR, A, dt, Yv, u, K,
+               Uo);
   count(1);
 }
 
 // sum of squares into scal_dev[0] (all ranks), no host round trip
 void Engine::norm2_dev(const double *x, long long n) {
-  k_norm2<256><<<G, 256, 0, stream>>>((int)n, x, part, G, &scal_dev[0], counter, nullptr);
+  launch_pdl(k_norm2<256>, dim3(G), dim3(256), 0, (int)n, x, part, G, &scal_dev[0], counter,
+             (const GCtrl *)nullptr);
   count(1);
   allreduce(&scal_dev[0], 1);
 }
@@ -743,9 +762,9 @@ void Engine::stage_values_n(const double *u, const double *K, double dt, double 
   for (int i = 0; i < s; ++i)
     for (int j = 0; j < s; ++j) A.a[i * MAXS + j] = tab.a0[i * IRKG_MAX_STAGES + j];
   if (pair_ok(n, u, K, Uo, Uo))
-    k_stage_values<2><<<grid_for(n / 2), 256, 0, stream>>>((int)n, s, u, K, A, dt, Uo);
+    launch_pdl(k_stage_values<2>, dim3(grid_for(n / 2)), dim3(256), 0, (int)n, s, u, K, A, dt, Uo);
   else
-    k_stage_values<1><<<grid_for(n), 256, 0, stream>>>((int)n, s, u, K, A, dt, Uo);
+    launch_pdl(k_stage_values<1>, dim3(grid_for(n)), dim3(256), 0, (int)n, s, u, K, A, dt, Uo);
   count(1);
 }
 
@@ -765,7 +784,8 @@ double Engine::residual(const double *U, const double *K, double *F, int nst) {
 
 void Engine::opfields(const double *U, const OpWeights &W, double *A) {
   dispatch_kind(prob.kind, [&](auto KD) {
-    k_opfields<decltype(KD)::value><<<grid_for(N), 256, 0, stream>>>((int)N, kp, W, U, A);
+    launch_pdl(k_opfields<decltype(KD)::value>, dim3(grid_for(N)), dim3(256), 0, (int)N, kp, W, U,
+               A);
   });
   count(1);
 }
@@ -781,9 +801,11 @@ void Engine::stage_mix_n(const double *M_rowmajor_s, const double *in, double *o
   for (int i = 0; i < s; ++i)
     for (int k = 0; k < s; ++k) M.a[i * MAXS + k] = M_rowmajor_s[i * s + k];
   if (pair_ok(n, in, out, out, out))
-    k_stage_mix<2><<<grid_for(n / 2), 256, 0, stream>>>((int)n, s, M, in, out, accumulate ? 1 : 0);
+    launch_pdl(k_stage_mix<2>, dim3(grid_for(n / 2)), dim3(256), 0, (int)n, s, M, in, out,
+               accumulate ? 1 : 0);
   else
-    k_stage_mix<1><<<grid_for(n), 256, 0, stream>>>((int)n, s, M, in, out, accumulate ? 1 : 0);
+    launch_pdl(k_stage_mix<1>, dim3(grid_for(n)), dim3(256), 0, (int)n, s, M, in, out,
+               accumulate ? 1 : 0);
   count(1);
 }
 
@@ -793,7 +815,7 @@ void Engine::step_update_n(double dt, const double *K, double *u, long long n) {
   StageConsts B{};
   B.s = s;
   for (int i = 0; i < s; ++i) B.v[i] = tab.b0[i];
-  k_step_update<<<grid_for(n), 256, 0, stream>>>((int)n, s, B, dt, K, u);
+  launch_pdl(k_step_update, dim3(grid_for(n)), dim3(256), 0, (int)n, s, B, dt, K, u);
   count(1);
 }
 
@@ -932,11 +954,11 @@ void Engine::mupdate(long long n, const double *coef, const double *w, double *o
 }
 
 void Engine::gmres_init(int maxit, double rtol) {
-  k_gmres_init<<<1, 1, 0, stream>>>(W, &scal_dev[0], maxit, rtol);
+  launch_pdl(k_gmres_init, dim3(1), dim3(1), 0, W, (const double *)&scal_dev[0], maxit, rtol);
   count(1);
 }
 void Engine::cycle_init(int m) {
-  k_cycle_init<<<1, 1, 0, stream>>>(W, m);
+  launch_pdl(k_cycle_init, dim3(1), dim3(1), 0, W, m);
   count(1);
 }
 void Engine::arnoldi_finish() {
@@ -944,19 +966,21 @@ void Engine::arnoldi_finish() {
   count(1);
 }
 void Engine::backsolve() {
-  k_backsolve<<<1, MAXR, 0, stream>>>(W);
+  launch_pdl(k_backsolve, dim3(1), dim3(MAXR), 0, W);
   count(1);
 }
 void Engine::vcombine(long long n, const double *coef, double *out) {
+  // (plain launch: with the PDL launch's maximum shared-memory carveout the
+  // basis combination ran 25 % slower -- it streams its slots through L1)
   k_vcombine<<<grid_for(n), 256, 0, stream>>>((int)n, V, vpitch, ctrl_dev, coef, out);
   count(1);
 }
 void Engine::axpy(long long n, double a, const double *x, double *y) {
-  k_axpy<<<grid_for(n), 256, 0, stream>>>((int)n, a, x, y);
+  launch_pdl(k_axpy, dim3(grid_for(n)), dim3(256), 0, (int)n, a, x, y);
   count(1);
 }
 void Engine::cycle_end() {
-  k_cycle_end<<<1, 1, 0, stream>>>(W);
+  launch_pdl(k_cycle_end, dim3(1), dim3(1), 0, W);
   count(1);
 }
 

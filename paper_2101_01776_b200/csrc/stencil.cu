@@ -564,6 +564,7 @@ __global__ void __launch_bounds__(SBX)
     k_residual_s(Grid g, KindParams kp, int s_st, const double *__restrict__ U, StageGhosts ug,
                  const double *__restrict__ K, double *__restrict__ F, int span, double *part,
                  unsigned *counter, double *out) {
+  pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
   const int n = g.n;
   int ix, iy;
   const int q = column_q<NDIM>(g, ix, iy);
@@ -625,6 +626,7 @@ template <int KIND, int NDIM>
 __global__ void __launch_bounds__(SBX)
     k_backsub_s(Grid g, KindParams kp, double dt, BacksubTerms T, const double *__restrict__ gst,
                 const double *__restrict__ y, double *__restrict__ rhs, int span) {
+  pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
   const int n = g.n;
   int ix, iy;
   const int q = column_q<NDIM>(g, ix, iy);
@@ -784,8 +786,8 @@ void Engine::backsub_s(double dt, BacksubTerms T, const double *gst, const doubl
     for (int r = 0; r < T.rows; ++r) T.od[r][qq] = opref(T.od[r][qq]);
   }
   dispatch_kd23(prob.kind, ndim, [&](auto KD, auto ND) {
-    k_backsub_s<decltype(KD)::value, decltype(ND)::value>
-        <<<gr, SBX, 0, stream>>>(grid, kp, dt, T, gst, y, rhs, span);
+    launch_pdl(k_backsub_s<decltype(KD)::value, decltype(ND)::value>, gr, dim3(SBX), 0, grid, kp, dt,
+               T, gst, y, rhs, span);
   });
   count(1);
 }
@@ -796,9 +798,8 @@ double Engine::residual_s(const double *Ust, const double *K, double *Fo, int ns
   if (slab())
     for (int i = 0; i < nst; ++i) exchange(R_STAGE + i, Ust + (size_t)i * N, 1);
   dispatch_kd23(prob.kind, ndim, [&](auto KD, auto ND) {
-    k_residual_s<decltype(KD)::value, decltype(ND)::value>
-        <<<gr, SBX, 0, stream>>>(grid, kp, nst, Ust, stage_ghosts(Ust, N, nst), K, Fo, span, part,
-                                 counter, &scal_dev[0]);
+    launch_pdl(k_residual_s<decltype(KD)::value, decltype(ND)::value>, gr, dim3(SBX), 0, grid, kp,
+               nst, Ust, stage_ghosts(Ust, N, nst), K, Fo, span, part, counter, &scal_dev[0]);
   });
   count(1);
   allreduce(&scal_dev[0], 1);
