@@ -258,6 +258,17 @@ def run_dae_case(name, n, family, s, nsteps, dt=1e-3, nu=1e-4):
           f"krylov={[x['krylov_iterations'] for x in steps]}")
 
 
+def run_larger():
+    """The BASELINE configs at larger reduced grids (reference runs of tens of
+    seconds): closer to the full-size Krylov counts than the small cases."""
+    sp1 = baseline_config(1, n=256, nsteps=2)
+    run_case("cfg1_n256", sp1.problem, sp1.u0(), "gauss", 3, sp1.dt, 2, sp1.solver)
+    sp2 = baseline_config(2, n=256, nsteps=1)
+    run_case("cfg2_gauss2_n256", sp2.problem, sp2.u0(), "gauss", 2, sp2.dt, 1, sp2.solver)
+    sp3 = baseline_config(3, n=32, nsteps=1)
+    run_case("cfg3_n32", sp3.problem, sp3.u0(), "gauss", 5, sp3.dt, 1, sp3.solver)
+
+
 def run_dae():
     run_dae_case("dae_n16_gauss2", 16, "gauss", 2, 3)
     run_dae_case("dae_n64_gauss2", 64, "gauss", 2, 4)
@@ -266,9 +277,11 @@ def run_dae():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tableaux", "transformed", "configs", "dae", "sdirk"]
+    which = sys.argv[1:] or ["tableaux", "transformed", "configs", "dae", "sdirk", "larger"]
     if "dae" in which:
         run_dae()
+    if "larger" in which:
+        run_larger()
     if "tableaux" in which:
         dump_tableaux()
     if "transformed" in which:
