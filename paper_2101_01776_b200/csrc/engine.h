@@ -323,15 +323,11 @@ struct Engine {
   void precond(const BlockSpec &B, const void *vin, double *z, const GCtrl *skip);
   void block_op(const BlockSpec &B, const double *z, double *w, const double *b,
                 double *out_norm, const GCtrl *skip);
-  void mdot(long long n, const double *w, double *out_c, double *out_norm);
-  void mupdate(long long n, const double *coef, const double *w, double *out, bool to_next,
-               double *out_norm);
   void cycle_init(int m);
   void gmres_init(int maxit, double rtol);
   void norm2_dev(const double *x, long long n);
   void newton_update(const double *QR_rowmajor_s, double dt, const double *Yv, const double *u,
                      double *K, double *Uo);
-  void arnoldi_finish();
   void backsolve();
   void vcombine(long long n, const double *coef, double *out);
   void axpy(long long n, double a, const double *x, double *y);

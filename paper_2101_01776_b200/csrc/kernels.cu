@@ -421,95 +421,7 @@ __global__ void k_block_op(Grid g, KindParams kp, double eta, double beta, doubl
 
 // ----------------------------------------------------------- CGS2 sweeps
 
-// c_l = alpha_l * (s_l . w), l = 0..j  and  ||w||^2 (index j+1)
-// (src/sparsela.py:222, 225).  Each CTA owns a contiguous row chunk; warps
-// take disjoint l's; partials part[l*G + cta] folded by the last CTA.
-template <int BS>
-__global__ void k_mdot(int n, const double *__restrict__ V, long long pitch,
-                       const double *__restrict__ alpha, const GCtrl *ctrl,
-                       const double *__restrict__ w, double *part, int G, double *out_c,
-                       double *out_norm, unsigned *counter) {
-  __shared__ double acc[MAXR + 2];
-  if (ctrl->cycle_done) return;
-  const int L = ctrl->j + 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NW = BS / 32;
-  int chunk = (n + G - 1) / G;
-  chunk = (chunk + 31) & ~31;
-  const int r0 = blockIdx.x * chunk;
-  const int r1 = min(n, r0 + chunk);
-  const int nl = out_norm ? L + 1 : L;
-  for (int l = warp; l < nl; l += NW) {
-    const double *vl = (l == L) ? w : V + (size_t)l * pitch;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int r = r0 + lane;
-    for (; r + 96 < r1; r += 128) {
-      s0 += vl[r] * w[r];
-      s1 += vl[r + 32] * w[r + 32];
-      s2 += vl[r + 64] * w[r + 64];
-      s3 += vl[r + 96] * w[r + 96];
-    }
-    for (; r < r1; r += 32) s0 += vl[r] * w[r];
-    double s = warp_sum((s0 + s1) + (s2 + s3));
-    if (lane == 0) acc[l] = s;
-  }
-  __syncthreads();
-  for (int l = threadIdx.x; l < nl; l += BS) part[(size_t)l * G + blockIdx.x] = acc[l];
-  if (!last_block(counter, G)) return;
-  for (int l = warp; l < nl; l += NW) {
-    double s = fold_partials(part, l, G);
-    if (lane == 0) {
-      if (l == L)
-        *out_norm = s;
-      else
-        out_c[l] = alpha[l] * s;
-    }
-  }
-  if (threadIdx.x == 0) *counter = 0u;
-}
 
-// out = w - sum_l s_l (alpha_l c_l), l = 0..j  (src/sparsela.py:226); when
-// to_next_slot, out is basis slot j+1 and ||out||^2 is reduced (228).
-template <int BS>
-__global__ void k_mupdate(int n, double *__restrict__ V, long long pitch,
-                          const double *__restrict__ alpha, const GCtrl *ctrl,
-                          const double *__restrict__ coef, const double *w, double *out,
-                          int to_next_slot, double *part, int G, double *out_norm,
-                          unsigned *counter) {
-  __shared__ double cs[MAXR + 1];
-  __shared__ double sm[32];
-  if (ctrl->cycle_done) return;
-  const int L = ctrl->j + 1;
-  for (int l = threadIdx.x; l < L; l += BS) cs[l] = alpha[l] * coef[l];
-  __syncthreads();
-  double *o = to_next_slot ? V + (size_t)L * pitch : out;
-  double nrm = 0.0;
-  for (int r = blockIdx.x * BS + threadIdx.x; r < n; r += G * BS) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int l = 0;
-    for (; l + 4 <= L; l += 4) {
-      a0 += V[(size_t)l * pitch + r] * cs[l];
-      a1 += V[(size_t)(l + 1) * pitch + r] * cs[l + 1];
-      a2 += V[(size_t)(l + 2) * pitch + r] * cs[l + 2];
-      a3 += V[(size_t)(l + 3) * pitch + r] * cs[l + 3];
-    }
-    for (; l < L; ++l) a0 += V[(size_t)l * pitch + r] * cs[l];
-    double v = w[r] - ((a0 + a1) + (a2 + a3));
-    o[r] = v;
-    nrm += v * v;
-  }
-  if (!out_norm) return;
-  nrm = block_sum<BS>(nrm, sm);
-  if (threadIdx.x == 0) part[blockIdx.x] = nrm;
-  if (!last_block(counter, G)) return;
-  if (threadIdx.x < 32) {
-    double t = fold_partials(part, 0, G);
-    if (threadIdx.x == 0) {
-      *out_norm = t;
-      *counter = 0u;
-    }
-  }
-}
 
 // ------------------------------------------------------ scalar control
 
@@ -551,53 +463,6 @@ __global__ void k_cycle_init(GWork W, int m) {
   W.alpha[0] = 1.0 / c->beta;
 }
 
-// Finish Arnoldi column j: H column, breakdown test, Givens rotations,
-// residual estimate and the loop exit test (src/sparsela.py:227-256).
-__global__ void k_arnoldi_finish(GWork W) {
-  GCtrl *c = W.ctrl;
-  if (c->cycle_done) return;
-  const int j = c->j;
-  double *h = W.H + (size_t)j * (MAXR + 1);
-  for (int i = 0; i <= j; ++i) h[i] = (0.0 + W.c1[i]) + W.c2[i];
-  const double hj = sqrt(c->hn2);
-  const double wnorm0 = sqrt(c->wn2);
-  h[j + 1] = hj;
-  bool breakdown = hj <= 1e-14 * fmax(wnorm0, 1e-300);
-  if (!breakdown) W.alpha[j + 1] = 1.0 / hj;
-  for (int i = 0; i < j; ++i) {
-    double tmp = W.cs[i] * h[i] + W.sn[i] * h[i + 1];
-    h[i + 1] = -W.sn[i] * h[i] + W.cs[i] * h[i + 1];
-    h[i] = tmp;
-  }
-  double denom = hypot(h[j], h[j + 1]);
-  if (denom == 0.0) {
-    // dead column: drop it and stop (src/sparsela.py:239-246)
-    c->breakdown = 1;
-    c->total_it += 1;
-    W.res[c->n_res] = W.res[c->n_res - 1];
-    c->n_res += 1;
-    c->k = j;
-    c->cycle_done = 1;
-    return;
-  }
-  W.cs[j] = h[j] / denom;
-  W.sn[j] = h[j + 1] / denom;
-  h[j] = denom;
-  h[j + 1] = 0.0;
-  W.g[j + 1] = -W.sn[j] * W.g[j];
-  W.g[j] = W.cs[j] * W.g[j];
-  c->total_it += 1;
-  double est = fabs(W.g[j + 1]) / c->bnorm;
-  W.res[c->n_res] = est;
-  c->n_res += 1;
-  if (breakdown) c->breakdown = 1;
-  if (est <= c->rtol || breakdown || c->total_it >= c->maxit || j + 1 >= c->m) {
-    c->k = j + 1;
-    c->cycle_done = 1;
-  } else {
-    c->j = j + 1;
-  }
-}
 
 // y = H(:k,:k)^{-1} g(:k) by back substitution (src/sparsela.py:258-261),
 // then fold alpha into y so that x += V (alpha .* y).
@@ -940,18 +805,7 @@ void Engine::block_op(const BlockSpec &B, const double *z, double *w, const doub
   count(1);
 }
 
-void Engine::mdot(long long n, const double *w, double *out_c, double *out_norm) {
-  k_mdot<256><<<G, 256, 0, stream>>>((int)n, V, vpitch, W.alpha, ctrl_dev, w, part, G, out_c,
-                                     out_norm, counter);
-  count(1);
-}
 
-void Engine::mupdate(long long n, const double *coef, const double *w, double *out,
-                     bool to_next, double *out_norm) {
-  k_mupdate<256><<<G, 256, 0, stream>>>((int)n, V, vpitch, W.alpha, ctrl_dev, coef, w, out,
-                                        to_next ? 1 : 0, part, G, out_norm, counter);
-  count(1);
-}
 
 void Engine::gmres_init(int maxit, double rtol) {
   launch_pdl(k_gmres_init, dim3(1), dim3(1), 0, W, (const double *)&scal_dev[0], maxit, rtol);
@@ -961,10 +815,7 @@ void Engine::cycle_init(int m) {
   launch_pdl(k_cycle_init, dim3(1), dim3(1), 0, W, m);
   count(1);
 }
-void Engine::arnoldi_finish() {
-  k_arnoldi_finish<<<1, 1, 0, stream>>>(W);
-  count(1);
-}
+
 void Engine::backsolve() {
   launch_pdl(k_backsolve, dim3(1), dim3(MAXR), 0, W);
   count(1);
