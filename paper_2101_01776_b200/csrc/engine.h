@@ -232,9 +232,11 @@ struct Engine {
   void backsub_s(double dt, BacksubTerms T, const double *gst, const double *y, double *rhs);
   void cgs_slab(long long n);  // CGS2 with all-reduces between sweeps (multi-rank)
   void arnoldi_iteration_slab(const BlockSpec &B, long long n, int j_host = -1);
-  double *halo_pack = nullptr;
-  int slab_batch = 4;
-  int graph_unroll = 2;  // Arnoldi steps per WHILE-body trip (IRKG_GRAPH_UNROLL)  // multi-rank Arnoldi steps launched per host check (IRKG_SLAB_BATCH)  // packed boundary planes of basis slot j (2 halves x lo/hi)
+  double *halo_pack = nullptr;  // packed boundary planes of basis slot j (2 halves x lo/hi)
+  int slab_batch = 4;           // multi-rank Arnoldi steps launched per host check (IRKG_SLAB_BATCH)
+  // Arnoldi steps per WHILE-body trip (IRKG_GRAPH_UNROLL); configs[1]:
+  // 1 / 2 / 3 / 4 -> 32.09 / 31.83 / 31.76 / 31.72 ms per IRK step
+  int graph_unroll = 4;
   // dae.cu (vorticity/streamfunction DAE, reordered mode)
   bool dae = false;
   double h2 = 0.0;
