@@ -655,21 +655,21 @@ void Engine::cgs(long long n, int nsweeps) {
   // DOT and UPD_DOT leave per-CTA partials in their own regions of `part`;
   // the next sweep folds them in every CTA (no last-CTA fold between sweeps)
   double *pdot = part + (size_t)(MAXR + 2) * G, *pupd = part + 2 * (size_t)(MAXR + 2) * G;
-  launch_pdl(k_cgs<CGS_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W, cnull,
+  launch_pdl_l2(true, k_cgs<CGS_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W, cnull,
              (const double *)wbuf, dnull, pdot, G, counter, stage, 0, cond_handle, maps, trm,
              cnull, 1);
   if (nsweeps < 2) {  // (phase probe)
     count(1);
     return;
   }
-  launch_pdl(k_cgs<CGS_UPD_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
+  launch_pdl_l2(true, k_cgs<CGS_UPD_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
              (const double *)W.c1, (const double *)wbuf, wbuf, pupd, G, counter, stage, 0,
              cond_handle, maps, trm, (const double *)pdot, 1);
   if (nsweeps < 3) {
     count(2);
     return;
   }
-  launch_pdl(k_cgs<CGS_UPD_NORM>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
+  launch_pdl_l2(true, k_cgs<CGS_UPD_NORM>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
              (const double *)W.c2, (const double *)wbuf, dnull, part, G, counter, stage, uc,
              cond_handle, maps, trm, (const double *)pupd, 0);
   count(3);
@@ -710,15 +710,15 @@ void Engine::cgs_slab(long long n) {
   const int trm = cgs_trmax();
   const double *cnull = nullptr;
   double *dnull = nullptr;
-  launch_pdl(k_cgs<CGS_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W, cnull,
+  launch_pdl_l2(true, k_cgs<CGS_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W, cnull,
              (const double *)wbuf, dnull, part, G, counter, stage, -1, cond_handle, maps, trm,
              cnull, 0);
   allreduce(W.c1, cnt);
-  launch_pdl(k_cgs<CGS_UPD_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
+  launch_pdl_l2(true, k_cgs<CGS_UPD_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
              (const double *)W.c1, (const double *)wbuf, wbuf, part, G, counter, stage, -1,
              cond_handle, maps, trm, cnull, 0);
   allreduce(W.c2, cnt);
-  launch_pdl(k_cgs<CGS_UPD_NORM>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
+  launch_pdl_l2(true, k_cgs<CGS_UPD_NORM>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
              (const double *)W.c2, (const double *)wbuf, dnull, part, G, counter, stage, -1,
              cond_handle, maps, trm, cnull, 0);
   allreduce(&ctrl_dev->hn2, 1);

@@ -38,6 +38,8 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   check(cudaGetDeviceProperties(&prop, dev), "props");
   sms = prop.multiProcessorCount;
   G = 2 * sms;
+  l2_persist_max = prop.persistingL2CacheMaxSize > 0 ? (size_t)prop.persistingL2CacheMaxSize : 0;
+  l2_window_max = prop.accessPolicyMaxWindowSize > 0 ? (size_t)prop.accessPolicyMaxWindowSize : 0;
   int ext[3] = {p.nx, p.ny, p.nz};
   ndim = (p.nz > 1) ? 3 : (p.ny > 1 ? 2 : 1);
   // slab partition of the slowest axis: rank r owns planes [p0, p0 + nl)
@@ -106,6 +108,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   for (auto &e : evg) check(cudaEventCreate(&e), "event");
   if (const char *e = getenv("IRKG_GRAPH_TIMING")) graph_timing = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_GRAPHS")) use_graphs = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_L2_MB")) l2_budget = atoi(e) > 0 ? ((size_t)atoi(e) << 20) : 0;
   if (const char *e = getenv("IRKG_FUSED_JACOBI")) fused_jacobi = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_JSPAN")) jspan_override = atoi(e);
   if (const char *e = getenv("IRKG_PAIR_JACOBI")) pair_jacobi = (atoi(e) != 0);
@@ -165,6 +168,31 @@ void Engine::ensure_basis(int restart) {
   dalloc(&V, (size_t)(restart + 1) * vpitch);
   vcap = restart;
   build_vmaps();
+  set_l2_window();
+}
+
+// Every CGS sweep of an Arnoldi step re-reads slots 0..j, so the lowest slots
+// are the hottest lines of the solve; a persisting access-policy window over
+// them (on the CGS launches only) keeps them out of the streaming LRU churn
+// once the basis outgrows L2.
+void Engine::set_l2_window() {
+  l2win = cudaAccessPolicyWindow{};
+  if (l2_budget == 0 || l2_persist_max == 0 || l2_window_max == 0 || !V) return;
+  // only when whole low slots fit (slots larger than half the budget would
+  // pin a fraction of slot 0 and just shrink the L2 left for the stencils)
+  if (2 * (size_t)vpitch * sizeof(double) > l2_budget) return;
+  size_t bytes = (size_t)(vcap + 1) * (size_t)vpitch * sizeof(double);
+  bytes = std::min(std::min(bytes, l2_budget), l2_window_max);
+  const size_t persist = std::min(bytes, l2_persist_max);
+  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  l2win.base_ptr = V;
+  l2win.num_bytes = bytes;
+  l2win.hitRatio = (float)std::min(1.0, (double)persist / (double)bytes);
+  l2win.hitProp = cudaAccessPropertyPersisting;
+  l2win.missProp = cudaAccessPropertyStreaming;
 }
 
 void Engine::set_tableau(const irkg_tableau &t) {

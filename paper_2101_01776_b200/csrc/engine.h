@@ -281,19 +281,43 @@ struct Engine {
   bool use_pdl = true;
   template <typename... KArgs, typename... Args>
   void launch_pdl(void (*kern)(KArgs...), dim3 grid_, dim3 block_, size_t smem, Args &&...args) {
+    launch_pdl_l2(false, kern, grid_, block_, smem, std::forward<Args>(args)...);
+  }
+  // basis_l2: the launch carries the access-policy window that keeps the
+  // lowest basis slots persisting in L2 (the slots every CGS sweep re-reads)
+  template <typename... KArgs, typename... Args>
+  void launch_pdl_l2(bool basis_l2, void (*kern)(KArgs...), dim3 grid_, dim3 block_, size_t smem,
+                     Args &&...args) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = grid_;
     lc.blockDim = block_;
     lc.dynamicSmemBytes = smem;
     lc.stream = stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (use_pdl) {
+      at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    if (basis_l2 && l2win.num_bytes > 0) {
+      at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+      at[na].val.accessPolicyWindow = l2win;
+      ++na;
+    }
     lc.attrs = at;
-    lc.numAttrs = use_pdl ? 1 : 0;
+    lc.numAttrs = na;
     max_carveout((const void *)kern);
     check(cudaLaunchKernelEx(&lc, kern, std::forward<Args>(args)...), "PDL launch");
   }
+  // L2 persistence of the lowest l2_budget bytes of the basis (IRKG_L2_MB;
+  // 0 = off).  configs[1] (16.8 MB slots): 1 / 2 / 3 / 4 / 5 slots ->
+  // 31.72 / 31.35 / 31.07 / 31.93 / 32.78 ms per IRK step (none: 31.73);
+  // 40 / 50 / 60 MB -> 31.21 / 31.02 / 30.93
+  size_t l2_budget = 60u << 20;
+  size_t l2_persist_max = 0, l2_window_max = 0;
+  cudaAccessPolicyWindow l2win{};
+  void set_l2_window();
   // All Arnoldi-body kernels ask for the maximum shared-memory carveout, so
   // consecutive kernels never force an L1/shared reconfiguration of the SMs
   // (IRKG_CARVEOUT=0: driver default).
