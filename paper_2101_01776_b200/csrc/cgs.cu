@@ -62,6 +62,22 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
       : "memory");
 }
 
+// the same with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void tma_load_1d_hint(void *dst, const void *src, uint32_t bytes,
+                                                 uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 // 2-D tile of the basis: box (rows x slots) at (row c0, slot c1), landing in
 // shared memory slot-major, i.e. exactly the stage layout
 __device__ __forceinline__ void tma_load_2d(void *dst, const void *map, int c0, int c1,
@@ -183,6 +199,7 @@ struct TileArgs {
   double *red;
   const char *maps;  // tensor maps of this tile height (null: 1-D copies)
   int rev;           // walk the row tiles last-to-first (L2 reuse between sweeps)
+  int ef_from;       // basis slots >= ef_from are read evict-first (1-D copies)
 };
 
 // Tile issue, out of line: one copy of the code for every tile height and
@@ -213,14 +230,21 @@ __device__ __noinline__ void issue_boxed(double *dst, const char *maps, const do
 // issue from one warp compiles to a serial waterfall).  Thread 0's expect_tx
 // may land after some copies complete (the tx-count goes transiently
 // negative); the phase cannot flip before its arrival.
+// Slots at or above ef_from (past the L2-persisting window: re-read only
+// after the whole basis has streamed through L2) go out evict-first, so they
+// do not displace the lines the next kernels reuse.
 __device__ __noinline__ void issue_slots(double *dst, const double *V, long long pitch,
                                          const double *win, int r0, int TR, int L, int warp,
-                                         uint64_t *bar, bool with_w) {
+                                         uint64_t *bar, bool with_w, int ef_from) {
   const uint32_t bytes = TR * 8u;
+  const uint64_t pol = evict_first_policy();
 #pragma unroll 1
   for (int l = warp; l <= L - (with_w ? 0 : 1); l += CGS_NW) {
     const double *src = (l < L) ? V + (size_t)l * pitch + r0 : win + r0;
-    tma_load_1d(dst + l * TR, src, bytes, bar);
+    if (l < L && l >= ef_from)
+      tma_load_1d_hint(dst + l * TR, src, bytes, bar, pol);
+    else
+      tma_load_1d(dst + l * TR, src, bytes, bar);
   }
 }
 
@@ -334,7 +358,8 @@ __device__ __forceinline__ void tile_issue(const TileArgs &A, int t, int s, bool
   } else {
     if (tid == 0) mbar_expect_tx(&A.bars[s], TRC * 8u * (uint32_t)(A.L + 1));
     if ((tid & 31) == 0)
-      issue_slots(dst, A.V, A.pitch, A.win, t * TRC, TRC, A.L, tid >> 5, &A.bars[s], with_w);
+      issue_slots(dst, A.V, A.pitch, A.win, t * TRC, TRC, A.L, tid >> 5, &A.bars[s], with_w,
+                  A.ef_from);
   }
 }
 
@@ -454,7 +479,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
     k_cgs(int n, double *__restrict__ V, long long pitch, GWork W, const double *cin,
           const double *win, double *wout, double *part, int G, unsigned *counter,
           int ring_doubles, int use_cond, cudaGraphConditionalHandle cond,
-          const char *__restrict__ vmaps, int trmax, const double *pin, int defer) {
+          const char *__restrict__ vmaps, int trmax, const double *pin, int defer, int ef_from) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bars[CGS_MAXST];
   __shared__ double cs[MAXR + 1];
@@ -491,7 +516,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   __syncthreads();
 
   TileArgs A{n, L, G, ntiles, V, pitch, win, out, sm, nst, bars, cs, red,
-             TR <= 256 ? vmaps : nullptr, (cgs_rev_mask >> MODE) & 1};
+             TR <= 256 ? vmaps : nullptr, (cgs_rev_mask >> MODE) & 1, ef_from};
   double nrm = 0.0;
   double acc[CGS_Q];
 #pragma unroll
@@ -625,6 +650,15 @@ static int cgs_trmax() {
   return v;
 }
 
+// First basis slot read evict-first: the slots past the L2-persisting window
+// (all of them when no window applies); IRKG_CGS_EF=0: none.
+int Engine::cgs_ef_from() const {
+  static int on = -1;
+  if (on < 0) on = getenv("IRKG_CGS_EF") ? (atoi(getenv("IRKG_CGS_EF")) != 0) : 1;
+  if (!on) return 1 << 30;
+  return (int)(l2win.num_bytes / ((size_t)vpitch * sizeof(double)));
+}
+
 // Shared-memory ring per CTA, in doubles: 2 x 52 KB (2 CTAs per SM) unless
 // the restart length needs two 32-row tiles of more slots.
 int Engine::cgs_stage_doubles() const {
@@ -649,6 +683,7 @@ void Engine::cgs(long long n, int nsweeps) {
   }
   const int uc = cond_active ? 1 : 0;
   const char *maps = cgs_maps(vmaps);
+  const int ef = cgs_ef_from();
   const int trm = cgs_trmax();
   const double *cnull = nullptr;
   double *dnull = nullptr;
@@ -657,21 +692,21 @@ void Engine::cgs(long long n, int nsweeps) {
   double *pdot = part + (size_t)(MAXR + 2) * G, *pupd = part + 2 * (size_t)(MAXR + 2) * G;
   launch_pdl_l2(true, k_cgs<CGS_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W, cnull,
              (const double *)wbuf, dnull, pdot, G, counter, stage, 0, cond_handle, maps, trm,
-             cnull, 1);
+             cnull, 1, ef);
   if (nsweeps < 2) {  // (phase probe)
     count(1);
     return;
   }
   launch_pdl_l2(true, k_cgs<CGS_UPD_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
              (const double *)W.c1, (const double *)wbuf, wbuf, pupd, G, counter, stage, 0,
-             cond_handle, maps, trm, (const double *)pdot, 1);
+             cond_handle, maps, trm, (const double *)pdot, 1, ef);
   if (nsweeps < 3) {
     count(2);
     return;
   }
   launch_pdl_l2(true, k_cgs<CGS_UPD_NORM>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
              (const double *)W.c2, (const double *)wbuf, dnull, part, G, counter, stage, uc,
-             cond_handle, maps, trm, (const double *)pupd, 0);
+             cond_handle, maps, trm, (const double *)pupd, 0, ef);
   count(3);
 }
 
@@ -707,20 +742,21 @@ void Engine::cgs_slab(long long n) {
   }
   const int cnt = vcap + 1;  // >= j + 2 for every j of the cycle
   const char *maps = cgs_maps(vmaps);
+  const int ef = cgs_ef_from();
   const int trm = cgs_trmax();
   const double *cnull = nullptr;
   double *dnull = nullptr;
   launch_pdl_l2(true, k_cgs<CGS_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W, cnull,
              (const double *)wbuf, dnull, part, G, counter, stage, -1, cond_handle, maps, trm,
-             cnull, 0);
+             cnull, 0, ef);
   allreduce(W.c1, cnt);
   launch_pdl_l2(true, k_cgs<CGS_UPD_DOT>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
              (const double *)W.c1, (const double *)wbuf, wbuf, part, G, counter, stage, -1,
-             cond_handle, maps, trm, cnull, 0);
+             cond_handle, maps, trm, cnull, 0, ef);
   allreduce(W.c2, cnt);
   launch_pdl_l2(true, k_cgs<CGS_UPD_NORM>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
              (const double *)W.c2, (const double *)wbuf, dnull, part, G, counter, stage, -1,
-             cond_handle, maps, trm, cnull, 0);
+             cond_handle, maps, trm, cnull, 0, ef);
   allreduce(&ctrl_dev->hn2, 1);
   k_arnoldi_finish_slab<<<1, 128, 0, stream>>>(W, cond_active ? 1 : 0, cond_handle);
   count(4);

@@ -318,6 +318,7 @@ struct Engine {
   size_t l2_persist_max = 0, l2_window_max = 0;
   cudaAccessPolicyWindow l2win{};
   void set_l2_window();
+  int cgs_ef_from() const;
   // All Arnoldi-body kernels ask for the maximum shared-memory carveout, so
   // consecutive kernels never force an L1/shared reconfiguration of the SMs
   // (IRKG_CARVEOUT=0: driver default).
