@@ -387,6 +387,31 @@ __device__ __forceinline__ void tile_load_tail(const TileArgs &A, double *buf, i
 // next sweep).
 __device__ __forceinline__ double fold_partials(const double *pl, int G, int lane) {
   double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;
+  constexpr int MAXK = 12;  // G <= 32 * MAXK: all of a lane's loads in flight at once
+  if (G <= 32 * MAXK) {
+    double v[MAXK];
+#pragma unroll
+    for (int k = 0; k < MAXK; ++k) {
+      const int c = lane + 32 * k;
+      v[k] = c < G ? __ldcg(pl + c) : 0.0;
+    }
+    // the association of the loop below: blocks of 4 strided values while
+    // c + 96 < G, then the tail into f0
+    int nb = 0;
+#pragma unroll
+    for (int b = 0; b < MAXK / 4; ++b)
+      if (nb == b && lane + 128 * b + 96 < G) {
+        f0 += v[4 * b];
+        f1 += v[4 * b + 1];
+        f2 += v[4 * b + 2];
+        f3 += v[4 * b + 3];
+        nb = b + 1;
+      }
+#pragma unroll
+    for (int k = 0; k < MAXK; ++k)
+      if (k >= 4 * nb && lane + 32 * k < G) f0 += v[k];
+    return wsum((f0 + f1) + (f2 + f3));
+  }
   int c = lane;
   for (; c + 96 < G; c += 128) {
     f0 += __ldcg(pl + c);

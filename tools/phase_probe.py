@@ -18,11 +18,13 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--js", default="0,2,4,8,12,16,24,32")
+    ap.add_argument("--block1", action="store_true",
+                    help="probe a 1x1 block (eta = 4.644371, configs[1]'s real eigenvalue)")
     args = ap.parse_args()
     import torch
 
     import paper_2101_01776_b200 as pk
-    from paper_2101_01776_b200.engine import Context
+    from paper_2101_01776_b200.engine import context_for
 
     spec = pk.baseline_config(args.config, n=args.n)
     tab = pk.make_tableau(spec.family, spec.s)
@@ -30,13 +32,21 @@ def main():
     cfg = pk.SolverConfig(variant=sv["variant"], krylov_maxit=sv["krylov_maxit"],
                           restart=sv["restart"], newton_maxit=sv["newton_maxit"],
                           precond=pk.PrecondSpec(inner=sv["inner"]))
-    ctx = Context(spec.problem, 0)
+    ctx = context_for(spec.problem)  # (block_gmres below shares it)
     ctx.set_prep(pk.prepare_stages(tab))
     ctx.set_config(cfg)
     u = torch.from_numpy(spec.u0()).cuda()
     # the last block solved in a step is the leading 2x2 block (reversed order)
     ctx.step_device(u, 0.0, spec.dt)
     torch.cuda.synchronize()
+    if args.block1:
+        import numpy as np
+
+        f = pk.OperatorField.linearize(spec.problem, u.cpu().numpy()[None, :])
+        rhs = np.random.default_rng(0).standard_normal(spec.problem.dim)
+        pk.block_gmres((4.644371, f, spec.dt), rhs, pk.PrecondSpec(inner=sv["inner"]), rtol=1e-5,
+                       maxit=200, restart=200)
+        torch.cuda.synchronize()
     lib, h = ctx.lib, ctx.h
 
     def probe(ph, j, reps=None):
@@ -49,7 +59,7 @@ def main():
         return out.value
 
     pin = probe(7, 0)
-    n2 = 2 * spec.problem.dim
+    n2 = (1 if args.block1 else 2) * spec.problem.dim
     mb = n2 * 8 / 1e6
     print(f"grid {spec.problem.shape}  2N vector = {mb:.1f} MB  pin kernel {pin:.2f} us")
     for name, ph in [("precond (2 chains)", 0), ("jacobi chain 1", 1), ("jacobi chain 2", 2),
