@@ -542,8 +542,7 @@ double Engine::dae_residual(const double *UW, const double *K2, double *F2) {
   count(1);
   allreduce(&scal_dev[0], 1);
   double v = 0.0;
-  check(cudaMemcpyAsync(&v, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost, stream));
-  check(cudaStreamSynchronize(stream));
+  v = read_scalar();
   return v;
 }
 
@@ -554,8 +553,7 @@ double Engine::dae_gnorm(const double *UW) {
   count(1);
   allreduce(&scal_dev[0], 1);
   double v = 0.0;
-  check(cudaMemcpyAsync(&v, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost, stream));
-  check(cudaStreamSynchronize(stream));
+  v = read_scalar();
   return std::sqrt(v);
 }
 

@@ -227,6 +227,15 @@ void Engine::ensure_res(int maxit) {
   rescap = maxit + 4;
 }
 
+// scal_dev[0] -> host through the pinned control-block mirror (a pageable
+// destination would make the runtime stage the copy)
+double Engine::read_scalar() {
+  check(cudaMemcpyAsync(&ctrl_host->scalar, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost,
+                        stream));
+  check(cudaStreamSynchronize(stream), "sync");
+  return ctrl_host->scalar;
+}
+
 void Engine::read_ctrl() {
   check(cudaMemcpyAsync(ctrl_host, ctrl_dev, sizeof(GCtrl), cudaMemcpyDeviceToHost, stream));
   check(cudaStreamSynchronize(stream), "sync");

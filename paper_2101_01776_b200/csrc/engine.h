@@ -365,6 +365,7 @@ struct Engine {
   bool have_last_block = false;
   double probe_phase(int phase, int j, int reps);
   void read_ctrl();
+  double read_scalar();
   int graph_body_kernels = 0;  // body size of the WHILE graph launched this cycle
   std::vector<double> qr_matrix() const;  // Q R0, row-major s x s
   // want_residuals = false: the residual history is copied back only when

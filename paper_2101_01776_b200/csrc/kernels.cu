@@ -586,8 +586,7 @@ double Engine::norm2(const double *x, long long n, const GCtrl *skip) {
   count(1);
   allreduce(&scal_dev[0], 1);
   double v = 0.0;
-  check(cudaMemcpyAsync(&v, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost, stream));
-  check(cudaStreamSynchronize(stream));
+  v = read_scalar();
   return v;
 }
 
@@ -642,8 +641,7 @@ double Engine::residual(const double *U, const double *K, double *F, int nst) {
   });
   count(1);
   double v = 0.0;
-  check(cudaMemcpyAsync(&v, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost, stream));
-  check(cudaStreamSynchronize(stream));
+  v = read_scalar();
   return v;
 }
 

@@ -804,8 +804,7 @@ double Engine::residual_s(const double *Ust, const double *K, double *Fo, int ns
   count(1);
   allreduce(&scal_dev[0], 1);
   double v = 0.0;
-  check(cudaMemcpyAsync(&v, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost, stream));
-  check(cudaStreamSynchronize(stream));
+  v = read_scalar();
   return v;
 }
 
