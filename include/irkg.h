@@ -152,6 +152,10 @@ typedef struct {
   double arnoldi_ms_1x1;
   double arnoldi_ms_2x2;
   double cycle_end_ms;
+  /* ... and the device idle time across the host round trips: residual norm
+   * read -> next Newton iteration, block solve end -> next block */
+  double newton_gap_ms;
+  double block_gap_ms;
 } irkg_counters;
 
 /* Host-callback transport for the slab partition (alternative to NCCL):

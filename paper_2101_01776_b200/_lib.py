@@ -130,6 +130,8 @@ class Counters(C.Structure):
         ("arnoldi_ms_1x1", C.c_double),
         ("arnoldi_ms_2x2", C.c_double),
         ("cycle_end_ms", C.c_double),
+        ("newton_gap_ms", C.c_double),
+        ("block_gap_ms", C.c_double),
     ]
 
 

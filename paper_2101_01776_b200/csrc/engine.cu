@@ -106,6 +106,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   check(cudaEventCreate(&evp[0]), "event");
   check(cudaEventCreate(&evp[1]), "event");
   for (auto &e : evg) check(cudaEventCreate(&e), "event");
+  for (auto &e : evh) check(cudaEventCreate(&e), "event");
   if (const char *e = getenv("IRKG_GRAPH_TIMING")) graph_timing = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_GRAPHS")) use_graphs = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_L2_MB")) l2_budget = atoi(e) > 0 ? ((size_t)atoi(e) << 20) : 0;
@@ -135,6 +136,8 @@ Engine::~Engine() {
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   for (auto e : evg)
+    if (e) cudaEventDestroy(e);
+  for (auto e : evh)
     if (e) cudaEventDestroy(e);
   drop_graphs();
   if (cap_stream) cudaStreamDestroy(cap_stream);
@@ -230,13 +233,31 @@ void Engine::ensure_res(int maxit) {
 // scal_dev[0] -> host through the pinned control-block mirror (a pageable
 // destination would make the runtime stage the copy)
 double Engine::read_scalar() {
+  gap_mark();
   check(cudaMemcpyAsync(&ctrl_host->scalar, &scal_dev[0], sizeof(double), cudaMemcpyDeviceToHost,
                         stream));
   check(cudaStreamSynchronize(stream), "sync");
   return ctrl_host->scalar;
 }
 
+void Engine::gap_mark() {
+  if (!graph_timing) return;
+  check(cudaEventRecord(evh[0], stream));
+  gap_armed = true;
+}
+
+void Engine::gap_close(double &acc) {
+  if (!graph_timing || !gap_armed) return;
+  check(cudaEventRecord(evh[1], stream));
+  check(cudaEventSynchronize(evh[1]), "sync");
+  float ms = 0.f;
+  check(cudaEventElapsedTime(&ms, evh[0], evh[1]), "elapsed");
+  acc += ms;
+  gap_armed = false;
+}
+
 void Engine::read_ctrl() {
+  gap_mark();
   check(cudaMemcpyAsync(ctrl_host, ctrl_dev, sizeof(GCtrl), cudaMemcpyDeviceToHost, stream));
   check(cudaStreamSynchronize(stream), "sync");
 }
@@ -700,6 +721,7 @@ void Engine::transformed_solve(double dt, const double *rhs, double *dk, irkg_st
         T.od[r][q] = op_of(od_slot[off + r][j]);
       }
     }
+    gap_close(counters.block_gap_ms);
     backsub(dt, T, Gs, Y, RHS);
     BlockSpec B{};
     B.size = size;
@@ -837,6 +859,7 @@ double Engine::probe_phase(int phase, int j, int reps) {
 // src/nonlinear.py:186-236.  K (s,N) in/out.
 void Engine::newton(const double *u, double *K, double t, double dt, irkg_step_stats *stats) {
   auto tic = std::chrono::steady_clock::now();
+  gap_armed = false;
   const std::vector<double> qrm = qr_matrix();
   stage_values(u, K, dt, U);
   double f0 = std::sqrt(residual(U, K, F));
@@ -855,6 +878,7 @@ void Engine::newton(const double *u, double *K, double t, double dt, irkg_step_s
       finish();
       return;
     }
+    gap_close(counters.newton_gap_ms);
     if (!have_ops || cfg.jacobian_refresh == 0) {
       build_linearization(U);  // U = u + dt A0 K at the current iterate
       stats->jacobian_assemblies += s;

@@ -160,6 +160,10 @@ struct Engine {
   GCtrl *ctrl_host = nullptr;   // pinned mirror
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evp[2] = {nullptr, nullptr};
   cudaEvent_t evg[3] = {nullptr, nullptr, nullptr};  // cycle graph / cycle end (IRKG_GRAPH_TIMING)
+  cudaEvent_t evh[2] = {nullptr, nullptr};  // host round-trip gaps (IRKG_GRAPH_TIMING)
+  bool gap_armed = false;
+  void gap_mark();              // before a host sync: the device work enqueued so far
+  void gap_close(double &acc);  // after it: first work of the next phase
   bool graph_timing = false;
 
   // current linearisation: operator slot per diag row and per offdiag key

@@ -57,12 +57,16 @@ def main():
     a1 = c1["arnoldi_ms_1x1"] - c0["arnoldi_ms_1x1"]
     a2 = c1["arnoldi_ms_2x2"] - c0["arnoldi_ms_2x2"]
     ce = c1["cycle_end_ms"] - c0["cycle_end_ms"]
+    ng = c1["newton_gap_ms"] - c0["newton_gap_ms"]
+    bg = c1["block_gap_ms"] - c0["block_gap_ms"]
     rest = total - a1 - a2 - ce
     print(f"{args.steps} steps, {newton} Newton iterations, Krylov its per block offset {its}")
     print(f"total device time     {total:9.2f} ms  ({total / args.steps:.2f} ms/step)")
     for name, v in [("Arnoldi graphs 2x2", a2), ("Arnoldi graphs 1x1", a1),
                     ("cycle ends", ce), ("rest (Newton, transforms, host)", rest)]:
         print(f"{name:32s} {v:9.2f} ms  {100 * v / total:5.1f} %")
+    print(f"  of which device idle across host round trips: Newton residual -> next iteration "
+          f"{ng:.2f} ms, block end -> next block {bg:.2f} ms")
     for off, n_it in sorted(its.items()):
         size = 2 if off == 0 else 1
         ms = a2 if size == 2 else a1
