@@ -396,7 +396,10 @@ def test_config1_full_size_first_step_properties():
     u0 = spec.u0()
     tab = pk.make_tableau("gauss", 3)
     cfg = _solver(spec.solver)
+    u0_before = u0.copy()
     u1, stats = pk.step(prob, u0, 0.0, spec.dt, tab, cfg)
+    # value semantics of the reference's step(): a new array, u untouched
+    assert u1 is not u0 and np.array_equal(u0, u0_before)
     assert stats.converged
     assert stats.residual_history[-1] <= 1e-9 * stats.residual_history[0]
     assert 3 <= stats.newton_iterations <= 10
