@@ -429,9 +429,6 @@ __global__ void __launch_bounds__(JPW * 32, 3)
     k_jacobi_sp2d(Grid g, Op L, JacCoef jc, VecIn vin, int in_off, FRef zcr, double cpl,
                   double *__restrict__ x_out, int span, int strips, int nwarps, GCtrl *flag_ctrl,
                   const GCtrl *skip) {
-  pdl_wait();  // inputs: v_j / z1 from the predecessors
-  pdl_trigger();
-  if (skip && skip->cycle_done) return;
   constexpr int H = K - 1;
   constexpr int HS = (H + 1) & ~1;
   constexpr int WC = 64 - 2 * HS;
@@ -441,8 +438,8 @@ __global__ void __launch_bounds__(JPW * 32, 3)
   const int gw = blockIdx.x * JPW + (threadIdx.x >> 5);
   if (gw >= nwarps) return;  // whole warp idle
   const int strip = gw % strips, band = gw / strips;
-  double scale;
-  const FRef inr = vin_resolve(vin, in_off, scale);
+  double scale = 1.0;
+  FRef inr{};  // v_j (the predecessor's output): resolved after pdl_wait()
   const FRef ar = fref(L);
   const bool has_zc = zcr.base != nullptr;
   const int lane = threadIdx.x & 31;
@@ -500,8 +497,30 @@ __global__ void __launch_bounds__(JPW * 32, 3)
     }
     cp_async_commit();
   };
+  // the operator-field rows of the first ring group go out before the
+  // dependency wait (no predecessor writes them; v_j / z1 only after it) --
+  // they join the first commit group
 #pragma unroll
-  for (int i = 0; i < JRING; ++i) issue_row(t0 + i, i);
+  for (int i = 0; i < JRING; ++i)
+    if (t0 + i < t1) cp_async16(ring + i * 3 * 64 + 2 * lane, rowp(ar, t0 + i) + c0);
+  pdl_wait();  // inputs: v_j / z1 from the predecessors
+  pdl_trigger();
+  if (skip && skip->cycle_done) {
+    cp_async_commit();
+    cp_async_wait<0>();
+    return;
+  }
+  inr = vin_resolve(vin, in_off, scale);
+#pragma unroll
+  for (int i = 0; i < JRING; ++i) {
+    const int t = t0 + i;
+    if (t < t1) {
+      double *d = ring + i * 3 * 64 + 2 * lane;
+      cp_async16(d + 64, rowp(inr, t) + c0);
+      if (has_zc) cp_async16(d + 128, rowp(zcr, t) + c0);
+    }
+    cp_async_commit();
+  }
 
   auto step = [&](int t, int slot) {
     cp_async_wait<JRING - 1>();

@@ -333,13 +333,15 @@ __global__ void __launch_bounds__(BPW * 32)
                      Op l1, Op l2, Op c12, Op c21, FRef z1r, FRef z2r, double *__restrict__ w,
                      const double *__restrict__ b, int span, int strips, int nwarps,
                      double *part, unsigned *counter, double *out_norm, const GCtrl *skip) {
-  pdl_wait();  // z from the preconditioner
-  pdl_trigger();
-  if (skip && skip->cycle_done) return;
   constexpr int NF = bop_nf<SIZE>();
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * BPW + (threadIdx.x >> 5);
   double nrm = 0.0;
+  if (gw >= nwarps) {  // idle warp: nothing to prefetch
+    pdl_wait();
+    pdl_trigger();
+    if (skip && skip->cycle_done) return;
+  }
   if (gw < nwarps) {
     const int nx = g.nx, ny = g.ny, n = g.n;
     const int strip = gw % strips, band = gw / strips;
@@ -406,8 +408,38 @@ __global__ void __launch_bounds__(BPW * 32)
     auto field_nb = [&](int f, int s, Nb &n0, Nb &n1) {
       nb2(rd(f, s - 1), rd(f, s), rd(f, s + 1), n0, n1);
     };
+    // coefficient fields (a1 [, a2, c12, c21]) are not written by the
+    // predecessors: their first rows go out before the dependency wait and
+    // join the first commit group; z1 [, z2] only after it
+    auto coef_field = [](int f) { return f == 1 || f == 3 || f == 4 || f == 5; };
 #pragma unroll
-    for (int i = 0; i < BRING - 1; ++i) issue_row(y0 - 1 + i);  // rows y0-1 .. y0+BRING-3
+    for (int i = 0; i < BRING - 1; ++i) {
+      const int t = y0 - 1 + i;
+      if (t <= y1) {
+        double *d = ring + ((t - y0 + 1) % BRING) * NF * 64;
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+          if (have[f] && coef_field(f)) cp_async16(d + f * 64, rowp(fr[f], t) + c0);
+      }
+    }
+    pdl_wait();  // z from the preconditioner
+    pdl_trigger();
+    if (skip && skip->cycle_done) {
+      cp_async_commit();
+      cp_async_wait<0>();
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < BRING - 1; ++i) {  // rows y0-1 .. y0+BRING-3
+      const int t = y0 - 1 + i;
+      if (t <= y1) {
+        double *d = ring + ((t - y0 + 1) % BRING) * NF * 64;
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+          if (have[f] && !coef_field(f)) cp_async16(d + f * 64, rowp(fr[f], t) + c0);
+      }
+      cp_async_commit();
+    }
     // per-row coefficient combinations of rows s-1, s, s+1 slide down the band
     // in registers: each row's combination is formed once, not three times
     double qtm[2], rtm[2], qbm[2], rbm[2], qtc[2], rtc[2], qbc[2], rbc[2], qtp[2], rtp[2],
