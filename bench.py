@@ -47,57 +47,101 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clocks / throttle reasons during the timed region.
 
-    def __init__(self, index=0):
+    NVML in-process (20 ms polls; the timed region of the default run is only
+    ~0.3 s, shorter than an `nvidia-smi -lms` start-up, which left runs with no
+    samples), falling back to an `nvidia-smi -lms 50` subprocess.  `__enter__`
+    returns only after the first sample, so the timed region is covered.
+    """
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index=0, period=0.02):
         self.index = index
+        self.period = period
         self.proc = None
-        self.lines = []
+        self.thread = None
+        self.stop = threading.Event()
+        self.samples = []  # (sm_mhz, max_mhz, set(reasons))
+        self.source = None
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40,
+                    "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+
+            def poll():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), float(mx),
+                                     {n for n, b in bits.items() if r & b}))
+
+            poll()
+            self.source = "nvml"
+
+            def loop():
+                while not self.stop.wait(self.period):
+                    try:
+                        poll()
+                    except Exception:
+                        return
+
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.samples = []
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.source = "nvidia-smi"
+            first = threading.Event()
+
+            def read():
+                for line in self.proc.stdout:
+                    parts = [p.strip() for p in line.split(",")]
+                    try:
+                        self.samples.append((float(parts[0]), float(parts[1]),
+                                             {n for n, f in zip(self.NAMES, parts[3:7])
+                                              if f.lower() == "active"}))
+                    except (ValueError, IndexError):
+                        continue
+                    first.set()
+
+            self.thread = threading.Thread(target=read, daemon=True)
             self.thread.start()
+            first.wait(timeout=5)
         except Exception:
             self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for name, flag in zip(names, parts[3:7]):
-                if flag.lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [s[0] for s in self.samples]
+        reasons = set().union(*[s[2] for s in self.samples]) if self.samples else set()
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": self.samples[-1][1] if self.samples else None,
+                "reasons": sorted(reasons), "samples": len(sm), "source": self.source}
 
 
 def dist_init():

@@ -120,6 +120,15 @@ __device__ void arnoldi_finish_block(GWork W, double *scr) {
   const int tid = threadIdx.x, nt = blockDim.x;
   double *hs = scr, *css = scr + (MAXR + 2), *sns = scr + 2 * (MAXR + 2);
   double *h = W.H + (size_t)j * (MAXR + 1);
+  // thread 0's scalar inputs are loaded up front, all at once, alongside the
+  // column staging (reading them between its stores made each one a
+  // dependent L2 round trip on the serial tail of the sweep)
+  GCtrl cl;
+  double gj = 0.0;
+  if (tid == 0) {
+    cl = *c;
+    gj = W.g[j];
+  }
   for (int i = tid; i <= j; i += nt) {
     hs[i] = (0.0 + W.c1[i]) + W.c2[i];
     if (i < j) {
@@ -129,8 +138,8 @@ __device__ void arnoldi_finish_block(GWork W, double *scr) {
   }
   __syncthreads();
   if (tid == 0) {
-    const double hj = sqrt(c->hn2);
-    const double wnorm0 = sqrt(c->wn2);
+    const double hj = sqrt(cl.hn2);
+    const double wnorm0 = sqrt(cl.wn2);
     hs[j + 1] = hj;
     const bool breakdown = hj <= 1e-14 * fmax(wnorm0, 1e-300);
     if (!breakdown) W.alpha[j + 1] = 1.0 / hj;
@@ -145,24 +154,27 @@ __device__ void arnoldi_finish_block(GWork W, double *scr) {
     const double denom = hypot(hs[j], hs[j + 1]);
     if (denom == 0.0) {  // dead column (src/sparsela.py:239-246)
       c->breakdown = 1;
-      c->total_it += 1;
-      W.res[c->n_res] = W.res[c->n_res - 1];
-      c->n_res += 1;
+      c->total_it = cl.total_it + 1;
+      W.res[cl.n_res] = W.res[cl.n_res - 1];
+      c->n_res = cl.n_res + 1;
       c->k = j;
       c->cycle_done = 1;
     } else {
-      W.cs[j] = hs[j] / denom;
-      W.sn[j] = hs[j + 1] / denom;
+      const double csj = hs[j] / denom, snj = hs[j + 1] / denom;
+      W.cs[j] = csj;
+      W.sn[j] = snj;
       hs[j] = denom;
       hs[j + 1] = 0.0;
-      W.g[j + 1] = -W.sn[j] * W.g[j];
-      W.g[j] = W.cs[j] * W.g[j];
-      c->total_it += 1;
-      const double est = fabs(W.g[j + 1]) / c->bnorm;
-      W.res[c->n_res] = est;
-      c->n_res += 1;
+      const double g1 = -snj * gj;
+      W.g[j + 1] = g1;
+      W.g[j] = csj * gj;
+      const int total_it = cl.total_it + 1;
+      c->total_it = total_it;
+      const double est = fabs(g1) / cl.bnorm;
+      W.res[cl.n_res] = est;
+      c->n_res = cl.n_res + 1;
       if (breakdown) c->breakdown = 1;
-      if (est <= c->rtol || breakdown || c->total_it >= c->maxit || j + 1 >= c->m) {
+      if (est <= cl.rtol || breakdown || total_it >= cl.maxit || j + 1 >= cl.m) {
         c->k = j + 1;
         c->cycle_done = 1;
       } else {
@@ -344,6 +356,60 @@ __device__ __forceinline__ void tile_compute(const TileArgs &A, double *buf, int
   }
 }
 
+// Row-owner form of the DOT / UPD_DOT tile work for short bases (L <= LMAX,
+// tiles of >= CGS_BS rows): each thread owns rows tid, tid + CGS_BS, ...,
+// reads each basis entry of its rows from shared memory once, forms w1 in a
+// register (UPD_DOT: same association as tile_compute, so w1 is bit-identical)
+// and keeps one running dot per slot (acc[l]; DOT: nrm = ||w||^2) across rows
+// and tiles.  The slot-owner form above reads w once per slot, syncs the CTA
+// between the update and the dots and leaves warps with uneven slot counts.
+template <int MODE, int TRC, int LMAX>
+__device__ __forceinline__ void tile_compute_ro(const TileArgs &A, const double (&csr)[LMAX],
+                                                double *buf, int r0, int rows,
+                                                double (&acc)[CGS_Q], double &nrm) {
+  constexpr int RPT = TRC / CGS_BS;
+  const int L = A.L;
+  const double *wt = buf + L * TRC;
+#pragma unroll(LMAX <= 8 ? 2 : 1)
+  for (int m = 0; m < RPT; ++m) {
+    const int r = threadIdx.x + CGS_BS * m;
+    double v[LMAX];
+#pragma unroll
+    for (int l = 0; l < LMAX; ++l) v[l] = (l < L) ? buf[l * TRC + r] : 0.0;
+    double w = wt[r];
+    if (MODE == CGS_UPD_DOT) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int l = 0; l < LMAX; l += 2) {
+        if (l < L) {
+          if (l + 1 < L) {
+            s0 += v[l] * csr[l];
+            s1 += v[l + 1] * csr[l + 1];
+          } else {
+            s0 += v[l] * csr[l];
+          }
+        }
+      }
+      w = w - (s0 + s1);
+      if (r < rows)
+        A.out[r0 + r] = w;
+      else
+        w = 0.0;
+    } else {
+      nrm += w * w;
+    }
+#pragma unroll
+    for (int l = 0; l < LMAX; ++l)
+      if (l < L) acc[l] += v[l] * w;
+  }
+}
+
+// IRKG_CGS_RO mask (bits 24.. of the trmax word): bit m = row-owner tile work
+// in sweep m (DOT, UPD_DOT); default 2 (UPD_DOT only: the slot-owner DOT,
+// which has no update to fuse, measured faster)
+template <int MODE>
+__device__ __forceinline__ bool cgs_ro_on(int trmax_word) { return (trmax_word >> (24 + MODE)) & 1; }
+
 template <int TRC>
 __device__ __forceinline__ bool tile_full(const TileArgs &A, int t) {
   return (long long)(t + 1) * TRC <= (long long)A.n;
@@ -424,7 +490,8 @@ __device__ __forceinline__ double fold_partials(const double *pl, int G, int lan
 }
 
 // One sweep's tile loop (grid-stride over row tiles, NST tiles in flight).
-template <int MODE, int TRC>
+// LMAX > 0: the row-owner tile work (DOT / UPD_DOT with L <= LMAX).
+template <int MODE, int TRC, int LMAX = 0>
 __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q], double &nrm,
                                           const GWork &W, const double *cin, const double *pin) {
   const int G = A.G, ntiles = A.ntiles;
@@ -471,6 +538,12 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
   }
   __syncthreads();
   pdl_trigger();
+  constexpr int LR = LMAX > 0 ? LMAX : 1;
+  double csr[LR];
+  if constexpr (LMAX > 0) {
+#pragma unroll
+    for (int l = 0; l < LMAX; ++l) csr[l] = (MODE == CGS_UPD_DOT && l < A.L) ? A.cs[l] : 0.0;
+  }
 
   int s = 0;
   uint32_t phase = 0;
@@ -484,8 +557,12 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
     } else {
       tile_load_tail<TRC>(A, buf, r0, rows);
     }
-    tile_compute<MODE, TRC>(A, buf, r0, rows, acc, nrm);
-    if (MODE == CGS_UPD_DOT) fence_proxy_async();  // wt was written via the generic proxy
+    if constexpr (LMAX > 0) {
+      tile_compute_ro<MODE, TRC, LR>(A, csr, buf, r0, rows, acc, nrm);
+    } else {
+      tile_compute<MODE, TRC>(A, buf, r0, rows, acc, nrm);
+      if (MODE == CGS_UPD_DOT) fence_proxy_async();
+    }  // wt was written via the generic proxy
     __syncthreads();  // stage s consumed
     {
       const int tn = t + NST * G;
@@ -519,7 +596,8 @@ __global__ void __launch_bounds__(CGS_BS, 2)
     return;
   }
   const int L = ctrl->j + 1;
-  const int cgs_rev_mask = trmax >> 16;
+  const int trmax_raw = trmax;
+  const int cgs_rev_mask = (trmax >> 16) & 0xff;
   trmax &= 0xffff;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double *out = (MODE == CGS_UPD_NORM) ? V + (size_t)L * pitch : wout;
@@ -546,7 +624,24 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   double acc[CGS_Q];
 #pragma unroll
   for (int q = 0; q < CGS_Q; ++q) acc[q] = 0.0;
-  switch (TR) {
+  // row-owner dots for short bases in tall tiles (all of configs[1]'s
+  // typical cycle lengths); bucketed so the register arrays stay static
+  const int ro = (MODE != CGS_UPD_NORM && TR >= CGS_BS && cgs_ro_on<MODE>(trmax_raw))
+                     ? (L <= 4 ? 4 : L <= 8 ? 8 : L <= 16 ? 16 : 0)
+                     : 0;
+  if (ro) {
+    switch (TR * 100 + ro) {
+      case 25604: cgs_tiles<MODE, 256, 4>(A, acc, nrm, W, cin, pin); break;
+      case 25608: cgs_tiles<MODE, 256, 8>(A, acc, nrm, W, cin, pin); break;
+      case 25616: cgs_tiles<MODE, 256, 16>(A, acc, nrm, W, cin, pin); break;
+      case 51204: cgs_tiles<MODE, 512, 4>(A, acc, nrm, W, cin, pin); break;
+      case 51208: cgs_tiles<MODE, 512, 8>(A, acc, nrm, W, cin, pin); break;
+      case 51216: cgs_tiles<MODE, 512, 16>(A, acc, nrm, W, cin, pin); break;
+      case 102404: cgs_tiles<MODE, 1024, 4>(A, acc, nrm, W, cin, pin); break;
+      case 102408: cgs_tiles<MODE, 1024, 8>(A, acc, nrm, W, cin, pin); break;
+      default: cgs_tiles<MODE, 1024, 16>(A, acc, nrm, W, cin, pin); break;
+    }
+  } else switch (TR) {
     case 32: cgs_tiles<MODE, 32>(A, acc, nrm, W, cin, pin); break;
     case 64: cgs_tiles<MODE, 64>(A, acc, nrm, W, cin, pin); break;
     case 128: cgs_tiles<MODE, 128>(A, acc, nrm, W, cin, pin); break;
@@ -556,7 +651,23 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   }
 
   // per-CTA partials -> part[l * G + cta]
-  if (MODE != CGS_UPD_NORM) {
+  if (ro) {
+    // row-owner: every thread holds a partial of every entry; warp sums into
+    // shared memory, then one thread per entry adds the warps in order
+#pragma unroll
+    for (int l = 0; l < 17; ++l) {
+      if (l <= L && l < nd) {
+        const double v = wsum(l == L ? nrm : acc[l]);
+        if (lane == 0) red[warp * 17 + l] = v;
+      }
+    }
+    __syncthreads();
+    if (tid < nd) {
+      double tot = 0.0;
+      for (int w = 0; w < CGS_NW; ++w) tot += red[w * 17 + tid];
+      part[(size_t)tid * G + blockIdx.x] = tot;
+    }
+  } else if (MODE != CGS_UPD_NORM) {
     const int nq = (nd + CGS_NW - 1) / CGS_NW;
 #pragma unroll
     for (int q = 0; q < CGS_Q; ++q) {
@@ -671,6 +782,8 @@ static int cgs_trmax() {
     // bit m: sweep m (DOT, UPD_DOT, UPD_NORM) walks the row tiles backwards
     const char *r = getenv("IRKG_CGS_REV");
     v |= (r ? atoi(r) : 2) << 16;
+    const char *ro = getenv("IRKG_CGS_RO");
+    v |= ((ro ? atoi(ro) : 2) & 3) << 24;
   }
   return v;
 }
