@@ -377,7 +377,7 @@ __device__ __forceinline__ void tile_compute_ro(const TileArgs &A, const double 
 #pragma unroll
     for (int l = 0; l < LMAX; ++l) v[l] = (l < L) ? buf[l * TRC + r] : 0.0;
     double w = wt[r];
-    if (MODE == CGS_UPD_DOT) {
+    if (MODE != CGS_DOT) {
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int l = 0; l < LMAX; l += 2) {
@@ -395,18 +395,21 @@ __device__ __forceinline__ void tile_compute_ro(const TileArgs &A, const double 
         A.out[r0 + r] = w;
       else
         w = 0.0;
+      if (MODE == CGS_UPD_NORM) nrm += w * w;
     } else {
       nrm += w * w;
     }
+    if (MODE != CGS_UPD_NORM) {
 #pragma unroll
-    for (int l = 0; l < LMAX; ++l)
-      if (l < L) acc[l] += v[l] * w;
+      for (int l = 0; l < LMAX; ++l)
+        if (l < L) acc[l] += v[l] * w;
+    }
   }
 }
 
 // IRKG_CGS_RO mask (bits 24.. of the trmax word): bit m = row-owner tile work
-// in sweep m (DOT, UPD_DOT); default 2 (UPD_DOT only: the slot-owner DOT,
-// which has no update to fuse, measured faster)
+// in sweep m (DOT, UPD_DOT, UPD_NORM); default 6 (the update sweeps; DOT, which
+// has no update to fuse, measured the same either way)
 template <int MODE>
 __device__ __forceinline__ bool cgs_ro_on(int trmax_word) { return (trmax_word >> (24 + MODE)) & 1; }
 
@@ -542,7 +545,7 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
   double csr[LR];
   if constexpr (LMAX > 0) {
 #pragma unroll
-    for (int l = 0; l < LMAX; ++l) csr[l] = (MODE == CGS_UPD_DOT && l < A.L) ? A.cs[l] : 0.0;
+    for (int l = 0; l < LMAX; ++l) csr[l] = (MODE != CGS_DOT && l < A.L) ? A.cs[l] : 0.0;
   }
 
   int s = 0;
@@ -626,7 +629,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   for (int q = 0; q < CGS_Q; ++q) acc[q] = 0.0;
   // row-owner dots for short bases in tall tiles (all of configs[1]'s
   // typical cycle lengths); bucketed so the register arrays stay static
-  const int ro = (MODE != CGS_UPD_NORM && TR >= CGS_BS && cgs_ro_on<MODE>(trmax_raw))
+  const int ro = (TR >= CGS_BS && cgs_ro_on<MODE>(trmax_raw))
                      ? (L <= 4 ? 4 : L <= 8 ? 8 : L <= 16 ? 16 : 0)
                      : 0;
   if (ro) {
@@ -651,7 +654,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   }
 
   // per-CTA partials -> part[l * G + cta]
-  if (ro) {
+  if (ro && MODE != CGS_UPD_NORM) {
     // row-owner: every thread holds a partial of every entry; warp sums into
     // shared memory, then one thread per entry adds the warps in order
 #pragma unroll
@@ -783,7 +786,7 @@ static int cgs_trmax() {
     const char *r = getenv("IRKG_CGS_REV");
     v |= (r ? atoi(r) : 2) << 16;
     const char *ro = getenv("IRKG_CGS_RO");
-    v |= ((ro ? atoi(ro) : 2) & 3) << 24;
+    v |= ((ro ? atoi(ro) : 6) & 7) << 24;
   }
   return v;
 }
