@@ -372,13 +372,15 @@ def run_ours(args, spec, ws, rank, local):
     achieved = cgs_bytes / (cgs_ms * 1e-3) / 1e9 if cgs_ms > 0 else 0.0
     traffic, tnote = None, None
     try:  # DRAM bytes per CGS launch from the committed ncu capture (j = 8 sweeps)
-        with open(os.path.join(ROOT, "profiles", "r1s3_cgs_traffic.json")) as fh:
+        tname = next(f for f in ("r1s4_cgs_traffic.json", "r1s3_cgs_traffic.json")
+                     if os.path.exists(os.path.join(ROOT, "profiles", f)))
+        with open(os.path.join(ROOT, "profiles", tname)) as fh:
             tdoc = json.load(fh)
         traffic = tdoc["traffic_per_launch"]
         tnote = (f"ncu --set full, CGS sweeps at j={tdoc['j']}: {traffic / 1e6:.1f} MB DRAM per launch "
                  f"vs {tdoc['algorithmic_per_launch'] / 1e6:.1f} MB algorithmic "
-                 f"(ratio {tdoc['ratio']:.3f}; profiles/r1s3_cgs_traffic.json)")
-    except (OSError, KeyError, ValueError):
+                 f"(ratio {tdoc['ratio']:.3f}; profiles/{tname})")
+    except (OSError, KeyError, ValueError, StopIteration):
         pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "traffic_note": tnote,
