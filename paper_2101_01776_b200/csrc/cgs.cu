@@ -183,8 +183,9 @@ __device__ void arnoldi_finish_block(GWork W, double *scr) {
     }
   }
   __syncthreads();
+  // (no fence: the consumers are later kernels -- a launch boundary, or a
+  // griddepcontrol.wait, which waits for this grid's completion and flush)
   for (int i = tid; i <= j + 1; i += nt) h[i] = hs[i];
-  __threadfence();
   __syncthreads();
 }
 
@@ -719,8 +720,8 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   __syncthreads();
   // use_cond < 0: multi-rank -- the column is finished after the all-reduce
   if (MODE == CGS_UPD_NORM && use_cond >= 0) {
-    __threadfence();
-    arnoldi_finish_block(W, sm);  // the ring is drained: its memory is scratch now
+    // ctrl->hn2 came from this CTA (the barrier suffices); the drained ring is scratch
+    arnoldi_finish_block(W, sm);
     if (tid == 0 && use_cond > 0) cudaGraphSetConditional(cond, ctrl->cycle_done ? 0u : 1u);
   }
   if (tid == 0) *counter = 0u;
