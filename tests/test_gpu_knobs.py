@@ -60,3 +60,15 @@ def test_scheduling_knobs_are_bit_identical(tmp_path):
         u, stats = _run(str(tmp_path), name, env)
         assert stats == ref_stats, name
         assert u.tobytes() == ref_u.tobytes(), name
+
+
+def test_cgs_tile_forms_agree(tmp_path):
+    """The row-owner CGS update sweeps (IRKG_CGS_RO, default 6) sum the
+    second-pass dots in another order than the slot-owner form (0): the same
+    IRK steps to the parity bar (1e-10 relative, counts within +/-1)."""
+    ref_u, ref_stats = _run(str(tmp_path), "default", {})
+    for mask in ("0", "7"):
+        u, stats = _run(str(tmp_path), "ro" + mask, {"IRKG_CGS_RO": mask})
+        for (n0, k0, _), (n1, k1, _) in zip(ref_stats, stats):
+            assert abs(n0 - n1) <= 1 and abs(k0 - k1) <= max(1, n0), (mask, ref_stats, stats)
+        assert np.linalg.norm(u - ref_u) <= 1e-10 * np.linalg.norm(ref_u), mask

@@ -298,6 +298,43 @@ def test_block_gmres_counts_match_oracle(size):
         np.testing.assert_allclose(rep.residuals[: n - 1], repo.residuals[: n - 1], rtol=1e-6)
 
 
+@pytest.mark.parametrize("shape,size", [((36, 28), 1), ((66, 50), 2), ((130, 96), 2)])
+def test_block_gmres_ragged_tiles_all_cgs_forms(shape, size):
+    """Block sizes that leave a partial last CGS tile (n % 1024 != 0), with
+    restarts that put the basis in every row-owner bucket of the update
+    sweeps (L <= 4, 8, 16) and past it (L up to 24: slot-owner tile work):
+    counts within +/-1 of the oracle's GMRES (src/sparsela.py:176-280) and
+    the same solution."""
+    prob = GridProblem("burgers", shape, nu=1e-2)
+    pd, _ = _oracle_sys(prob)
+    rng = np.random.default_rng(11)
+    U = 0.5 * rng.standard_normal((2, pd.dim))
+    f1 = pk.OperatorField.linearize(prob, U[:1])
+    f2 = pk.OperatorField.linearize(prob, U[1:])
+    l1 = pd.linearize_csr(U[0], 0.0)
+    l2 = pd.linearize_csr(U[1], 0.0)
+    dt = 5e-3
+    eta, beta, phi = 3.677815, 3.508762, -10.983731
+    rhs = rng.standard_normal(size * pd.dim)
+    for restart in (4, 8, 16, 24):
+        if size == 2:
+            sysb = pk.Block2x2System(eta, beta, phi, None, f1, f2, dt)
+            x, rep = pk.block_gmres(sysb, rhs, pk.PrecondSpec(inner=4), 1e-10, 500, restart)
+            pre = irk.block2x2_precond(eta, beta, phi, l1, l2, dt, "star", 4)
+            xo, repo = irk.gmres(lambda v: irk.block2x2_apply(eta, beta, phi, l1, l2, dt, v), rhs,
+                                 2 * pd.dim, pre, 2, 1e-10, 500, restart)
+        else:
+            x, rep = pk.block_gmres((eta, f1, dt), rhs, pk.PrecondSpec(inner=4), 1e-10, 500,
+                                    restart)
+            solver = irk.ShiftedSolver(eta, l1, dt, 4)
+            xo, repo = irk.gmres(lambda v: eta * v - dt * (l1 @ v), rhs, pd.dim, solver.solve, 1,
+                                 1e-10, 500, restart)
+        assert rep.converged and repo.converged
+        assert abs(rep.iterations - repo.iterations) <= 1, (restart, rep.iterations,
+                                                            repo.iterations)
+        assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
 def test_block_gmres_maxit_and_zero_rhs():
     prob = GridProblem("nldiff", (16, 16))
     f = pk.OperatorField.linearize(prob, np.ones((1, 256)))
