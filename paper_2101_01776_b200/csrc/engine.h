@@ -317,8 +317,9 @@ struct Engine {
   // L2 persistence of the lowest l2_budget bytes of the basis (IRKG_L2_MB;
   // 0 = off).  configs[1] (16.8 MB slots): 1 / 2 / 3 / 4 / 5 slots ->
   // 31.72 / 31.35 / 31.07 / 31.93 / 32.78 ms per IRK step (none: 31.73);
-  // 40 / 50 / 60 MB -> 31.21 / 31.02 / 30.93
-  size_t l2_budget = 60u << 20;
+  // 40 / 50 / 60 MB -> 31.21 / 31.02 / 30.93; with the row-owner CGS update
+  // sweeps (session 4) 34 / 51 / 60 MB -> 29.68 / 29.68 / 29.80
+  size_t l2_budget = 51u << 20;
   size_t l2_persist_max = 0, l2_window_max = 0;
   cudaAccessPolicyWindow l2win{};
   void set_l2_window();
