@@ -622,17 +622,24 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   }
   __syncthreads();
 
-  TileArgs A{n, L, G, ntiles, V, pitch, win, out, sm, nst, bars, cs, red,
-             TR <= 256 ? vmaps : nullptr, (cgs_rev_mask >> MODE) & 1, ef_from};
-  double nrm = 0.0;
-  double acc[CGS_Q];
-#pragma unroll
-  for (int q = 0; q < CGS_Q; ++q) acc[q] = 0.0;
   // row-owner dots for short bases in tall tiles (all of configs[1]'s
   // typical cycle lengths); bucketed so the register arrays stay static
   const int ro = (TR >= CGS_BS && cgs_ro_on<MODE>(trmax_raw))
                      ? (L <= 4 ? 4 : L <= 8 ? 8 : L <= 16 ? 16 : 0)
                      : 0;
+  // 1-D per-slot copies instead of tensor-map boxes (IRKG_CGS_1D, bits 28..30:
+  // bit m = sweep m; default 7) in tiles of >= 256 rows (DOT: >= 128).
+  // Same-box probe at configs[1], DOT j = 12 / 24 / 32: 35.1 / 63.8 / 86.3 ->
+  // 30.2 / 55.5 / 73.3 us; the update sweeps lose in 128-row tiles
+  // (UPD_DOT j = 32: 91.7 -> 114.8 us), so large j keeps the boxes there.
+  const int m1d = (trmax_raw >> 28) & 7;
+  const bool one_d = ((m1d >> MODE) & 1) && TR >= (MODE == CGS_DOT ? 128 : 256);
+  TileArgs A{n, L, G, ntiles, V, pitch, win, out, sm, nst, bars, cs, red,
+             (TR <= 256 && !one_d) ? vmaps : nullptr, (cgs_rev_mask >> MODE) & 1, ef_from};
+  double nrm = 0.0;
+  double acc[CGS_Q];
+#pragma unroll
+  for (int q = 0; q < CGS_Q; ++q) acc[q] = 0.0;
   if (ro) {
     switch (TR * 100 + ro) {
       case 25604: cgs_tiles<MODE, 256, 4>(A, acc, nrm, W, cin, pin); break;
@@ -788,6 +795,8 @@ static int cgs_trmax() {
     v |= (r ? atoi(r) : 2) << 16;
     const char *ro = getenv("IRKG_CGS_RO");
     v |= ((ro ? atoi(ro) : 6) & 7) << 24;
+    const char *o1 = getenv("IRKG_CGS_1D");
+    v |= ((o1 ? atoi(o1) : 7) & 7) << 28;
   }
   return v;
 }
