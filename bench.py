@@ -6,16 +6,22 @@ Workload (N = 1): BASELINE ``configs[1]`` -- 2-D viscous Burgers on a
 seeded Fourier-mode u0 (|k| <= 8, sigma = 0.5); manifest: variant 3,
 gamma*, Jacobi-4 inner solves, restart 200, krylov_maxit 5000, Newton rtol
 1e-9, Krylov rtol 1e-5 (reference defaults).  A "step" is one IRK time step
-(all Newton iterations of the stage solve + the u update), marching the same
-trajectory: W warm-up steps, then K timed steps.
+(all Newton iterations of the stage solve + the u update); every step is the
+step from (t = 0, u0) -- configs[1] step 1, identical work each time -- so
+W warm-up steps never move the timed work and the reference arm can time
+the same Newton iterations.
 
 Headline metric: stage-DOF updates/s = sum_steps(newton_its * s * N) / time
 (SURVEY 8d); IRK steps/s and the CGS2 roofline are reported beside it.
 
-``--impl reference`` times the reference algorithm's CPU restatement
-(``oracle/``, a numpy/scipy port of irkit; the reference itself is Python and
-cannot travel to the GPU box) on the host cores: each of its steps is one full
-Newton iteration of the same trajectory at full size (a bounded sample).
+``--impl reference`` times the reference itself -- irkit installed into
+``baseline/_ref`` -- on the host cores (the numpy/scipy restatement in
+``oracle/`` when that install is absent): each of its steps is one Newton
+iteration of that same IRK step at full size, in order (a bounded sample).
+
+A ``largest_config`` object adds configs[2] at P = 1 (4096^2, Gauss(2),
+Jacobi-4; step 1): its CGS and whole-step HBM fractions are the north
+star's ">= 60 % on the largest 1-GPU config" check.
 """
 
 from __future__ import annotations
@@ -189,75 +195,134 @@ def sum_over_ranks(x, ws):
 
 # ------------------------------------------------------------ CPU leg
 
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 
-class OracleNewtonStream:
-    """Newton iterations of the configs[1] trajectory on the CPU oracle, one
-    per call (a complete reference Newton iteration: linearize s stages,
-    variant-3 combine, transformed solve, residual)."""
 
-    def __init__(self, spec):
-        from oracle import irk
-        from oracle import tableau as otab
+def _import_irkit():
+    """The unmodified reference package, installed by
+    ``pip install --target baseline/_ref``; None if absent."""
+    if os.path.isdir(REF_PATH) and REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    try:
+        import irkit  # noqa: F401
+        from irkit import nonlinear  # noqa: F401
+        return irkit
+    except Exception:
+        return None
+
+
+class Step1NewtonCycle:
+    """The CPU arm's work unit: Newton iterations of the benched IRK step --
+    the step from (t = 0, u0) -- in order; once the step's Newton loop
+    converges it starts over from u0.  So the reference times the same
+    Newton iterations (same Krylov work per iteration) as the GPU arm's
+    steps.  ``impl="irkit"`` drives the reference package itself (its
+    ``stage_residual`` / ``build_variant_jacobian`` /
+    ``solve_transformed_system``, exactly the body of ``newton_like_step``,
+    src/nonlinear.py:196-225, on the configs problem written as an irkit
+    ``OdeSystem`` plugin); ``impl="port"`` the numpy/scipy restatement
+    (oracle/irk.py)."""
+
+    def __init__(self, spec, impl):
         from oracle.problems import build_problem
 
-        self.irk = irk
+        self.impl = impl
         prob = spec.problem
         pd = build_problem(prob.kind, prob.shape, **prob.oracle_params())
-        self.sys = irk.OdeSystem(pd.dim, pd.rhs, pd.linearize_csr)
-        self.prep = otab.prepare(spec.family, spec.s)
         sv = spec.solver
-        self.cfg = irk.Config(variant=sv["variant"], krylov_maxit=sv["krylov_maxit"],
-                              restart=sv["restart"], inner=sv["inner"],
-                              newton_maxit=sv["newton_maxit"])
-        self.dt = spec.dt
-        self.u = spec.u0()
-        self.t = 0.0
-        self.s = spec.s
-        self.n = pd.dim
+        self.dt, self.s, self.n = spec.dt, spec.s, pd.dim
+        self.u0 = spec.u0()
+        if impl == "irkit":
+            import irkit
+            from irkit import nonlinear as nl
+            from irkit.irk_core import PrecondSpec, solve_transformed_system
+            from irkit.sparsela import SparseMatrix
+
+            self.nl, self.solve = nl, solve_transformed_system
+            self.sys = pd.as_ode_system(nl.OdeSystem, SparseMatrix)
+            self.prep = irkit.prepare_stages(irkit.make_tableau(spec.family, spec.s))
+            self.cfg = nl.SolverConfig(variant=sv["variant"], krylov_maxit=sv["krylov_maxit"],
+                                       restart=sv["restart"], newton_maxit=sv["newton_maxit"],
+                                       precond=PrecondSpec(inner=sv["inner"]))
+        else:
+            from oracle import irk
+            from oracle import tableau as otab
+
+            self.irk = irk
+            self.sys = irk.OdeSystem(pd.dim, pd.rhs, pd.linearize_csr)
+            self.prep = otab.prepare(spec.family, spec.s)
+            self.cfg = irk.Config(variant=sv["variant"], krylov_maxit=sv["krylov_maxit"],
+                                  restart=sv["restart"], inner=sv["inner"],
+                                  newton_maxit=sv["newton_maxit"])
         self._new_step()
 
+    def _residual(self):
+        tab = self.prep.tableau
+        if self.impl == "irkit":
+            return self.nl.stage_residual(self.sys, self.st, tab)
+        return self.irk.stage_residual(self.sys, self.u0, self.k, 0.0, self.dt, tab)
+
     def _new_step(self):
-        irk, tab = self.irk, self.prep.tableau
         self.k = np.zeros((self.s, self.n))
-        self.res = irk.stage_residual(self.sys, self.u, self.k, self.t, self.dt, tab)
-        f0 = np.linalg.norm(self.res)
-        self.tol = max(self.cfg.newton_rtol * f0, self.cfg.newton_abs_floor)
+        if self.impl == "irkit":
+            self.st = self.nl.StageState(k=self.k, u=self.u0, t=0.0, dt=self.dt)
+        self.res = self._residual()
+        self.tol = max(self.cfg.newton_rtol * np.linalg.norm(self.res),
+                       self.cfg.newton_abs_floor)
 
     def newton_iteration(self):
-        irk, tab, cfg = self.irk, self.prep.tableau, self.cfg
+        """One Newton iteration; returns its Krylov iteration count."""
+        tab, cfg = self.prep.tableau, self.cfg
         if np.linalg.norm(self.res) <= self.tol:
-            self.u = self.u + self.dt * (tab.b0 @ self.k)
-            self.t += self.dt
             self._new_step()
-        times = self.t + tab.c0 * self.dt
-        u_stage = self.u[None, :] + self.dt * (tab.a0 @ self.k)
+        times = tab.c0 * self.dt
+        u_stage = self.u0[None, :] + self.dt * (tab.a0 @ self.k)
         ops = [self.sys.linearize(u_stage[i], times[i]) for i in range(self.s)]
-        vjac = irk.build_variant_jacobian(self.prep, ops, cfg.variant, cfg.variant0_stage)
-        dk, st = irk.solve_transformed(self.prep, vjac, self.dt, self.res, cfg.gamma_mode,
-                                       cfg.inner, cfg.krylov_rtol, cfg.krylov_maxit, cfg.restart)
-        self.k = self.k + dk
-        self.res = irk.stage_residual(self.sys, self.u, self.k, self.t, self.dt, tab)
+        if self.impl == "irkit":
+            vjac = self.nl.build_variant_jacobian(self.prep, ops, cfg.variant, cfg.variant0_stage)
+            dk, st = self.solve(self.prep, dt=self.dt, rhs_stages=self.res, mass=None,
+                                precond=cfg.precond, krylov_rtol=cfg.krylov_rtol,
+                                krylov_maxit=cfg.krylov_maxit, restart=cfg.restart,
+                                variant_jacobian=vjac)
+            self.st.k = self.st.k + dk
+            self.k = self.st.k
+        else:
+            irk = self.irk
+            vjac = irk.build_variant_jacobian(self.prep, ops, cfg.variant, cfg.variant0_stage)
+            dk, st = irk.solve_transformed(self.prep, vjac, self.dt, self.res, cfg.gamma_mode,
+                                           cfg.inner, cfg.krylov_rtol, cfg.krylov_maxit,
+                                           cfg.restart)
+            self.k = self.k + dk
+        self.res = self._residual()
         return st.krylov_iterations
 
 
+def cpu_arm():
+    return ("irkit", "reference") if _import_irkit() is not None else ("port", "port")
+
+
 def cpu_sample(spec, n_iters):
+    impl, kind = cpu_arm()
     threads = os.cpu_count() or 1
-    stream = OracleNewtonStream(spec)
+    stream = Step1NewtonCycle(spec, impl)
     t0 = time.perf_counter()
     kry = 0
     for _ in range(n_iters):
         kry += stream.newton_iteration()
     dt = time.perf_counter() - t0
     dof = n_iters * spec.s * spec.problem.dim / dt
-    return dof, dt, kry, threads
+    return dof, dt, kry, threads, kind
 
 
 def run_reference(args, spec, ws, rank):
     if rank != 0:
         return
-    stream = OracleNewtonStream(spec)
-    for _ in range(args.warmup):
+    impl, kind = cpu_arm()
+    stream = Step1NewtonCycle(spec, impl)
+    warm = min(args.warmup, 1)   # CPU numpy: one untimed iteration pages everything in
+    for _ in range(warm):
         stream.newton_iteration()
+    stream._new_step()            # the timed iterations start at step 1's first
     t0 = time.perf_counter()
     kry = 0
     for _ in range(args.steps):
@@ -265,25 +330,127 @@ def run_reference(args, spec, ws, rank):
     el = time.perf_counter() - t0
     value = args.steps * spec.s * spec.problem.dim / el
     cores = os.cpu_count() or 1
+    who = ("irkit (the unmodified reference from baseline/_ref: stage_residual, "
+           "build_variant_jacobian, solve_transformed_system)" if impl == "irkit" else
+           "the numpy/scipy restatement of irkit (oracle/irk.py; baseline/_ref absent)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": ws, "steps": args.steps, "warmup": warm,
         "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Fourier-mode u0)",
-        "config": {"workload": spec.name, "grid": list(spec.problem.shape), "scheme": "gauss(3)",
-                   "dt": spec.dt, "inner": "jacobi-4", "variant": 3},
+        "config": _config(spec, ws, spec.problem.shape),
+        "step_unit": ("one Newton iteration of the benched IRK step (configs[1] from t=0, u0), "
+                      "in order, restarting from u0 when the step converges"),
+        "newton_iterations": args.steps, "krylov_iterations": kry,
+        "krylov_per_newton": kry / max(1, args.steps),
         "cpu_baseline": {
-            "value": value, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{args.steps} full Newton iterations (after {args.warmup} warm-up) of the "
-                      f"configs[1] trajectory at full 1024^2 size on the numpy/scipy restatement "
-                      f"of irkit (oracle/irk.py); {kry} Krylov iterations",
+            "value": value, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{args.steps} Newton iterations of configs[1] step 1 at {spec.problem.shape[0]}^2 on "
+                      f"{who}, host BLAS threads = {cores}; {kry} Krylov iterations",
         },
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def _config(spec, ws, grid):
+    return {"workload": spec.name + " step 1 (t=0, u0)", "grid": list(grid),
+            "scheme": f"{spec.family}({spec.s})", "dt": spec.dt, "inner": "jacobi-4",
+            "variant": 3, "restart": 200,
+            "parallelism": (f"slab{ws} (y-slabs, NCCL halos + allreduce; weak: configs[1] tiled "
+                            f"{ws}x in y)") if ws > 1 else "1 GPU",
+            "l2": "inputs > L2 (V basis 201 x 16.8 MB per rank; step-1 Arnoldi index up to ~40)"}
+
+
 # ------------------------------------------------------------ GPU leg
+
+
+def _solver_cfg(pk, spec):
+    sv = spec.solver
+    return pk.SolverConfig(variant=sv["variant"], krylov_maxit=sv["krylov_maxit"],
+                           restart=sv["restart"], newton_maxit=sv["newton_maxit"],
+                           precond=pk.PrecondSpec(inner=sv["inner"]))
+
+
+def _traffic_note():
+    """DRAM bytes per CGS launch from the committed warm-L2 ncu capture of the
+    benched step (tools/cgs_traffic.py), or the older cold capture."""
+    for f in ("r2_cgs_traffic.json", "r1s4_cgs_traffic.json"):
+        path = os.path.join(ROOT, "profiles", f)
+        if not os.path.exists(path):
+            continue
+        try:
+            with open(path) as fh:
+                t = json.load(fh)
+            return t["traffic_per_launch"], (
+                f"ncu ({t.get('cache', 'cold L2')}), {t.get('what', 'CGS sweeps')}: "
+                f"{t['traffic_per_launch'] / 1e6:.1f} MB DRAM per launch vs "
+                f"{t['algorithmic_per_launch'] / 1e6:.1f} MB algorithmic "
+                f"(ratio {t['ratio']:.3f}; profiles/{f})")
+        except (OSError, KeyError, ValueError):
+            continue
+    return None, None
+
+
+def largest_config(args, local):
+    """configs[2] at P = 1 (4096^2 nonlinear diffusion, Gauss(2), Jacobi-4):
+    the IRK step from (t = 0, u0), with the engine's per-phase timing on --
+    the north star's "largest 1-GPU config" roofline check."""
+    import torch
+
+    import paper_2101_01776_b200 as pk
+    from paper_2101_01776_b200.engine import Context
+    from paper_2101_01776_b200.problems import baseline_config
+
+    spec = baseline_config(2, n=args.large_n)
+    ctx = Context(spec.problem, local)
+    ctx.set_prep(pk.prepare_stages(pk.make_tableau(spec.family, spec.s)))
+    ctx.set_config(_solver_cfg(pk, spec))
+    u0 = torch.from_numpy(spec.u0()).cuda()
+    u = u0.clone()
+    stream = torch.cuda.current_stream()
+    ctx.set_timing(True)
+    c0 = ctx.counters()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        st = ctx.step_device(u, 0.0, spec.dt)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    c1 = ctx.counters()
+    ctx.set_timing(False)
+    ms = ev0.elapsed_time(ev1)
+    peak, _ = _peaks()
+    d = {k: c1[k] - c0[k] for k in ("cgs_bytes", "cgs_time_ms", "precond_bytes",
+                                     "precond_time_ms", "op_bytes", "op_time_ms",
+                                     "cgs_launches")}
+    krylov_bytes = d["cgs_bytes"] + d["precond_bytes"] + d["op_bytes"]
+    cgs_gbs = d["cgs_bytes"] / (d["cgs_time_ms"] * 1e-3) / 1e9 if d["cgs_time_ms"] > 0 else 0.0
+    step_gbs = krylov_bytes / (ms * 1e-3) / 1e9
+    out = {
+        "workload": f"configs[2] step 1 (t=0, u0): nldiff {args.large_n}^2, "
+                    f"{spec.family}({spec.s}), Jacobi-4, P=1",
+        "ms_step": ms, "newton_iterations": st.newton_iterations,
+        "krylov_iterations": st.krylov_iterations,
+        "stage_dof_per_s": st.newton_iterations * spec.s * spec.problem.dim / (ms * 1e-3),
+        "cgs": {"achieved_gbs": cgs_gbs, "frac": cgs_gbs / peak,
+                "bytes_per_launch": d["cgs_bytes"] / max(1, d["cgs_launches"]),
+                "avg_launch_us": 1e3 * d["cgs_time_ms"] / max(1, d["cgs_launches"]),
+                "share_of_step": d["cgs_time_ms"] / ms},
+        "krylov_phases_gbs": step_gbs, "krylov_phases_frac": step_gbs / peak,
+        "krylov_phases_note": "algorithmic bytes of the CGS2 sweeps + inner solves + block "
+                              "operators / whole-step device time (Newton-level kernels and "
+                              "restart-cycle ends counted as time, not bytes)",
+        "inner_solve_gbs": d["precond_bytes"] / (d["precond_time_ms"] * 1e-3) / 1e9
+        if d["precond_time_ms"] > 0 else None,
+        "block_op_gbs": d["op_bytes"] / (d["op_time_ms"] * 1e-3) / 1e9
+        if d["op_time_ms"] > 0 else None,
+        "peak_gbs": peak, "clocks": clk.summary(),
+    }
+    ctx.close()
+    return out
 
 
 def run_ours(args, spec, ws, rank, local):
@@ -296,11 +463,8 @@ def run_ours(args, spec, ws, rank, local):
     prob = spec.problem
     tab = pk.make_tableau(spec.family, spec.s)
     prep = pk.prepare_stages(tab)
-    sv = spec.solver
-    cfg = pk.SolverConfig(variant=sv["variant"], krylov_maxit=sv["krylov_maxit"],
-                          restart=sv["restart"], newton_maxit=sv["newton_maxit"],
-                          precond=pk.PrecondSpec(inner=sv["inner"]))
-    u0 = spec.u0()
+    cfg = _solver_cfg(pk, spec)
+    u0h = spec.u0()
     if ws > 1:
         # weak scaling: configs[1] tiled ws times along y (same h, dt, nu); rank r
         # owns one 1024^2 slab (= the N = 1 field, since u0 is 1-periodic);
@@ -315,17 +479,17 @@ def run_ours(args, spec, ws, rank, local):
         ctx = Context(prob, local)
     ctx.set_prep(prep)
     ctx.set_config(cfg)
-    u = torch.from_numpy(u0).cuda()
+    # Every step -- warm-up, timed, roofline and e2e -- is the IRK step from
+    # (t = 0, u0): configs[1] step 1, the same Newton/Krylov work each time
+    # and the same work unit the reference arm times (its Newton iterations).
+    u0 = torch.from_numpy(u0h).cuda()
+    u = torch.empty_like(u0)
     stream = torch.cuda.current_stream()
     N = u.numel()  # points owned by this rank
-    t = 0.0
     for _ in range(args.warmup):
-        ctx.step_device(u, t, spec.dt)
-        t += spec.dt
+        u.copy_(u0)
+        ctx.step_device(u, 0.0, spec.dt)
     torch.cuda.synchronize()
-    # the roofline and e2e passes below replay exactly these timed steps (same
-    # state, same t => same Newton/Krylov work), so their numbers compare 1:1
-    u_start, t_start = u.clone(), t
     c0 = ctx.counters()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -335,8 +499,8 @@ def run_ours(args, spec, ws, rank, local):
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            stats.append(ctx.step_device(u, t, spec.dt))
-            t += spec.dt
+            u.copy_(u0)
+            stats.append(ctx.step_device(u, 0.0, spec.dt))
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier(ws)
@@ -351,16 +515,14 @@ def run_ours(args, spec, ws, rank, local):
     launches = int(c1["kernel_launches"] - c0["kernel_launches"])
 
     # roofline pass: device time of the CGS2 sweeps (CUDA events on the engine
-    # stream around the 4 sweeps of each Arnoldi step) over extra steps
+    # stream around the sweeps of each Arnoldi step) over the same step
     ctx.set_timing(True)
-    u.copy_(u_start)
-    t = t_start
     r0 = ctx.counters()
     rsteps = max(1, min(args.steps, 3))
     tr0 = time.perf_counter()
     for _ in range(rsteps):
-        ctx.step_device(u, t, spec.dt)
-        t += spec.dt
+        u.copy_(u0)
+        ctx.step_device(u, 0.0, spec.dt)
     torch.cuda.synchronize()
     tr = time.perf_counter() - tr0
     ctx.set_timing(False)
@@ -370,18 +532,7 @@ def run_ours(args, spec, ws, rank, local):
     cgs_launch = r1["cgs_launches"] - r0["cgs_launches"]
     peak, peak_kind = _peaks()
     achieved = cgs_bytes / (cgs_ms * 1e-3) / 1e9 if cgs_ms > 0 else 0.0
-    traffic, tnote = None, None
-    try:  # DRAM bytes per CGS launch from the committed ncu capture (j = 8 sweeps)
-        tname = next(f for f in ("r1s4_cgs_traffic.json", "r1s3_cgs_traffic.json")
-                     if os.path.exists(os.path.join(ROOT, "profiles", f)))
-        with open(os.path.join(ROOT, "profiles", tname)) as fh:
-            tdoc = json.load(fh)
-        traffic = tdoc["traffic_per_launch"]
-        tnote = (f"ncu --set full, CGS sweeps at j={tdoc['j']}: {traffic / 1e6:.1f} MB DRAM per launch "
-                 f"vs {tdoc['algorithmic_per_launch'] / 1e6:.1f} MB algorithmic "
-                 f"(ratio {tdoc['ratio']:.3f}; profiles/{tname})")
-    except (OSError, KeyError, ValueError, StopIteration):
-        pass
+    traffic, tnote = _traffic_note()
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "traffic_note": tnote,
             "kernel": "k_cgs<DOT|UPD_DOT|UPD_NORM> (CGS2 sweeps)",
@@ -390,23 +541,22 @@ def run_ours(args, spec, ws, rank, local):
             "avg_launch_us": 1e3 * cgs_ms / max(1, cgs_launch),
             "share_of_step": (cgs_ms * 1e-3) / tr if tr > 0 else None}
 
-    # e2e: the public API with host buffers (H2D of u + D2H of u_next per step)
+    # e2e: the public API with host buffers (H2D of u + D2H of u_next per step),
     # the caller's state in page-locked memory (pk.step returns u_next pinned too)
-    uh = u_start.cpu().pin_memory().numpy()
-    t = t_start
+    uh = torch.from_numpy(u0h).pin_memory().numpy()
     if ws == 1:  # untimed: the caching host allocator's first page-locked blocks
         for _ in range(2):
-            pk.step(prob, uh, t, spec.dt, tab, cfg, prep=prep)
+            pk.step(prob, uh, 0.0, spec.dt, tab, cfg, prep=prep)
     e_stats = []
     barrier(ws)
     te0 = time.perf_counter()
     for _ in range(args.steps):
         if ws > 1:  # the slab context's host-buffer step (irkg_step_host)
-            st = ctx.step_host(uh, t, spec.dt)
-        else:  # the public irkit-style API with a host numpy state
-            uh, st = pk.step(prob, uh, t, spec.dt, tab, cfg, prep=prep)
+            ub = uh.copy()
+            st = ctx.step_host(ub, 0.0, spec.dt)
+        else:  # the public irkit-style API with a host numpy state: u_next is new
+            _, st = pk.step(prob, uh, 0.0, spec.dt, tab, cfg, prep=prep)
         e_stats.append(st)
-        t += spec.dt
     te = max_over_ranks(time.perf_counter() - te0, ws)
     e_dof = sum_over_ranks(sum(s.newton_iterations for s in e_stats) * spec.s * N, ws)
     e2e = {"value": e_dof / te, "unit": UNIT, "h2d_bytes_per_step": 8 * N,
@@ -419,21 +569,26 @@ def run_ours(args, spec, ws, rank, local):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Fourier-mode u0, BASELINE configs[1] shape)",
-            "config": {"workload": spec.name, "grid": list(prob.shape), "scheme": "gauss(3)",
-                       "dt": spec.dt, "inner": "jacobi-4", "variant": 3, "restart": 200,
-                       "parallelism": (f"slab{ws} (y-slabs, NCCL halos + allreduce; weak: "
-                                       f"configs[1] tiled {ws}x in y)") if ws > 1 else "1 GPU",
-                       "global_grid": list(prob.shape),
-                       "l2": "working set > L2 (V basis 201 x 16.8 MB per rank)"},
+            "config": _config(spec, ws, prob.shape),
+            "step_unit": "one IRK step of configs[1] from (t=0, u0): all its Newton iterations "
+                         "+ the u update (u reset from u0 by a device copy inside the timed "
+                         "region)",
             "steps_per_s": steps_per_s, "newton_iterations": newton, "krylov_iterations": krylov,
+            "krylov_per_newton": krylov / max(1, newton),
             "gpu_launches": launches, "roofline": roof, "e2e": e2e, "clocks": clk.summary(),
         }
+    ctx.close()
+    if rank == 0:
+        if ws == 1 and not args.no_large:
+            torch.cuda.empty_cache()
+            line["largest_config"] = largest_config(args, local)
         if ws == 1 and not args.no_cpu:
-            dof_cpu, el, kry, cores = cpu_sample(spec, 1)
+            dof_cpu, el, kry, cores, kind = cpu_sample(spec, 1)
             line["cpu_baseline"] = {
-                "value": dof_cpu, "unit": UNIT, "cores": cores, "kind": "port",
-                "sample": f"first Newton iteration of step 1 at full 1024^2 on the numpy/scipy "
-                          f"restatement of irkit (oracle/irk.py): {el:.1f} s, {kry} Krylov its",
+                "value": dof_cpu, "unit": UNIT, "cores": cores, "kind": kind,
+                "sample": f"first Newton iteration of configs[1] step 1 at full 1024^2 on "
+                          f"{'irkit (baseline/_ref)' if kind == 'reference' else 'the numpy/scipy restatement of irkit (oracle/irk.py)'}"
+                          f": {el:.1f} s, {kry} Krylov its, host BLAS threads = {cores}",
             }
         print(json.dumps(line), flush=True)
     return line
@@ -447,6 +602,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=None, help="override grid size (testing)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-large", action="store_true", help="skip the configs[2] P=1 step")
+    ap.add_argument("--large-n", type=int, default=4096, help="configs[2] grid (testing)")
     args = ap.parse_args()
     from paper_2101_01776_b200.problems import baseline_config
 

@@ -8,10 +8,14 @@
 //     UPD_NORM  s_{j+1} = w1 - V c2, ||s_{j+1}||^2; last CTA finishes the column
 // Each CTA streams row tiles of all (j+1) basis slots + w into a shared-memory
 // ring of up to CGS_MAXST tiles (one mbarrier each) with TMA bulk copies:
-// 2-D tensor-map boxes for tiles of <= 256 rows, else one 1-D copy per slot.
-// The tile is read once from HBM for both the update and the dots.  Per-CTA
-// partials are folded by the last CTA in fixed order (deterministic, no fp
-// atomics).
+// 2-D tensor-map boxes (popcount(j+1) boxes of 2^b slots) or, per the
+// IRKG_CGS_1D sweep mask (default: all three sweeps in tiles of >= 256
+// rows), one 1-D cp.async.bulk per slot.  The only partial tile (the
+// globally last) is loaded with generic zero-padded loads.  The tile is read
+// once from HBM for both the update and the dots.  Per-CTA partials are
+// folded in a fixed order (deterministic, no fp atomics) by every CTA of the
+// NEXT sweep (UPD_DOT folds DOT's, UPD_NORM folds UPD_DOT's); UPD_NORM's are
+// folded by its last CTA, which finishes the Hessenberg column.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -555,7 +559,8 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
     const int r0 = ph(t) * TRC;
     const int rows = min(TRC, A.n - r0);
     double *buf = A.ring + (size_t)s * (A.L + 1) * TRC;
-    if (tile_full<TRC>(A, ph(t))) {
+    const bool full = tile_full<TRC>(A, ph(t));
+    if (full) {
       while (!mbar_try_wait(&A.bars[s], phase)) {
       }
     } else {
@@ -565,8 +570,11 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
       tile_compute_ro<MODE, TRC, LR>(A, csr, buf, r0, rows, acc, nrm);
     } else {
       tile_compute<MODE, TRC>(A, buf, r0, rows, acc, nrm);
-      if (MODE == CGS_UPD_DOT) fence_proxy_async();
-    }  // wt was written via the generic proxy
+    }
+    // the slot is refilled by TMA below: order this thread's generic-proxy
+    // writes to it (the zero-padded tail tile; the slot-owner UPD_DOT's w1)
+    // before the async-proxy copy
+    if (!full || (LMAX == 0 && MODE == CGS_UPD_DOT)) fence_proxy_async();
     __syncthreads();  // stage s consumed
     {
       const int tn = t + NST * G;

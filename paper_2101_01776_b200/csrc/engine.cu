@@ -144,6 +144,7 @@ Engine::~Engine() {
   dae_fini();
   free_ghosts();
   delete comm;
+  release_l2_limit();
 }
 
 void Engine::ensure_stage_buffers() {
@@ -178,6 +179,31 @@ void Engine::ensure_basis(int restart) {
 // are the hottest lines of the solve; a persisting access-policy window over
 // them (on the CGS launches only) keeps them out of the streaming LRU churn
 // once the basis outgrows L2.
+//
+// cudaLimitPersistingL2CacheSize is device-wide: the engines of a process
+// share it through a per-device refcount; the first one records the limit it
+// found, later ones only raise it, and the last one to go resets the
+// persisting lines (cudaCtxResetPersistingL2Cache) and restores the limit, so
+// nothing is left set aside for torch or other libraries on the GPU.
+namespace {
+constexpr int kMaxDev = 64;
+int g_l2_users[kMaxDev] = {};
+size_t g_l2_prev[kMaxDev] = {};
+size_t g_l2_set[kMaxDev] = {};
+}  // namespace
+
+void Engine::release_l2_limit() {
+  if (!l2_holder) return;
+  l2_holder = false;
+  if (device < 0 || device >= kMaxDev) return;
+  if (--g_l2_users[device] == 0) {
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_l2_prev[device]);
+    g_l2_set[device] = 0;
+    cudaGetLastError();
+  }
+}
+
 void Engine::set_l2_window() {
   l2win = cudaAccessPolicyWindow{};
   if (l2_budget == 0 || l2_persist_max == 0 || l2_window_max == 0 || !V) return;
@@ -187,9 +213,24 @@ void Engine::set_l2_window() {
   size_t bytes = (size_t)(vcap + 1) * (size_t)vpitch * sizeof(double);
   bytes = std::min(std::min(bytes, l2_budget), l2_window_max);
   const size_t persist = std::min(bytes, l2_persist_max);
-  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist) != cudaSuccess) {
-    cudaGetLastError();
-    return;
+  if (device < 0 || device >= kMaxDev) return;
+  if (!l2_holder) {
+    if (g_l2_users[device]++ == 0) {
+      if (cudaDeviceGetLimit(&g_l2_prev[device], cudaLimitPersistingL2CacheSize) != cudaSuccess) {
+        cudaGetLastError();
+        g_l2_prev[device] = 0;
+      }
+      g_l2_set[device] = 0;
+    }
+    l2_holder = true;
+  }
+  if (persist > g_l2_set[device]) {
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist) != cudaSuccess) {
+      cudaGetLastError();
+      release_l2_limit();
+      return;
+    }
+    g_l2_set[device] = persist;
   }
   l2win.base_ptr = V;
   l2win.num_bytes = bytes;

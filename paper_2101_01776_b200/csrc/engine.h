@@ -322,6 +322,8 @@ struct Engine {
   size_t l2_budget = 51u << 20;
   size_t l2_persist_max = 0, l2_window_max = 0;
   cudaAccessPolicyWindow l2win{};
+  bool l2_holder = false;  // counted in the per-device persisting-limit refcount
+  void release_l2_limit();
   void set_l2_window();
   int cgs_ef_from() const;
   // All Arnoldi-body kernels ask for the maximum shared-memory carveout, so

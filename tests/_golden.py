@@ -70,3 +70,38 @@ def oracle_config(solver):
 
     fields = irk.Config.__dataclass_fields__
     return irk.Config(**{k: v for k, v in solver.items() if k in fields})
+
+
+#: Goldens at the sizes SURVEY §8(c) / BASELINE.md §3 prescribe (full-size
+#: configs[1]; configs[2]/[4] at 256^2 x 10 steps; configs[3] at 48^3/64^3 x
+#: 5 steps).  The GPU tests run them all; the CPU oracle tests skip them
+#: (minutes of numpy each) -- the oracle is pinned on the smaller cases.
+def is_survey_size(name):
+    return name == "cfg1_full" or name.endswith("_s10") or name.endswith("_s5")
+
+
+def assert_counts_within_one(got_steps, want_steps, per_block=True):
+    """The north star's count bar: the same number of steps, per-step Newton
+    and Krylov counts within +/-1, and (when the Newton counts agree) the
+    per-block iteration lists of the same length with every entry within
+    +/-1.  Returns the largest deviations seen (for the parity record)."""
+    got_steps = list(got_steps)
+    assert len(got_steps) == len(want_steps), (len(got_steps), len(want_steps))
+    worst = {"newton": 0, "krylov": 0, "block": 0}
+    for i, (got, want) in enumerate(zip(got_steps, want_steps)):
+        dn = abs(got.newton_iterations - want["newton_iterations"])
+        dk = abs(got.krylov_iterations - want["krylov_iterations"])
+        assert dn <= 1, ("newton", i, got.newton_iterations, want["newton_iterations"])
+        assert dk <= 1, ("krylov", i, got.krylov_iterations, want["krylov_iterations"])
+        worst["newton"] = max(worst["newton"], dn)
+        worst["krylov"] = max(worst["krylov"], dk)
+        if per_block and dn == 0:
+            wb = {int(k): v for k, v in want["block_iterations"].items()}
+            assert sorted(got.block_iterations) == sorted(wb), (i, got.block_iterations, wb)
+            for off, its in wb.items():
+                g = got.block_iterations[off]
+                assert len(g) == len(its), (i, off, g, its)
+                d = max((abs(a - b) for a, b in zip(g, its)), default=0)
+                assert d <= 1, (i, off, g, its)
+                worst["block"] = max(worst["block"], d)
+    return worst

@@ -100,6 +100,7 @@ def _cfg(solver):
         krylov_maxit=solver.get("krylov_maxit", 200),
         restart=solver.get("restart", 200),
         precond=PrecondSpec(gamma_mode=solver.get("gamma_mode", "star"), inner=inner),
+        jacobian_refresh=solver.get("jacobian_refresh", "every"),
     )
 
 
@@ -269,6 +270,40 @@ def run_larger():
     run_case("cfg3_n32", sp3.problem, sp3.u0(), "gauss", 5, sp3.dt, 1, sp3.solver)
 
 
+SURVEY_CASES = {
+    # SURVEY §8(c) / BASELINE.md §3 plan: the BASELINE configs at the sizes the
+    # survey prescribes for the oracle comparison (full size where irkit can
+    # run it in host RAM, else the reduced grid with the full step count).
+    "cfg1_full": lambda: _survey_ode(1, None, None, "cfg1_full"),
+    "cfg2_gauss2_n256_s10": lambda: _survey_ode(2, 256, 10, "cfg2_gauss2_n256_s10"),
+    "cfg2_radau_iia3_n256_s10": lambda: _survey_ode(2, 256, 10, "cfg2_radau_iia3_n256_s10",
+                                                    family="radau_iia", s=3),
+    "cfg3_n48_s5": lambda: _survey_ode(3, 48, 5, "cfg3_n48_s5"),
+    "cfg3_n64_s5": lambda: _survey_ode(3, 64, 5, "cfg3_n64_s5"),
+    "dae_n256_gauss2_s10": lambda: run_dae_case("dae_n256_gauss2_s10", 256, "gauss", 2, 10),
+}
+
+
+def _survey_ode(index, n, nsteps, name, family=None, s=None):
+    sp = baseline_config(index, n=n, nsteps=nsteps, family=family, s=s)
+    run_case(name, sp.problem, sp.u0(), sp.family, sp.s, sp.dt, sp.nsteps, sp.solver)
+
+
+def run_frozen():
+    """Simplified Newton (jacobian_refresh="frozen", src/nonlinear.py:204-209)
+    on 2-D Burgers and on the 1-D KPP reaction problem."""
+    prob = GridProblem("burgers", (48, 48), nu=2e-2)
+    u0 = fourier_u0(prob.shape, 1, 4, 0.5, seed=6)
+    run_case("frozen_burgers48_radau2", prob, u0, "radau_iia", 2, 5e-3, 3,
+             dict(variant=3, inner=4, krylov_maxit=4000, newton_maxit=60,
+                  jacobian_refresh="frozen"))
+    prob = GridProblem("rad", (64,), nu=1e-3, c=0.5, lam=1.0, mu=-1.0)
+    u0 = 0.5 + fourier_u0(prob.shape, 1, 3, 0.1, seed=7)
+    run_case("frozen_rad1d_gauss3", prob, u0, "gauss", 3, 0.05, 3,
+             dict(variant=3, inner=4, krylov_rtol=1e-8, newton_maxit=60,
+                  jacobian_refresh="frozen"))
+
+
 def run_dae():
     run_dae_case("dae_n16_gauss2", 16, "gauss", 2, 3)
     run_dae_case("dae_n64_gauss2", 64, "gauss", 2, 4)
@@ -278,6 +313,9 @@ def run_dae():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["tableaux", "transformed", "configs", "dae", "sdirk", "larger"]
+    for case in which:
+        if case in SURVEY_CASES:
+            SURVEY_CASES[case]()
     if "dae" in which:
         run_dae()
     if "larger" in which:
@@ -290,3 +328,5 @@ if __name__ == "__main__":
         run_configs()
     if "sdirk" in which:
         run_sdirk()
+    if "frozen" in which:
+        run_frozen()

@@ -11,7 +11,7 @@ from oracle import irk
 from oracle import tableau as otab
 from oracle.problems import DaeProblemDef
 
-from _golden import case_names, load_dae_case
+from _golden import assert_counts_within_one, case_names, load_dae_case
 
 pytestmark = pytest.mark.gpu
 
@@ -32,9 +32,8 @@ def test_dae_integrate_matches_reference_golden(name):
     ru = np.linalg.norm(res.u_final - meta["u_final"]) / np.linalg.norm(meta["u_final"])
     rw = np.linalg.norm(res.w_final - meta["w_final"]) / np.linalg.norm(meta["w_final"])
     assert ru <= 1e-10 and rw <= 1e-10, (ru, rw)
+    assert_counts_within_one(res.step_stats, meta["steps"])
     for got, want in zip(res.step_stats, meta["steps"]):
-        assert abs(got.newton_iterations - want["newton_iterations"]) <= 1
-        assert abs(got.krylov_iterations - want["krylov_iterations"]) <= want["newton_iterations"]
         assert got.constraint_solves == want["constraint_solves"]
         assert got.differential_solves == 2 * got.krylov_iterations
         assert got.constraint_residual <= 1e-11
@@ -55,7 +54,7 @@ def test_dae_stage_residual_and_step_match_oracle():
     assert np.linalg.norm(u1 - ou) <= 1e-11 * np.linalg.norm(ou)
     assert np.linalg.norm(w1 - ow) <= 1e-11 * np.linalg.norm(ow)
     assert st.newton_iterations == ost.newton_iterations
-    assert abs(st.krylov_iterations - ost.krylov_iterations) <= ost.newton_iterations
+    assert abs(st.krylov_iterations - ost.krylov_iterations) <= 1
 
 
 def test_dae_inconsistent_initial_state_is_rejected():

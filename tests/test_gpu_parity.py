@@ -15,7 +15,7 @@ from oracle import tableau as otab
 from oracle.problems import build_problem
 from paper_2101_01776_b200.problems import GridProblem
 
-from _golden import case_names, grid_problem, load_case, load_transformed
+from _golden import assert_counts_within_one, case_names, grid_problem, load_case, load_transformed
 
 pytestmark = pytest.mark.gpu
 
@@ -31,6 +31,7 @@ def _solver(sv):
         krylov_maxit=sv.get("krylov_maxit", 200),
         restart=sv.get("restart", 200),
         precond=pk.PrecondSpec(inner=sv.get("inner", 4)),
+        jacobian_refresh=sv.get("jacobian_refresh", "every"),
     )
 
 
@@ -47,10 +48,9 @@ def test_integrate_matches_reference_golden(name):
     ref = meta["u_final"]
     rel = np.linalg.norm(res.u_final - ref) / np.linalg.norm(ref)
     assert rel <= RTOL_U, rel
-    for got, want in zip(res.step_stats, meta["steps"]):
-        assert abs(got.newton_iterations - want["newton_iterations"]) <= 1
-        assert abs(got.krylov_iterations - want["krylov_iterations"]) <= max(
-            1, want["newton_iterations"])
+    # per-step Newton and Krylov counts within +/-1, per-block lists within +/-1
+    assert_counts_within_one(res.step_stats, meta["steps"])
+    for got in res.step_stats:
         assert got.precond_applications >= got.krylov_iterations
         assert got.converged
 
@@ -71,6 +71,7 @@ def test_config0_exact_inner_mode_matches_reference_golden():
     res = pk.integrate(prob, meta["u0"], 0.0, meta["nsteps"] * meta["dt"], meta["dt"], tab, cfg)
     rel = np.linalg.norm(res.u_final - meta["u_final"]) / np.linalg.norm(meta["u_final"])
     assert rel <= RTOL_U, rel
+    assert len(res.step_stats) == len(meta["steps"])
     for got, want in zip(res.step_stats, meta["steps"]):
         assert got.newton_iterations == want["newton_iterations"]
         assert got.block_iterations == want["block_iterations"]
@@ -108,6 +109,7 @@ def test_config0_counts_exact_per_block():
     prob = grid_problem(meta)
     tab = pk.make_tableau("gauss", 2)
     res = pk.integrate(prob, meta["u0"], 0.0, 10e-3, 1e-3, tab, _solver(meta["solver"]))
+    assert len(res.step_stats) == len(meta["steps"])
     for got, want in zip(res.step_stats, meta["steps"]):
         assert got.newton_iterations == want["newton_iterations"]
         for off, its in want["block_iterations"].items():
