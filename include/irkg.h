@@ -274,6 +274,23 @@ int irkg_prepare_linearization(irkg_ctx *ctx, const double *u_dev, const double 
 int irkg_transformed_solve(irkg_ctx *ctx, double dt, const double *rhs_dev, double *dk_dev,
                            irkg_step_stats *stats);
 
+/* solve_transformed_system(..., variant_jacobian=vj) (src/irk_core.py:225-237)
+ * with a VariantJacobian (src/nonlinear.py:86-96) supplied by the caller
+ * instead of irkg_prepare_linearization: `diag` holds the s diagonal
+ * operators, (off_i[q], off_j[q]) -> off[q] the coupling operators; a field
+ * with a_dev = NULL and sigma = 0 is a skipped (zero) key.  The fields are
+ * copied; the next irkg_transformed_solve uses them. */
+int irkg_set_variant_jacobian(irkg_ctx *ctx, const irkg_opfield *diag, int n_off,
+                              const int *off_i, const int *off_j, const irkg_opfield *off);
+
+/* y = L x for one operator field: the matvec of a stage operator / a
+ * combine()d sum (SparseMatrix.__matmul__, src/sparsela.py:29-103). */
+int irkg_operator_apply(irkg_ctx *ctx, const irkg_opfield *l, const double *x_dev,
+                        double *y_dev);
+
+/* OdeSystem.rhs (src/nonlinear.py:35-48): f = N(u, t) (autonomous kinds; one rank). */
+int irkg_rhs(irkg_ctx *ctx, const double *u_dev, double t, double *f_dev);
+
 /* ---- index-1 DAE (vorticity/streamfunction, IRKG_KIND_ARAKAWA) ----
  * State uw = [u; w] (2N: vorticity then streamfunction), stage arrays
  * (s, 2N) with rows [k_i; l_i] -- the reference's composite layout

@@ -35,8 +35,11 @@ from .solver import (
     ShiftedSolver,
     StageLinearization,
     StageState,
+    VariantJacobian,
     apply_block2x2,
     block_gmres,
+    build_variant_jacobian,
+    combine,
     dae_integrate,
     dae_step,
     integrate,
@@ -45,6 +48,7 @@ from .solver import (
     solve_transformed_system,
     stage_residual,
     step,
+    variant_weights,
 )
 from .stats import IntegrationResult, KrylovReport, SolveStats, StepStats, write_step_stats_csv
 from .tableau import (
@@ -89,7 +93,10 @@ __all__ = [
     "StageState",
     "StepFailureError",
     "StepStats",
+    "VariantJacobian",
     "apply_block2x2",
+    "build_variant_jacobian",
+    "combine",
     "baseline_config",
     "block_gmres",
     "fourier_u0",
@@ -102,5 +109,6 @@ __all__ = [
     "solve_transformed_system",
     "stage_residual",
     "step",
+    "variant_weights",
     "write_step_stats_csv",
 ]

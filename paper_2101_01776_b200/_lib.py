@@ -186,6 +186,10 @@ _SIGS = {
     ),
     "irkg_prepare_linearization": (_I, [_P, _P, _P, _D]),
     "irkg_transformed_solve": (_I, [_P, _D, _P, _P, C.POINTER(StepStatsC)]),
+    "irkg_set_variant_jacobian": (_I, [_P, C.POINTER(OpField), _I, C.POINTER(C.c_int),
+                                       C.POINTER(C.c_int), C.POINTER(OpField)]),
+    "irkg_operator_apply": (_I, [_P, C.POINTER(OpField), _P, _P]),
+    "irkg_rhs": (_I, [_P, _P, _D, _P]),
     "irkg_dae_stage_residual": (_I, [_P, _P, _P, _D, _D, _P, C.POINTER(_D)]),
     "irkg_dae_step": (_I, [_P, _P, _D, _D, C.POINTER(StepStatsC)]),
     "irkg_dae_step_host": (_I, [_P, _P, _D, _D, C.POINTER(StepStatsC)]),

@@ -46,6 +46,13 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                : "memory");
 }
 
+// plain arrival (no transaction bytes): completes the phase of a ring slot
+// whose tile is not TMA-loaded (the zero-padded tail tile), so every slot
+// advances exactly one phase per ring round and the parity waits stay in step
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -513,8 +520,12 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
   // part of the first NST tiles goes out while the predecessor drains; w
   // (and the coefficients) only after pdl_wait()
   for (int i = 0; i < NST; ++i)
-    if (t0 + i * G < ntiles && tile_full<TRC>(A, ph(t0 + i * G)))
-      tile_issue<TRC>(A, ph(t0 + i * G), i, false);
+    if (t0 + i * G < ntiles) {
+      if (tile_full<TRC>(A, ph(t0 + i * G)))
+        tile_issue<TRC>(A, ph(t0 + i * G), i, false);
+      else if (threadIdx.x == 0)
+        mbar_arrive(&A.bars[i]);  // the tail tile: generic loads at consumption
+    }
   pdl_wait();
   fence_proxy_async_global();  // w was written through the generic proxy
   for (int i = 0; i < NST; ++i)
@@ -560,12 +571,11 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
     const int rows = min(TRC, A.n - r0);
     double *buf = A.ring + (size_t)s * (A.L + 1) * TRC;
     const bool full = tile_full<TRC>(A, ph(t));
-    if (full) {
-      while (!mbar_try_wait(&A.bars[s], phase)) {
-      }
-    } else {
-      tile_load_tail<TRC>(A, buf, r0, rows);
+    // every slot completes one phase per ring round (TMA bytes, or the plain
+    // arrival issued for the tail tile), so the parity wait is uniform
+    while (!mbar_try_wait(&A.bars[s], phase)) {
     }
+    if (!full) tile_load_tail<TRC>(A, buf, r0, rows);
     if constexpr (LMAX > 0) {
       tile_compute_ro<MODE, TRC, LR>(A, csr, buf, r0, rows, acc, nrm);
     } else {
@@ -578,7 +588,12 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
     __syncthreads();  // stage s consumed
     {
       const int tn = t + NST * G;
-      if (tn < ntiles && tile_full<TRC>(A, ph(tn))) tile_issue<TRC>(A, ph(tn), s);
+      if (tn < ntiles) {
+        if (tile_full<TRC>(A, ph(tn)))
+          tile_issue<TRC>(A, ph(tn), s);
+        else if (threadIdx.x == 0)
+          mbar_arrive(&A.bars[s]);
+      }
     }
     if (++s == NST) {
       s = 0;

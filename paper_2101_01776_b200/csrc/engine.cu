@@ -129,7 +129,7 @@ Engine::~Engine() {
   cudaStreamSynchronize(stream);
   void *bufs[] = {part, counter, scal_dev, ctrl_dev, W.H, W.cs, W.sn, W.g, W.alpha, W.y,
                   W.c1, W.c2, W.res, V, wbuf, zbuf, ubuf, tmp_x, tmp_t, U, F, Gs, Y, DK,
-                  Kst, RHS, ufield, opA, vmaps};
+                  Kst, RHS, ufield, opA, vmaps, zero_n};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (ctrl_host) cudaFreeHost(ctrl_host);
@@ -725,6 +725,58 @@ void Engine::build_weights() {
   }
 }
 
+// A VariantJacobian given directly (src/nonlinear.py:86-96; the reference's
+// solve_transformed_system(..., variant_jacobian=vj), src/irk_core.py:225-237):
+// the s diagonal fields and the coupling fields keyed (i, j) are copied into
+// the operator slots the transformed solve reads.  A field with a NULL
+// coefficient array and sigma = 0 is the zero operator (a skipped key).
+void Engine::set_variant_jacobian(const irkg_opfield *diag, int n_off, const int *oi,
+                                  const int *oj, const irkg_opfield *off) {
+  if (n_off < 0 || s + n_off > MAXOPS) throw SolveError(IRKG_ERR_CONFIG, "too many operator fields");
+  nops = s + n_off;
+  if (nops > nops_cap) {
+    dalloc(&opA, (size_t)nops * N);
+    nops_cap = nops;
+  }
+  for (int i = 0; i < MAXS; ++i)
+    for (int j = 0; j < MAXS; ++j) od_slot[i][j] = -1;
+  weights = OpWeights{};
+  weights.nops = nops;
+  weights.s = s;
+  for (int o = 0; o < nops; ++o) {
+    const irkg_opfield &f = o < s ? diag[o] : off[o - s];
+    if (o < s) {
+      diag_slot[o] = o;
+    } else {
+      const int i = oi[o - s], j = oj[o - s];
+      if (i < 0 || i >= s || j < 0 || j >= s || i == j)
+        throw SolveError(IRKG_ERR_VALUE, "coupling key out of range");
+      od_slot[i][j] = o;
+    }
+    double *dst = opA + (size_t)o * N;
+    if (f.a_dev)
+      check(cudaMemcpyAsync(dst, f.a_dev, (size_t)N * sizeof(double), cudaMemcpyDeviceToDevice,
+                            stream), "variant jacobian copy");
+    else
+      check(cudaMemsetAsync(dst, 0, (size_t)N * sizeof(double), stream), "variant jacobian zero");
+    op_sigma[o] = f.sigma;
+    op_zero[o] = (f.a_dev == nullptr && f.sigma == 0.0);
+  }
+  if (slab())
+    for (int o = 0; o < nops; ++o)
+      if (!op_zero[o]) exchange(R_OP + o, opA + (size_t)o * N, jhalo());
+}
+
+// N(u) for one state (OdeSystem.rhs): the stage residual kernel with one
+// stage and K = 0.
+void Engine::rhs(const double *u, double *f) {
+  if (!zero_n) {
+    dalloc(&zero_n, N);
+    check(cudaMemsetAsync(zero_n, 0, (size_t)N * sizeof(double), stream), "zero");
+  }
+  residual(u, zero_n, f, 1);
+}
+
 Op Engine::op_of(int slot) const {
   Op o{};
   if (slot < 0 || op_zero[slot]) {
@@ -1278,6 +1330,46 @@ int irkg_prepare_linearization(irkg_ctx *ctx, const double *u_dev, const double 
     if (e.dae) throw SolveError(IRKG_ERR_CONFIG, "DAE context: use the irkg_dae_* entry points");
     e.stage_values(u_dev, k_dev, dt, e.U);
     e.build_linearization(e.U);
+    check(cudaStreamSynchronize(e.stream));
+  });
+}
+
+int irkg_set_variant_jacobian(irkg_ctx *ctx, const irkg_opfield *diag, int n_off,
+                              const int *off_i, const int *off_j, const irkg_opfield *off) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    if (!e.have_tab) throw SolveError(IRKG_ERR_CONFIG, "tableau not set");
+    if (e.dae) throw SolveError(IRKG_ERR_CONFIG, "DAE context: use the irkg_dae_* entry points");
+    e.set_variant_jacobian(diag, n_off, off_i, off_j, off);
+    check(cudaStreamSynchronize(e.stream));
+  });
+}
+
+int irkg_operator_apply(irkg_ctx *ctx, const irkg_opfield *l, const double *x_dev,
+                        double *y_dev) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    if (e.dae) throw SolveError(IRKG_ERR_CONFIG, "DAE context: use the irkg_dae_* entry points");
+    BlockSpec B{};
+    B.size = 1;
+    B.eta = 0.0;  // y = eta x - dt L x with eta = 0, dt = -1
+    B.beta = 0.0;
+    B.phi = 1.0;
+    B.dt = -1.0;
+    B.l1 = to_op(l);
+    B.l1.present = 1;
+    e.block_op(B, x_dev, y_dev, nullptr, nullptr, nullptr);
+    check(cudaStreamSynchronize(e.stream));
+  });
+}
+
+int irkg_rhs(irkg_ctx *ctx, const double *u_dev, double t, double *f_dev) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    (void)t;  // every supported kind is autonomous
+    if (e.dae) throw SolveError(IRKG_ERR_CONFIG, "DAE context: use the irkg_dae_* entry points");
+    if (e.nranks > 1) throw SolveError(IRKG_ERR_CONFIG, "irkg_rhs: one rank only");
+    e.rhs(u_dev, f_dev);
     check(cudaStreamSynchronize(e.stream));
   });
 }

@@ -156,6 +156,7 @@ struct Engine {
   double *RHS = nullptr;        // (2, N) block rhs
   double *ufield = nullptr;     // N (step_host staging)
   double *opA = nullptr;        // (nops, N) operator fields
+  double *zero_n = nullptr;     // N zeros (irkg_rhs: K = 0)
   int nops_cap = 0;
   GCtrl *ctrl_host = nullptr;   // pinned mirror
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evp[2] = {nullptr, nullptr};
@@ -382,6 +383,9 @@ struct Engine {
                   int restart, bool want_residuals = true);
   void build_linearization(const double *U);
   Op op_of(int slot) const;
+  void set_variant_jacobian(const irkg_opfield *diag, int n_off, const int *oi, const int *oj,
+                            const irkg_opfield *off);
+  void rhs(const double *u, double *f);
   double gamma_of(double eta, double beta) const;
   // dk == nullptr: leave y in Y (the Newton loop fuses dk = (Q R0) y into its update)
   void transformed_solve(double dt, const double *rhs, double *dk, irkg_step_stats *stats);

@@ -80,6 +80,23 @@ class GridProblem:
     def h(self):
         return tuple(L / n for L, n in zip(self.box, self.shape))
 
+    # ---- the OdeSystem protocol (src/nonlinear.py:35-48): dim, rhs,
+    # linearize, mass, name -- so a GridProblem is itself a valid irkit
+    # OdeSystem whose callables run on the device (irkg_rhs; the Jacobian is
+    # a matrix-free OperatorField whose ``@`` / ``matvec`` is
+    # irkg_operator_apply)
+    def rhs(self, u, t=0.0):
+        """N(u, t) by the device stencil kernel; numpy in -> numpy out."""
+        from .solver import problem_rhs
+
+        return problem_rhs(self, u, t)
+
+    def linearize(self, u, t=0.0):
+        """The exact Jacobian dN/du at u as a device ``OperatorField``."""
+        from .solver import OperatorField
+
+        return OperatorField.linearize(self, u)
+
     def oracle_params(self):
         """Keyword arguments for ``oracle.problems.build_problem`` (tests only)."""
         p = {"lengths": self.box}

@@ -42,6 +42,20 @@ def _check_sys(sys):
         )
 
 
+def problem_rhs(sys, u, t=0.0):
+    """``OdeSystem.rhs`` of a GridProblem on the device (irkg_rhs)."""
+    _check_sys(sys)
+    ctx = context_for(sys)
+    ud = as_device(u).reshape(-1)
+    if ud.numel() != sys.dim:
+        raise ValueError(f"u has {ud.numel()} entries, the system has {sys.dim}")
+    f = torch().empty_like(ud)
+    rc = ctx.lib.irkg_rhs(ctx.h, ptr(ud), float(t), ptr(f))
+    if rc:
+        _raise(rc)
+    return _out(f, u)
+
+
 def _is_torch(x):
     try:
         return isinstance(x, torch().Tensor)
@@ -243,6 +257,113 @@ class OperatorField:
         a, sig = ctx.linearize(U.contiguous(), weights)
         return cls(problem, a, sig)
 
+    @property
+    def n(self):
+        return self.problem.dim
+
+    def matvec(self, x):
+        """``L x`` on the device (SparseMatrix.matvec, src/sparsela.py:29-103)."""
+        xd = as_device(x)
+        if tuple(xd.shape) != (self.n,):
+            raise ValueError(f"x has shape {tuple(xd.shape)}, expected ({self.n},)")
+        ctx = context_for(self.problem)
+        y = torch().empty_like(xd)
+        rc = ctx.lib.irkg_operator_apply(ctx.h, opfield(self), ptr(xd), ptr(y))
+        if rc:
+            _raise(rc)
+        return _out(y, x)
+
+    def __matmul__(self, x):
+        return self.matvec(x)
+
+
+def combine(coeffs, fields):
+    """``sum_k c_k L_k`` of operator fields of one problem
+    (src/sparsela.py:106-128): zero weights skipped, summed in order k = 0..,
+    the same association the reference's CSR sum uses; None when every
+    weight is zero (the reference's empty matrix)."""
+    coeffs = [float(c) for c in coeffs]
+    fields = list(fields)
+    if len(coeffs) != len(fields):
+        raise ValueError("coefficient / operator count mismatch")
+    a, sig, prob = None, 0.0, None
+    for c, f in zip(coeffs, fields):
+        if c == 0.0:
+            continue
+        prob = f.problem
+        term = None if f.a is None else c * f.a
+        a = term if a is None else (a if term is None else a + term)
+        sig += c * f.sigma
+    if prob is None:
+        return None
+    return OperatorField(prob, a, sig)
+
+
+def _opfield_value(f):
+    """OperatorField (or None: a skipped, all-zero key) -> irkg_opfield value."""
+    out = _lib.OpField()
+    if f is None:
+        out.a_dev = None
+        out.sigma = 0.0
+        return out
+    if f.a is not None and not f.a.is_contiguous():
+        f.a = f.a.contiguous()
+    out.a_dev = C.c_void_p(f.a.data_ptr()) if f.a is not None else None
+    out.sigma = float(f.sigma)
+    return out
+
+
+@dataclass
+class VariantJacobian:
+    """The variant's diagonal and coupling operators (src/nonlinear.py:86-96)
+    as device operator fields: ``diag`` one per stage row, ``offdiag``
+    keyed ``(i, j)``."""
+
+    diag: tuple
+    offdiag: dict
+
+
+def variant_weights(prep, variant, variant0_stage=0):
+    """Per-row stage weights and coupling weights of each variant
+    (src/nonlinear.py:99-126): the same index logic (argmax |d_ii| first on
+    ties, variant-3 keys i<j plus the sub-diagonal of every 2x2 block)."""
+    s = prep.tableau.s
+    d = np.asarray(prep.d, dtype=float)
+    diag = np.zeros((s, s))
+    offdiag = {}
+    if variant == 0:
+        diag[:, variant0_stage] = 1.0
+        return diag, offdiag
+    if variant == 1:
+        for i in range(s):
+            diag[i, int(np.argmax(np.abs(d[i, i])))] = 1.0
+        return diag, offdiag
+    for i in range(s):
+        diag[i] = d[i, i]
+    if variant == 2:
+        return diag, offdiag
+    for i in range(s):
+        for j in range(i + 1, s):
+            offdiag[(i, j)] = d[i, j]
+    for blk in prep.schur.blocks:
+        if blk.size == 2:
+            i = blk.offset
+            offdiag[(i + 1, i)] = d[i + 1, i]
+    return diag, offdiag
+
+
+def build_variant_jacobian(prep, stage_ops, variant, variant0_stage=0):
+    """src/nonlinear.py:129-142 over device operator fields (one per stage,
+    e.g. ``OperatorField.linearize(sys, U_i)`` or ``sys.linearize(U_i, t_i)``)."""
+    stage_ops = list(stage_ops)
+    s = prep.tableau.s
+    if len(stage_ops) != s:
+        raise ValueError(f"expected {s} stage operators, got {len(stage_ops)}")
+    dw, ow = variant_weights(prep, variant, variant0_stage)
+    diag = tuple(combine(dw[i], stage_ops) for i in range(s))
+    offdiag = {key: combine(w, stage_ops) for key, w in ow.items()}
+    return VariantJacobian(diag=diag, offdiag=offdiag)
+
 
 @dataclass(frozen=True)
 class Block2x2System:
@@ -368,26 +489,54 @@ def solve_transformed_system(prep, stage_ops=None, variant=None, dt=None, rhs_st
                              krylov_maxit=200, restart=200, variant_jacobian=None):
     """Solve one linearised stage system through the Schur transform.
 
-    ``stage_ops`` is a :class:`StageLinearization`.  Returns ``(k, SolveStats)``;
-    a non-convergent block solve raises StageSolveError(block_offset, report).
+    The operators come as in the reference (src/irk_core.py:225-237): either
+    ``variant_jacobian`` (a :class:`VariantJacobian` of operator fields, e.g.
+    from :func:`build_variant_jacobian`), or ``stage_ops`` + ``variant`` with
+    ``stage_ops`` a list of s :class:`OperatorField` (the device analogue of
+    the list of CSR stage operators) or a :class:`StageLinearization` (stage
+    values; the fields are formed on the device).  Returns ``(k,
+    SolveStats)``; a non-convergent block solve raises
+    StageSolveError(block_offset, report).
     """
-    if variant_jacobian is not None:
-        raise ConfigurationError("pass stage_ops=StageLinearization(...) and variant")
     if mass is not None:
         raise ConfigurationError("identity mass only")
     if dt is None or dt <= 0.0:
         raise ValueError("dt must be positive")
-    lin = stage_ops
     s = prep.tableau.s
     rhs = as_device(rhs_stages)
     if rhs.shape[0] != s:
         raise ValueError(f"rhs has {rhs.shape[0]} stage rows, expected {s}")
-    cfg = SolverConfig(variant=variant, krylov_rtol=krylov_rtol, krylov_maxit=krylov_maxit,
-                       restart=restart, precond=precond)
-    ctx = context_for(lin.sys)
-    ctx.set_prep(prep)
-    ctx.set_config(cfg)
-    ctx.prepare_linearization(lin.u, lin.k.reshape(s, -1), lin.dt)
+    if variant_jacobian is None and not isinstance(stage_ops, StageLinearization):
+        if stage_ops is None or variant is None:
+            raise ValueError("need variant_jacobian or stage_ops with variant")
+        variant_jacobian = build_variant_jacobian(prep, stage_ops, variant)
+    cfg = SolverConfig(variant=3 if variant is None else variant, krylov_rtol=krylov_rtol,
+                       krylov_maxit=krylov_maxit, restart=restart, precond=precond)
+    if variant_jacobian is not None:
+        vj = variant_jacobian
+        if len(vj.diag) != s:
+            raise ValueError(f"variant_jacobian has {len(vj.diag)} diagonal operators, "
+                             f"expected {s}")
+        present = [f for f in list(vj.diag) + list(vj.offdiag.values()) if f is not None]
+        if not present:
+            raise ValueError("variant_jacobian has no operators")
+        ctx = context_for(present[0].problem)
+        ctx.set_prep(prep)
+        ctx.set_config(cfg)
+        keys = list(vj.offdiag.items())
+        diag = (_lib.OpField * s)(*[_opfield_value(f) for f in vj.diag])
+        off = (_lib.OpField * max(1, len(keys)))(*[_opfield_value(f) for _, f in keys])
+        oi = (C.c_int * max(1, len(keys)))(*[int(k[0]) for k, _ in keys])
+        oj = (C.c_int * max(1, len(keys)))(*[int(k[1]) for k, _ in keys])
+        rc = ctx.lib.irkg_set_variant_jacobian(ctx.h, diag, len(keys), oi, oj, off)
+        if rc:
+            _raise(rc)
+    else:
+        lin = stage_ops
+        ctx = context_for(lin.sys)
+        ctx.set_prep(prep)
+        ctx.set_config(cfg)
+        ctx.prepare_linearization(lin.u, lin.k.reshape(s, -1), lin.dt)
     dk = torch().empty_like(rhs)
     st = ctx.transformed_solve(dt, rhs.contiguous(), dk)
     stats = SolveStats()

@@ -107,7 +107,7 @@ def test_frozen_saves_assemblies_on_burgers_and_matches_oracle(shape):
     prob = GridProblem("burgers", shape, nu=0.02)
     u0 = fourier_u0(prob.shape, 1, 4, 0.5, seed=6)
     tab = pk.make_tableau("radau_iia", 2)
-    dt = 0.1 if len(shape) == 1 else 5e-3
+    dt = 0.02 if len(shape) == 1 else 5e-3  # (at 0.1 the frozen iteration stalls, oracle too)
     kw = dict(newton_rtol=1e-9, krylov_rtol=1e-6, newton_maxit=60, krylov_maxit=4000)
     cfg_e, _ = _cfgs(**kw)
     cfg_f, ocfg_f = _cfgs(jacobian_refresh="frozen", **kw)

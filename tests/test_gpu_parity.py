@@ -350,18 +350,35 @@ def test_block_gmres_maxit_and_zero_rhs():
         pk.block_gmres((2.0, f, 1e-2), np.ones(256), rtol=2.0)
 
 
-def test_transformed_solve_matches_reference_all_variants():
+@pytest.mark.parametrize("route", ["stage_linearization", "stage_ops", "variant_jacobian"])
+def test_transformed_solve_matches_reference_all_variants(route):
+    """solve_transformed_system (src/irk_core.py:225-338) against the
+    reference's own runs on every variant, with the operators passed each way
+    the reference accepts them: stage values (the device forms the fields),
+    a list of s stage operators + variant (the reference's
+    ``[lmat] * s`` call, tests/test_irk_core.py:152-167), or a prebuilt
+    VariantJacobian (``variant_jacobian=``, src/irk_core.py:225-237)."""
     prob = GridProblem("rad", (24,), nu=0.01, c=1.0)
+    lop = pk.OperatorField.linearize(prob, np.zeros((1, 24)))
     for case in load_transformed():
         s = case["s"]
         tab = pk.make_tableau(case["family"], s)
         prep = pk.prepare_stages(tab)
         rng = np.random.default_rng(case["seed"])
         rhs = rng.standard_normal((s, 24))
-        lin = pk.StageLinearization(prob, np.zeros(24), np.zeros((s, 24)), 0.05)
-        k, stats = pk.solve_transformed_system(
-            prep, lin, case["variant"], case["dt"], rhs,
-            precond=pk.PrecondSpec(inner=case["inner"]), krylov_rtol=1e-12, krylov_maxit=400)
+        kw = dict(precond=pk.PrecondSpec(inner=case["inner"]), krylov_rtol=1e-12,
+                  krylov_maxit=400)
+        if route == "stage_linearization":
+            lin = pk.StageLinearization(prob, np.zeros(24), np.zeros((s, 24)), 0.05)
+            k, stats = pk.solve_transformed_system(prep, lin, case["variant"], case["dt"], rhs,
+                                                   **kw)
+        elif route == "stage_ops":
+            k, stats = pk.solve_transformed_system(prep, [lop] * s, case["variant"], case["dt"],
+                                                   rhs, **kw)
+        else:
+            vj = pk.build_variant_jacobian(prep, [lop] * s, case["variant"])
+            k, stats = pk.solve_transformed_system(prep, dt=case["dt"], rhs_stages=rhs,
+                                                   variant_jacobian=vj, **kw)
         got = [[o, r.iterations] for o, r in stats.reports]
         assert [g[0] for g in got] == [w[0] for w in case["reports"]]
         for g, w in zip(got, case["reports"]):

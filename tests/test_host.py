@@ -266,3 +266,71 @@ def test_built_library_matches_sources():
     from paper_2101_01776_b200 import _build
 
     assert _build.is_fresh(), "libirkg.so is stale: run python -m paper_2101_01776_b200._build"
+
+
+def test_reference_side_ctypes_stub_layout_matches_c(tmp_path):
+    """include/irkg_ctypes.py -- the binding INTEGRATION.md tells a
+    maintainer to add to irkit -- declares every struct with the header's
+    exact size and field offsets (the r1 stub lacked length_y/length_z)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "irkg_ctypes", os.path.join(ROOT, "include", "irkg_ctypes.py"))
+    stub = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(stub)
+    checks = [("irkg_problem", stub.Problem, ["length", "length_y", "length_z"]),
+              ("irkg_tableau", stub.Tableau, ["d", "nblocks", "blk_phi"]),
+              ("irkg_solver", stub.Solver, ["inner", "jacobian_refresh", "variant0_stage"]),
+              ("irkg_krylov_report", stub.KrylovReport, ["residuals"]),
+              ("irkg_step_stats", stub.StepStats,
+               ["n_block_records", "wall_time", "fail_report", "constraint_residual"])]
+    lines = []
+    for cname, _, fields in checks:
+        lines.append(f'printf("%zu\\n", sizeof({cname}));')
+        lines += [f'printf("%zu\\n", offsetof({cname}, {f}));' for f in fields]
+    src = tmp_path / "stub.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "irkg.h"\n'
+                   "int main(void){" + "".join(lines) + "return 0;}\n")
+    exe = tmp_path / "stub"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = []
+    for _, cls, fields in checks:
+        want.append(C.sizeof(cls))
+        want += [getattr(cls, f).offset for f in fields]
+    assert got == want
+
+
+def test_integration_md_embeds_the_stub_verbatim():
+    """INTEGRATION.md shows include/irkg_ctypes.py's step_on_gpu as written
+    (the GPU test runs that file), so the document cannot drift again."""
+    with open(os.path.join(ROOT, "INTEGRATION.md")) as fh:
+        doc = fh.read()
+    with open(os.path.join(ROOT, "include", "irkg_ctypes.py")) as fh:
+        src = fh.read()
+    start = src.index("class Problem(C.Structure):")
+    end = src.index("class Tableau(C.Structure):")
+    assert src[start:end].strip() in doc
+    start = src.index("def step_on_gpu(")
+    assert src[start:].strip() in doc
+
+
+def test_variant_weights_index_logic_matches_oracle():
+    """variant_weights (src/nonlinear.py:99-126; bit-exact index logic):
+    argmax |d_ii| first on ties, the variant-3 key set, weights from d."""
+    from oracle import irk
+    from oracle import tableau as otab
+
+    for fam, s in (("gauss", 2), ("gauss", 3), ("radau_iia", 3), ("gauss", 4),
+                   ("lobatto_iiic", 4), ("gauss", 5)):
+        prep = pk.prepare_stages(pk.make_tableau(fam, s))
+        oprep = otab.prepare(fam, s)
+        for v in range(4):
+            dw, ow = pk.variant_weights(prep, v)
+            odw, oow = irk.variant_weights(oprep, v)
+            assert np.array_equal(dw, odw)
+            assert sorted(ow) == sorted(oow)
+            for key in ow:
+                assert np.array_equal(ow[key], oow[key])
