@@ -189,6 +189,11 @@ __global__ void __launch_bounds__(JW * 32)
 // rows ahead without holding registers (the sweep chain is load-latency bound).
 constexpr int JPW = 4;   // warps per CTA
 constexpr int JRING = 8; // rows in flight per warp (cp.async ring in shared memory)
+// the split-operator chain runs one warp per CTA: every loop bound is then
+// block-uniform, so the compiler emits the x-neighbour shuffles as plain
+// SHFL (a 4-warp CTA made the bounds thread-dependent in its eyes, and each
+// shuffle grew a WARPSYNC + divergent-collective fallback path)
+constexpr int JSPW = 1;
 
 namespace {
 
@@ -424,8 +429,8 @@ struct JacCoef {
   double xym, xyp;    // the y-terms regrouped: xym x_m + xyp x_p
 };
 
-template <int KIND, int K>
-__global__ void __launch_bounds__(JPW * 32, 3)
+template <int KIND, int K, bool SLAB>
+__global__ void __launch_bounds__(JSPW * 32, 12 / JSPW)
     k_jacobi_sp2d(Grid g, Op L, JacCoef jc, VecIn vin, int in_off, FRef zcr, double cpl,
                   double *__restrict__ x_out, int span, int strips, int nwarps, GCtrl *flag_ctrl,
                   const GCtrl *skip) {
@@ -435,7 +440,7 @@ __global__ void __launch_bounds__(JPW * 32, 3)
   constexpr bool CONST_D = (KIND == KIND_BURGERS);
   constexpr bool USE_P = (KIND != KIND_RAD);   // O acts on p = a x
   constexpr bool USE_XS = (KIND != KIND_NLDIFF);  // O acts on x (viscous / rad)
-  const int gw = blockIdx.x * JPW + (threadIdx.x >> 5);
+  const int gw = JSPW == 1 ? (int)blockIdx.x : (int)(blockIdx.x * JSPW + (threadIdx.x >> 5));
   if (gw >= nwarps) return;  // whole warp idle
   const int strip = gw % strips, band = gw / strips;
   double scale = 1.0;
@@ -472,28 +477,39 @@ __global__ void __launch_bounds__(JPW * 32, 3)
 
   const int t0 = y0 - H, t1 = y1 + H;  // input rows [t0, t1)
   auto rowp = [&](const FRef &f, int t) -> const double * {
-    if (!g.slab) {
+    if (!SLAB) {
       const int s = t < 0 ? t + ny : (t >= ny ? t - ny : t);
       return f.base + (size_t)s * nx;
     }
     return plane_ptr(f, t, ny, nx, 1);
   };
   extern __shared__ __align__(16) double jring[];
-  double *ring = jring + (size_t)(threadIdx.x >> 5) * JRING * 3 * 64;
+  double *ring = jring + (JSPW == 1 ? 0 : (size_t)(threadIdx.x >> 5) * JRING * 3 * 64);
+  // periodic (single-rank) rows: the element offset of the next row to issue
+  // advances by nx and wraps once at ny, so a refill is three cp.async with
+  // one add -- no per-row wrap branches or 64-bit multiplies in the hot loop
+  const long long nloc = (long long)nx * ny;
+  long long ioff = 0;  // offset (wrapped row * nx + c0) of row t0 + JRING
+  if (!SLAB) {
+    int w = t0 + JRING;
+    w = w < 0 ? w + ny : (w >= ny ? w - ny : w);
+    ioff = (long long)w * nx + c0;
+  }
+  const double *pa = ar.base, *pr = nullptr, *pz = zcr.base;
   auto issue_row = [&](int t, int slot) {
-    if (t < t1) {
-      double *d = ring + slot * 3 * 64 + 2 * lane;
-      if (!g.slab) {  // periodic wrap inside the local field: one offset for all fields
-        const int w = t < 0 ? t + ny : (t >= ny ? t - ny : t);
-        const size_t off = (size_t)w * nx + c0;
-        cp_async16(d, ar.base + off);
-        cp_async16(d + 64, inr.base + off);
-        if (has_zc) cp_async16(d + 128, zcr.base + off);
-      } else {
-        cp_async16(d, rowp(ar, t) + c0);
-        cp_async16(d + 64, rowp(inr, t) + c0);
-        if (has_zc) cp_async16(d + 128, rowp(zcr, t) + c0);
+    double *d = ring + slot * 3 * 64 + 2 * lane;
+    if (!SLAB) {
+      if (t < t1) {
+        cp_async16(d, pa + ioff);
+        cp_async16(d + 64, pr + ioff);
+        if (has_zc) cp_async16(d + 128, pz + ioff);
       }
+      ioff += nx;
+      if (ioff >= nloc) ioff -= nloc;
+    } else if (t < t1) {
+      cp_async16(d, rowp(ar, t) + c0);
+      cp_async16(d + 64, rowp(inr, t) + c0);
+      if (has_zc) cp_async16(d + 128, rowp(zcr, t) + c0);
     }
     cp_async_commit();
   };
@@ -511,6 +527,7 @@ __global__ void __launch_bounds__(JPW * 32, 3)
     return;
   }
   inr = vin_resolve(vin, in_off, scale);
+  pr = inr.base;
 #pragma unroll
   for (int i = 0; i < JRING; ++i) {
     const int t = t0 + i;
@@ -663,6 +680,7 @@ bool Engine::jacobi_chain_fused(const Op &L, double alpha, double dt, int inner,
     const int nb = (grid.ny + span - 1) / span;
     const int nwarps = strips * nb;
     const int blocks = (nwarps + JPW - 1) / JPW;
+    const int sblocks = (nwarps + JSPW - 1) / JSPW;
     const Op Lr = opref(L);
     auto go3 = [&](auto KD, auto KK) {
       constexpr int KIND_ = decltype(KD)::value;
@@ -697,18 +715,25 @@ bool Engine::jacobi_chain_fused(const Op &L, double alpha, double dt, int inner,
       }
       jc.xym = jc.xy - jc.xya;
       jc.xyp = jc.xy + jc.xya;
-      static bool attr = false;  // one per instantiation
-      if (!attr) {
-        check(cudaFuncSetAttribute((const void *)k_jacobi_sp2d<KIND_, decltype(KK)::value>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   JPW * JRING * 3 * 64 * 8),
-              "jacobi ring smem");
-        attr = true;
-      }
-      launch_pdl(k_jacobi_sp2d<KIND_, decltype(KK)::value>, dim3(blocks), dim3(JPW * 32),
-                 (size_t)JPW * JRING * 3 * 64 * sizeof(double), grid, Lr, jc, vin, in_off,
-                 zc ? ref(zc) : FRef{nullptr, nullptr, nullptr}, cpl, x_out, span, strips, nwarps,
-                 ctrl_dev, skip);
+      auto go_s = [&](auto SL) {
+        constexpr bool SLAB_ = decltype(SL)::value;
+        auto kfn = k_jacobi_sp2d<KIND_, decltype(KK)::value, SLAB_>;
+        static bool attr = false;  // one per instantiation
+        if (!attr) {
+          check(cudaFuncSetAttribute((const void *)kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     JSPW * JRING * 3 * 64 * 8),
+                "jacobi ring smem");
+          attr = true;
+        }
+        launch_pdl(kfn, dim3(sblocks), dim3(JSPW * 32),
+                   (size_t)JSPW * JRING * 3 * 64 * sizeof(double), grid, Lr, jc, vin, in_off,
+                   zc ? ref(zc) : FRef{nullptr, nullptr, nullptr}, cpl, x_out, span, strips,
+                   nwarps, ctrl_dev, skip);
+      };
+      if (grid.slab)
+        go_s(std::true_type{});
+      else
+        go_s(std::false_type{});
     };
     auto go2 = [&](auto KD, auto KK) {
       if (jacobi_split) {

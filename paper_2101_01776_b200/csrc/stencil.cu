@@ -318,7 +318,8 @@ __global__ void __launch_bounds__(SBX)
 // through a per-warp ring of BRING rows in shared memory filled by cp.async,
 // BRING-2 rows ahead of the row being computed.  (The one-column slide keeps
 // only one row in flight per thread and is load-latency bound.)
-constexpr int BPW = 2;    // warps per CTA
+constexpr int BPW = 1;    // warps per CTA (one: every loop bound is block-uniform, so the
+                          // x-neighbour shuffles compile without divergent-collective paths)
 constexpr int BRING = 6;  // ring rows per warp (rows s-1..s+1 + BRING-3 ahead)
 constexpr int BWC = 60;   // valid columns per strip (halo 2 keeps pairs aligned)
 
@@ -327,15 +328,15 @@ constexpr int bop_nf() {
   return SIZE == 1 ? 2 : 6;  // ring fields: z1, a1 [, z2, a2, c12, c21]
 }
 
-template <int KIND, int SIZE>
-__global__ void __launch_bounds__(BPW * 32)
+template <int KIND, int SIZE, bool SLAB>
+__global__ void __launch_bounds__(BPW * 32, 16 / BPW)
     k_block_op_strip(Grid g, KindParams kp, double eta, double beta, double phi, double dt,
                      Op l1, Op l2, Op c12, Op c21, FRef z1r, FRef z2r, double *__restrict__ w,
                      const double *__restrict__ b, int span, int strips, int nwarps,
                      double *part, unsigned *counter, double *out_norm, const GCtrl *skip) {
   constexpr int NF = bop_nf<SIZE>();
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * BPW + (threadIdx.x >> 5);
+  const int gw = BPW == 1 ? (int)blockIdx.x : (int)(blockIdx.x * BPW + (threadIdx.x >> 5));
   double nrm = 0.0;
   if (gw >= nwarps) {  // idle warp: nothing to prefetch
     pdl_wait();
@@ -369,17 +370,37 @@ __global__ void __launch_bounds__(BPW * 32)
       have[5] = h21;
     }
     extern __shared__ __align__(16) double bring[];
-    double *ring = bring + (size_t)(threadIdx.x >> 5) * BRING * NF * 64 + li;
+    double *ring = bring + (BPW == 1 ? 0 : (size_t)(threadIdx.x >> 5) * BRING * NF * 64) + li;
     auto rowp = [&](const FRef &f, int t) -> const double * {
-      if (!g.slab) {
+      if (!SLAB) {
         const int s = t < 0 ? t + ny : (t >= ny ? t - ny : t);
         return f.base + (size_t)s * nx;
       }
       return plane_ptr(f, t, ny, nx, 1);
     };
-    auto issue_row = [&](int t) {
-      if (t <= y1) {  // rows y0-1 .. y1 feed the band
-        double *d = ring + ((t - y0 + 1) % BRING) * NF * 64;
+    // periodic (single-rank) refills: the element offset of the next row to
+    // issue (row y0 + BRING - 2 first) advances by nx and wraps once at ny
+    const long long nloc = (long long)nx * ny;
+    long long ioff = 0;
+    if (!SLAB) {
+      int wr = y0 + BRING - 2;
+      wr = wr >= ny ? wr - ny : wr;
+      ioff = (long long)wr * nx + c0;
+    }
+    // the slot of row t is (t - y0 + 1) % BRING; in the unrolled row loop
+    // below it is a compile-time constant
+    auto issue_row_slot = [&](int t, int slot) {
+      if (!SLAB) {
+        if (t <= y1) {  // rows y0-1 .. y1 feed the band
+          double *d = ring + slot * NF * 64;
+#pragma unroll
+          for (int f = 0; f < NF; ++f)
+            if (have[f]) cp_async16(d + f * 64, fr[f].base + ioff);
+        }
+        ioff += nx;
+        if (ioff >= nloc) ioff -= nloc;
+      } else if (t <= y1) {
+        double *d = ring + slot * NF * 64;
 #pragma unroll
         for (int f = 0; f < NF; ++f)
           if (have[f]) cp_async16(d + f * 64, rowp(fr[f], t) + c0);
@@ -389,6 +410,9 @@ __global__ void __launch_bounds__(BPW * 32)
     // pair values of field f at row t (from the ring)
     auto rd = [&](int f, int t) {
       return *reinterpret_cast<const double2 *>(ring + (((t - y0 + 1) % BRING) * NF + f) * 64);
+    };
+    auto rds = [&](int f, int slot) {
+      return *reinterpret_cast<const double2 *>(ring + (slot * NF + f) * 64);
     };
     // neighbourhoods of the two columns from rows (m, c, p) of one field
     auto nb2 = [&](double2 m, double2 c, double2 p, Nb &n0, Nb &n1) {
@@ -444,7 +468,14 @@ __global__ void __launch_bounds__(BPW * 32)
     // in registers: each row's combination is formed once, not three times
     double qtm[2], rtm[2], qbm[2], rbm[2], qtc[2], rtc[2], qbc[2], rbc[2], qtp[2], rtp[2],
         qbp[2], rbp[2];
-    for (int s = y0; s < y1; ++s) {
+    // the row loop is unrolled over the ring (BRING rows per trip), so every
+    // ring slot below is a compile-time constant
+    for (int sb = y0; sb < y1; sb += BRING) {
+#pragma unroll
+    for (int ii = 0; ii < BRING; ++ii) {
+      const int s = sb + ii;
+      if (s >= y1) break;  // block-uniform
+      auto slot_of = [&](int d) { return (ii + 1 + d + BRING) % BRING; };  // slot of row s + d
       cp_async_wait<BRING - 4>();  // rows up to s+1 have landed (s+2 .. s+BRING-3 may pend)
       // The operator is linear in its coefficient fields, so the four
       // stencil applications of a 2x2 block collapse into two per row:
@@ -455,25 +486,25 @@ __global__ void __launch_bounds__(BPW * 32)
       constexpr bool CP = (KIND != KIND_RAD);  // coefficients enter the stencil
       const double s1 = l1.sigma, s2 = SIZE == 2 ? l2.sigma : 0.0;
       const double s12 = h12 ? c12.sigma : 0.0, s21 = h21 ? c21.sigma : 0.0;
-      auto combo = [&](int t, double (&qt)[2], double (&rt)[2], double (&qb)[2],
+      auto combo = [&](int sl, double (&qt)[2], double (&rt)[2], double (&qb)[2],
                        double (&rb)[2]) {
-        const double2 z1 = rd(0, t), A1 = rd(1, t);
+        const double2 z1 = rds(0, sl), A1 = rds(1, sl);
         const double zz1[2] = {z1.x, z1.y}, aa1[2] = {A1.x, A1.y};
         double zz2[2] = {0.0, 0.0}, aa2[2] = {0.0, 0.0}, cc12[2] = {0.0, 0.0},
                cc21[2] = {0.0, 0.0};
         if (SIZE == 2) {
-          const double2 z2 = rd(2, t), A2 = rd(3, t);
+          const double2 z2 = rds(2, sl), A2 = rds(3, sl);
           zz2[0] = z2.x;
           zz2[1] = z2.y;
           aa2[0] = A2.x;
           aa2[1] = A2.y;
           if (h12) {
-            const double2 c = rd(4, t);
+            const double2 c = rds(4, sl);
             cc12[0] = c.x;
             cc12[1] = c.y;
           }
           if (h21) {
-            const double2 c = rd(5, t);
+            const double2 c = rds(5, sl);
             cc21[0] = c.x;
             cc21[1] = c.y;
           }
@@ -492,10 +523,10 @@ __global__ void __launch_bounds__(BPW * 32)
         }
       };
       if (s == y0) {
-        combo(s - 1, qtm, rtm, qbm, rbm);
-        combo(s, qtc, rtc, qbc, rbc);
+        combo(slot_of(-1), qtm, rtm, qbm, rbm);
+        combo(slot_of(0), qtc, rtc, qbc, rbc);
       }
-      combo(s + 1, qtp, rtp, qbp, rbp);
+      combo(slot_of(1), qtp, rtp, qbp, rbp);
       // x-neighbours of a row-s combination (lane-1's second / lane+1's first column)
       auto lap = [&](const double (&m)[2], const double (&c)[2], const double (&p)[2], double out[2]) {
         const double l = __shfl_sync(0xffffffffu, c[1], (lane + 31) & 31);
@@ -532,7 +563,7 @@ __global__ void __launch_bounds__(BPW * 32)
       };
       double top[2], bot[2];
       {
-        const double2 z1 = rd(0, s);
+        const double2 z1 = rds(0, slot_of(0));
         const double zz1[2] = {z1.x, z1.y};
         double lt[2];
         lpart(qtm, qtc, qtp, rtm, rtc, rtp, lt);
@@ -540,7 +571,7 @@ __global__ void __launch_bounds__(BPW * 32)
 #pragma unroll
           for (int c = 0; c < 2; ++c) top[c] = eta * zz1[c] - dt * lt[c];
         } else {
-          const double2 z2 = rd(2, s);
+          const double2 z2 = rds(2, slot_of(0));
           const double zz2[2] = {z2.x, z2.y};
           double lb[2];
           lpart(qbm, qbc, qbp, rbm, rbc, rbp, lb);
@@ -579,7 +610,8 @@ __global__ void __launch_bounds__(BPW * 32)
         qbc[c] = qbp[c];
         rbc[c] = rbp[c];
       }
-      issue_row(s + BRING - 2);  // into the slot of row s-2 (no longer read)
+      issue_row_slot(s + BRING - 2, slot_of(BRING - 2));  // the slot of row s-2 (no longer read)
+    }
     }
     cp_async_wait<0>();
   }
@@ -757,8 +789,9 @@ void Engine::block_op_s(const BlockSpec &B, const double *z, double *w, const do
     const int nwarps = strips * ((grid.ny + span - 1) / span);
     const int blocks = (nwarps + BPW - 1) / BPW;
     const FRef z1 = ref(z);
-    auto launch = [&](auto KD) {
+    auto launch2 = [&](auto KD, auto SL) {
       constexpr int K_ = decltype(KD)::value;
+      constexpr bool S_ = decltype(SL)::value;
       // opt in above the 48 KB default (static + dynamic shared memory)
       static bool attr[2] = {false, false};
       auto opt_in = [&](const void *fn, int size, int bytes) {
@@ -768,19 +801,25 @@ void Engine::block_op_s(const BlockSpec &B, const double *z, double *w, const do
           attr[size - 1] = true;
         }
       };
-      opt_in((const void *)k_block_op_strip<K_, 1>, 1, BPW * BRING * bop_nf<1>() * 64 * 8);
-      opt_in((const void *)k_block_op_strip<K_, 2>, 2, BPW * BRING * bop_nf<2>() * 64 * 8);
+      opt_in((const void *)k_block_op_strip<K_, 1, S_>, 1, BPW * BRING * bop_nf<1>() * 64 * 8);
+      opt_in((const void *)k_block_op_strip<K_, 2, S_>, 2, BPW * BRING * bop_nf<2>() * 64 * 8);
       if (B.size == 1)
-        launch_pdl(k_block_op_strip<K_, 1>, dim3(blocks), dim3(BPW * 32),
+        launch_pdl(k_block_op_strip<K_, 1, S_>, dim3(blocks), dim3(BPW * 32),
                    (size_t)BPW * BRING * bop_nf<1>() * 64 * 8, grid, kp, B.eta, B.beta, B.phi,
                    B.dt, opref(B.l1), opref(B.l2), opref(B.c12), opref(B.c21), z1,
                    FRef{nullptr, nullptr, nullptr}, w, b, span, strips, nwarps, part, counter,
                    out_norm, skip);
       else
-        launch_pdl(k_block_op_strip<K_, 2>, dim3(blocks), dim3(BPW * 32),
+        launch_pdl(k_block_op_strip<K_, 2, S_>, dim3(blocks), dim3(BPW * 32),
                    (size_t)BPW * BRING * bop_nf<2>() * 64 * 8, grid, kp, B.eta, B.beta, B.phi,
                    B.dt, opref(B.l1), opref(B.l2), opref(B.c12), opref(B.c21), z1, ref(z + N), w,
                    b, span, strips, nwarps, part, counter, out_norm, skip);
+    };
+    auto launch = [&](auto KD) {
+      if (grid.slab)
+        launch2(KD, std::true_type{});
+      else
+        launch2(KD, std::false_type{});
     };
     switch (prob.kind) {
       case KIND_NLDIFF: launch(std::integral_constant<int, KIND_NLDIFF>{}); break;

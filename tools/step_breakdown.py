@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--march", action="store_true", help="march the trajectory instead")
     args = ap.parse_args()
     os.environ.setdefault("IRKG_GRAPH_TIMING", "1")
     import torch
@@ -33,9 +34,14 @@ def main():
     ctx = Context(spec.problem, 0)
     ctx.set_prep(pk.prepare_stages(tab))
     ctx.set_config(cfg)
-    u = torch.from_numpy(spec.u0()).cuda()
+    u0 = torch.from_numpy(spec.u0()).cuda()
+    u = u0.clone()
     t = 0.0
+    # default: every step is the bench's step (t = 0, u0); --march walks the trajectory
     for _ in range(args.warmup):
+        if not args.march:
+            u.copy_(u0)
+            t = 0.0
         ctx.step_device(u, t, spec.dt)
         t += spec.dt
     torch.cuda.synchronize()
@@ -45,6 +51,9 @@ def main():
     its = {}
     newton = 0
     for _ in range(args.steps):
+        if not args.march:
+            u.copy_(u0)
+            t = 0.0
         st = ctx.step_device(u, t, spec.dt)
         t += spec.dt
         newton += st.newton_iterations
