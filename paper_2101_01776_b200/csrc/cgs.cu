@@ -224,7 +224,23 @@ struct TileArgs {
   const char *maps;  // tensor maps of this tile height (null: 1-D copies)
   int rev;           // walk the row tiles last-to-first (L2 reuse between sweeps)
   int ef_from;       // basis slots >= ef_from are read evict-first (1-D copies)
+  int st_mode;       // output store flavour (timing experiments): 0 default, 1 .cs, 2 .wt, 3 L2 evict_last
 };
+
+__device__ __forceinline__ void out_store(const TileArgs &A, long long i, double v) {
+  double *p = A.out + i;
+  if (A.st_mode == 1) {
+    __stcs(p, v);
+  } else if (A.st_mode == 2) {
+    __stwt(p, v);
+  } else if (A.st_mode == 3) {
+    asm volatile("{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
+                 " st.global.L2::cache_hint.f64 [%0], %1, pol;\n}\n" ::"l"(p), "d"(v)
+                 : "memory");
+  } else {
+    *p = v;
+  }
+}
 
 // Tile issue, out of line: one copy of the code for every tile height and
 // call site (inlined, the unrolled copy loops made the kernels too large for
@@ -323,7 +339,7 @@ __device__ __forceinline__ void tile_compute(const TileArgs &A, double *buf, int
         double v = wt[r] - sum;
         if (r < rows) {
           if (MODE == CGS_UPD_NORM) nrm += v * v;
-          A.out[r0 + r] = v;
+          out_store(A, r0 + r, v);
         } else {
           v = 0.0;
         }
@@ -404,7 +420,7 @@ __device__ __forceinline__ void tile_compute_ro(const TileArgs &A, const double 
       }
       w = w - (s0 + s1);
       if (r < rows)
-        A.out[r0 + r] = w;
+        out_store(A, r0 + r, w);
       else
         w = 0.0;
       if (MODE == CGS_UPD_NORM) nrm += w * w;
@@ -627,7 +643,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   const int cgs_rev_mask = (trmax >> 16) & 0xff;
   trmax &= 0xffff;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double *out = (MODE == CGS_UPD_NORM) ? V + (size_t)L * pitch : wout;
+  double *out = (MODE == CGS_UPD_NORM && !wout) ? V + (size_t)L * pitch : wout;
   // tile rows: largest power of two with (L+1)*TR <= stage, within [32, 1024]
   int TR = trmax;
   while (TR > 32 && 2 * (L + 1) * TR > ring_doubles) TR >>= 1;
@@ -658,7 +674,8 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   const int m1d = (trmax_raw >> 28) & 7;
   const bool one_d = ((m1d >> MODE) & 1) && TR >= (MODE == CGS_DOT ? 128 : 256);
   TileArgs A{n, L, G, ntiles, V, pitch, win, out, sm, nst, bars, cs, red,
-             (TR <= 256 && !one_d) ? vmaps : nullptr, (cgs_rev_mask >> MODE) & 1, ef_from};
+             (TR <= 256 && !one_d) ? vmaps : nullptr, (cgs_rev_mask >> MODE) & 1, ef_from & 0xffff,
+             MODE == CGS_UPD_NORM ? (ef_from >> 16) : 0};
   double nrm = 0.0;
   double acc[CGS_Q];
 #pragma unroll
@@ -723,9 +740,15 @@ __global__ void __launch_bounds__(CGS_BS, 2)
     }
   }
   if (defer) return;  // the next sweep's CTAs fold these partials themselves
-  __threadfence();
+  // last-CTA ticket, the grid-sync pattern: the CTA barrier orders every
+  // thread's partial store before thread 0's fence + atomic (fence
+  // cumulativity), so one thread fences instead of all 256 -- a membar by
+  // every thread waited out each thread's pending output stores
   __syncthreads();
-  if (tid == 0) is_last = (atomicAdd(counter, 1u) == (unsigned)(G - 1));
+  if (tid == 0) {
+    __threadfence();
+    is_last = (atomicAdd(counter, 1u) == (unsigned)(G - 1));
+  }
   __syncthreads();
   if (!is_last) return;
   __threadfence();
@@ -878,9 +901,16 @@ void Engine::cgs(long long n, int nsweeps) {
     count(2);
     return;
   }
+  // (IRKG_CGS_EXP bit 0, timing experiments only -- wrong results: UPD_NORM
+  // without its last-CTA finish)
+  static const int exp_env = getenv("IRKG_CGS_EXP") ? atoi(getenv("IRKG_CGS_EXP")) : 0;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cap);
+  const int exp_bits = (probing && cap == cudaStreamCaptureStatusNone) ? exp_env : 0;
   launch_pdl_l2(true, k_cgs<CGS_UPD_NORM>, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W,
-             (const double *)W.c2, (const double *)wbuf, dnull, part, G, counter, stage, uc,
-             cond_handle, maps, trm, (const double *)pupd, 0, ef);
+             (const double *)W.c2, (const double *)wbuf, (exp_bits & 2) ? wbuf : dnull, part, G,
+             counter, stage, uc, cond_handle, maps, trm, (const double *)pupd, exp_bits & 1,
+             ef | (((exp_bits >> 2) & 3) << 16));
   count(3);
 }
 

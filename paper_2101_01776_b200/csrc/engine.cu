@@ -120,7 +120,13 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   if (const char *e = getenv("IRKG_GRAPH_UNROLL")) graph_unroll = atoi(e) > 0 ? atoi(e) : 1;
   if (const char *e = getenv("IRKG_JWPS")) jwarps_per_sm = atoi(e) > 0 ? atoi(e) : 12;
   if (const char *e = getenv("IRKG_STRIP_OP")) strip_op = (atoi(e) != 0);
-  if (const char *e = getenv("IRKG_BOP_WPS")) bop_wps = atoi(e) > 0 ? atoi(e) : 12;
+  // auto: on across real ranks (an inter-GPU exchange costs more than the
+  // ~4 us a split adds: two launches + a fork/join); off on a 1-rank ring,
+  // where the self-exchange is a local copy with nothing to hide
+  // (profiles/r2_slab_probe_overlap.txt: 1.41x -> 1.73x of the plain path)
+  halo_overlap = nranks > 1;
+  if (const char *e = getenv("IRKG_HALO_OVERLAP")) halo_overlap = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_BOP_WPS")) bop_wps = atoi(e) > 0 ? atoi(e) : 8;
   for (int i = 0; i < MAXS; ++i)
     for (int j = 0; j < MAXS; ++j) od_slot[i][j] = -1;
 }
@@ -141,6 +147,9 @@ Engine::~Engine() {
     if (e) cudaEventDestroy(e);
   drop_graphs();
   if (cap_stream) cudaStreamDestroy(cap_stream);
+  if (comm_stream) cudaStreamDestroy(comm_stream);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   dae_fini();
   free_ghosts();
   delete comm;
@@ -357,22 +366,81 @@ void Engine::arnoldi_iteration_slab(const BlockSpec &B, long long n, int j_host)
     vslot.lo[h] = g.lo;
     vslot.hi[h] = g.hi;
   }
-  comm->halo_batch(halves, xf, stream);
   counters.halo_exchanges += halves;
-  jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vslot, 0, nullptr, 0.0, zbuf, ctrl_dev);
-  if (B.size == 2) {
-    exchange(R_Z0, zbuf, H);  // z1 feeds the second row's rhs (and the operator below)
-    jacobi_chain(B.l2, B.gamma, B.dt, B.inner, &vslot, (int)N, zbuf, B.beta * B.beta / B.phi,
-                 zbuf + N, ctrl_dev);
-    exchange(R_X1, zbuf + N, 1);
+  const bool ovl = overlap_ok();
+  if (!ovl) {
+    comm->halo_batch(halves, xf, stream);
+    jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vslot, 0, nullptr, 0.0, zbuf, ctrl_dev);
+    if (B.size == 2) {
+      exchange(R_Z0, zbuf, H);  // z1 feeds the second row's rhs (and the operator below)
+      jacobi_chain(B.l2, B.gamma, B.dt, B.inner, &vslot, (int)N, zbuf, B.beta * B.beta / B.phi,
+                   zbuf + N, ctrl_dev);
+      exchange(R_X1, zbuf + N, 1);
+    } else {
+      exchange(R_X0, zbuf, 1);
+    }
+    counters.op_bytes += 8.0 * N * B.size * 3.0;
+    block_op_s(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev);
   } else {
-    exchange(R_X0, zbuf, 1);
+    // every halo goes out on comm_stream while the bands that read no ghost
+    // plane run; the edge bands follow the join (one split per stencil)
+    auto overlapped = [&](auto &&send, auto &&compute) {
+      fork_comm();
+      send();
+      band_sel = 1;
+      compute();
+      join_comm();
+      band_sel = 2;
+      compute();
+      band_sel = 0;
+    };
+    cudaStream_t main = stream;
+    auto on_comm = [&](auto &&f) {  // exchange() / halo_batch enqueue on `stream`
+      stream = comm_stream;
+      f();
+      stream = main;
+    };
+    overlapped([&] { on_comm([&] { comm->halo_batch(halves, xf, stream); }); },
+               [&] { jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vslot, 0, nullptr, 0.0, zbuf,
+                                  ctrl_dev); });
+    if (B.size == 2) {
+      overlapped([&] { on_comm([&] { exchange(R_Z0, zbuf, H); }); },
+                 [&] { jacobi_chain(B.l2, B.gamma, B.dt, B.inner, &vslot, (int)N, zbuf,
+                                    B.beta * B.beta / B.phi, zbuf + N, ctrl_dev); });
+      overlapped([&] { on_comm([&] { exchange(R_X1, zbuf + N, 1); }); },
+                 [&] { block_op_s(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev); });
+    } else {
+      overlapped([&] { on_comm([&] { exchange(R_X0, zbuf, 1); }); },
+                 [&] { block_op_s(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev); });
+    }
+    counters.op_bytes += 8.0 * N * B.size * 3.0;
   }
-  counters.op_bytes += 8.0 * N * B.size * 3.0;
-  block_op_s(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev);
   if (timing) check(cudaEventRecord(ev0, stream));
   cgs_slab(n);
   if (timing) check(cudaEventRecord(ev1, stream));
+}
+
+// The split launches exist for the 2-D fused Jacobi chain and the strip
+// block operator; the comm must enqueue device work only (NCCL) -- the host
+// callback transport synchronises inside halo() anyway.
+bool Engine::overlap_ok() const {
+  return halo_overlap && slab() && comm->capturable() && ndim == 2 && fused_jacobi &&
+         pair_jacobi && jacobi_split && strip_op && grid.nx % 2 == 0 && grid.nx >= 64;
+}
+
+void Engine::fork_comm() {
+  if (!comm_stream) {
+    check(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking), "comm stream");
+    check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
+    check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
+  }
+  check(cudaEventRecord(ev_fork, stream), "fork");
+  check(cudaStreamWaitEvent(comm_stream, ev_fork, 0), "fork wait");
+}
+
+void Engine::join_comm() {
+  check(cudaEventRecord(ev_join, comm_stream), "join");
+  check(cudaStreamWaitEvent(stream, ev_join, 0), "join wait");
 }
 
 // One Arnoldi step: z = M^{-1} v_j, w = A z, CGS2 + column finish.
@@ -1104,7 +1172,14 @@ int irkg_set_solver(irkg_ctx *ctx, const irkg_solver *cfg) { IRKG_GUARD(ctx->eng
 int irkg_set_timing(irkg_ctx *ctx, int on) { IRKG_GUARD(ctx->eng->timing = (on != 0)); }
 int irkg_get_counters(irkg_ctx *ctx, irkg_counters *out) { IRKG_GUARD(*out = ctx->eng->counters); }
 int irkg_probe_phase(irkg_ctx *ctx, int phase, int j, int reps, double *us) {
-  IRKG_GUARD(*us = ctx->eng->probe_phase(phase, j, reps));
+  IRKG_GUARD({
+    struct Flag {
+      bool &f;
+      ~Flag() { f = false; }
+    } guard{ctx->eng->probing};
+    ctx->eng->probing = true;
+    *us = ctx->eng->probe_phase(phase, j, reps);
+  });
 }
 
 int irkg_stage_residual(irkg_ctx *ctx, const double *u_dev, const double *k_dev, double t, double dt,

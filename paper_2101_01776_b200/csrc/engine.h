@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <map>
 #include <set>
 #include <utility>
@@ -277,7 +278,7 @@ struct Engine {
   bool jacobi_split = true;  // split-operator pair kernel (IRKG_JACOBI_SPLIT=0: textbook form)   // column-pair Jacobi kernel (IRKG_PAIR_JACOBI=0: one column per lane)
   int jwarps_per_sm = 12;    // pair kernel: target resident warps per SM (IRKG_JWPS)
   bool strip_op = true;      // 2-D block operator on column-pair strips (IRKG_STRIP_OP=0: slide)
-  int bop_wps = 12;          // strip block operator: target warps per SM (IRKG_BOP_WPS)
+  int bop_wps = 8;           // strip block operator: target warps per SM (IRKG_BOP_WPS)
   bool jacobi_chain_fused(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
                           int in_off, const double *zc, double cpl, double *x_out,
                           const GCtrl *skip);
@@ -323,7 +324,27 @@ struct Engine {
   size_t l2_budget = 51u << 20;
   size_t l2_persist_max = 0, l2_window_max = 0;
   cudaAccessPolicyWindow l2win{};
-  bool l2_holder = false;  // counted in the per-device persisting-limit refcount
+  bool l2_holder = false;
+  bool probing = false;     // inside irkg_probe_phase (timing experiments)
+  // slab halo / interior overlap (IRKG_HALO_OVERLAP): the 2-D fused chain and
+  // strip operator launch only the bands that read no ghost plane
+  // (band_sel 1) while the halo is in flight on comm_stream, then the edge
+  // bands (band_sel 2) after the join
+  int band_sel = 0;
+  bool halo_overlap = true;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // bands [lo, hi) of nb bands of `span` rows (local ny) read only local rows
+  // when the stencil reaches h rows beyond the band
+  void interior_bands(int nb, int span, int h, int &lo, int &hi) const {
+    lo = 0;
+    while (lo < nb && lo * span < h) ++lo;
+    hi = nb;
+    while (hi > lo && std::min(grid.ny, hi * span) + h > grid.ny) --hi;
+  }
+  bool overlap_ok() const;  // the slab step can split its stencils
+  void fork_comm();
+  void join_comm();  // counted in the per-device persisting-limit refcount
   void release_l2_limit();
   void set_l2_window();
   int cgs_ef_from() const;

@@ -432,8 +432,8 @@ struct JacCoef {
 template <int KIND, int K, bool SLAB>
 __global__ void __launch_bounds__(JSPW * 32, 12 / JSPW)
     k_jacobi_sp2d(Grid g, Op L, JacCoef jc, VecIn vin, int in_off, FRef zcr, double cpl,
-                  double *__restrict__ x_out, int span, int strips, int nwarps, GCtrl *flag_ctrl,
-                  const GCtrl *skip) {
+                  double *__restrict__ x_out, int span, int strips, int nwarps, int band0,
+                  GCtrl *flag_ctrl, const GCtrl *skip) {
   constexpr int H = K - 1;
   constexpr int HS = (H + 1) & ~1;
   constexpr int WC = 64 - 2 * HS;
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(JSPW * 32, 12 / JSPW)
   constexpr bool USE_XS = (KIND != KIND_NLDIFF);  // O acts on x (viscous / rad)
   const int gw = JSPW == 1 ? (int)blockIdx.x : (int)(blockIdx.x * JSPW + (threadIdx.x >> 5));
   if (gw >= nwarps) return;  // whole warp idle
-  const int strip = gw % strips, band = gw / strips;
+  const int strip = gw % strips, band = band0 + gw / strips;
   double scale = 1.0;
   FRef inr{};  // v_j (the predecessor's output): resolved after pdl_wait()
   const FRef ar = fref(L);
@@ -680,7 +680,22 @@ bool Engine::jacobi_chain_fused(const Op &L, double alpha, double dt, int inner,
     const int nb = (grid.ny + span - 1) / span;
     const int nwarps = strips * nb;
     const int blocks = (nwarps + JPW - 1) / JPW;
-    const int sblocks = (nwarps + JSPW - 1) / JSPW;
+    // band ranges to launch: all, or (slab halo overlap, band_sel) the
+    // interior bands that read no ghost plane / the edge bands that do
+    int br[2][2] = {{0, nb}, {0, 0}};
+    if (band_sel != 0) {
+      int lo, hi;
+      interior_bands(nb, span, inner - 1, lo, hi);
+      if (band_sel == 1) {
+        br[0][0] = lo;
+        br[0][1] = hi;
+      } else {
+        br[0][0] = 0;
+        br[0][1] = lo;
+        br[1][0] = hi;
+        br[1][1] = nb;
+      }
+    }
     const Op Lr = opref(L);
     auto go3 = [&](auto KD, auto KK) {
       constexpr int KIND_ = decltype(KD)::value;
@@ -725,10 +740,15 @@ bool Engine::jacobi_chain_fused(const Op &L, double alpha, double dt, int inner,
                 "jacobi ring smem");
           attr = true;
         }
-        launch_pdl(kfn, dim3(sblocks), dim3(JSPW * 32),
-                   (size_t)JSPW * JRING * 3 * 64 * sizeof(double), grid, Lr, jc, vin, in_off,
-                   zc ? ref(zc) : FRef{nullptr, nullptr, nullptr}, cpl, x_out, span, strips,
-                   nwarps, ctrl_dev, skip);
+        for (int r = 0; r < 2; ++r) {
+          const int nbr = br[r][1] - br[r][0];
+          if (nbr <= 0) continue;
+          const int nw = strips * nbr;
+          launch_pdl(kfn, dim3((nw + JSPW - 1) / JSPW), dim3(JSPW * 32),
+                     (size_t)JSPW * JRING * 3 * 64 * sizeof(double), grid, Lr, jc, vin, in_off,
+                     zc ? ref(zc) : FRef{nullptr, nullptr, nullptr}, cpl, x_out, span, strips,
+                     nw, br[r][0], ctrl_dev, skip);
+        }
       };
       if (grid.slab)
         go_s(std::true_type{});

@@ -33,9 +33,11 @@ __device__ __forceinline__ double block_sum(double v, double *sm) {
 // true in all threads of the CTA that finished last.
 __device__ __forceinline__ bool last_block(unsigned *counter, int G) {
   __shared__ bool is_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = (atomicAdd(counter, 1u) == (unsigned)(G - 1));
+  __syncthreads();  // every thread's partials ordered before thread 0's fence
+  if (threadIdx.x == 0) {
+    __threadfence();
+    is_last = (atomicAdd(counter, 1u) == (unsigned)(G - 1));
+  }
   __syncthreads();
   if (is_last) __threadfence();
   return is_last;

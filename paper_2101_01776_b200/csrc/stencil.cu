@@ -332,7 +332,7 @@ template <int KIND, int SIZE, bool SLAB>
 __global__ void __launch_bounds__(BPW * 32, 16 / BPW)
     k_block_op_strip(Grid g, KindParams kp, double eta, double beta, double phi, double dt,
                      Op l1, Op l2, Op c12, Op c21, FRef z1r, FRef z2r, double *__restrict__ w,
-                     const double *__restrict__ b, int span, int strips, int nwarps,
+                     const double *__restrict__ b, int span, int strips, int nwarps, int band0,
                      double *part, unsigned *counter, double *out_norm, const GCtrl *skip) {
   constexpr int NF = bop_nf<SIZE>();
   const int lane = threadIdx.x & 31;
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(BPW * 32, 16 / BPW)
   }
   if (gw < nwarps) {
     const int nx = g.nx, ny = g.ny, n = g.n;
-    const int strip = gw % strips, band = gw / strips;
+    const int strip = gw % strips, band = band0 + gw / strips;
     const int x0 = strip * BWC;
     const int li = 2 * lane;
     int c0 = x0 - 2 + li;
@@ -786,8 +786,23 @@ void Engine::block_op_s(const BlockSpec &B, const double *z, double *w, const do
     int span = (int)((grid.ny + bands - 1) / bands);
     span = span < 4 ? 4 : span;
     if (span > grid.ny) span = grid.ny;
-    const int nwarps = strips * ((grid.ny + span - 1) / span);
-    const int blocks = (nwarps + BPW - 1) / BPW;
+    const int nb = (grid.ny + span - 1) / span;
+    int br[2][2] = {{0, nb}, {0, 0}};
+    if (band_sel != 0 && !b) {  // slab halo overlap (never for the residual form)
+      int lo, hi;
+      interior_bands(nb, span, 1, lo, hi);
+      if (band_sel == 1) {
+        br[0][0] = lo;
+        br[0][1] = hi;
+      } else {
+        br[0][0] = 0;
+        br[0][1] = lo;
+        br[1][0] = hi;
+        br[1][1] = nb;
+      }
+    } else if (band_sel == 2) {
+      br[0][1] = 0;  // (band_sel 1 did all of them)
+    }
     const FRef z1 = ref(z);
     auto launch2 = [&](auto KD, auto SL) {
       constexpr int K_ = decltype(KD)::value;
@@ -803,17 +818,23 @@ void Engine::block_op_s(const BlockSpec &B, const double *z, double *w, const do
       };
       opt_in((const void *)k_block_op_strip<K_, 1, S_>, 1, BPW * BRING * bop_nf<1>() * 64 * 8);
       opt_in((const void *)k_block_op_strip<K_, 2, S_>, 2, BPW * BRING * bop_nf<2>() * 64 * 8);
-      if (B.size == 1)
-        launch_pdl(k_block_op_strip<K_, 1, S_>, dim3(blocks), dim3(BPW * 32),
-                   (size_t)BPW * BRING * bop_nf<1>() * 64 * 8, grid, kp, B.eta, B.beta, B.phi,
-                   B.dt, opref(B.l1), opref(B.l2), opref(B.c12), opref(B.c21), z1,
-                   FRef{nullptr, nullptr, nullptr}, w, b, span, strips, nwarps, part, counter,
-                   out_norm, skip);
-      else
-        launch_pdl(k_block_op_strip<K_, 2, S_>, dim3(blocks), dim3(BPW * 32),
-                   (size_t)BPW * BRING * bop_nf<2>() * 64 * 8, grid, kp, B.eta, B.beta, B.phi,
-                   B.dt, opref(B.l1), opref(B.l2), opref(B.c12), opref(B.c21), z1, ref(z + N), w,
-                   b, span, strips, nwarps, part, counter, out_norm, skip);
+      for (int r = 0; r < 2; ++r) {
+        const int nbr = br[r][1] - br[r][0];
+        if (nbr <= 0) continue;
+        const int nwarps = strips * nbr;
+        const int blocks = (nwarps + BPW - 1) / BPW;
+        if (B.size == 1)
+          launch_pdl(k_block_op_strip<K_, 1, S_>, dim3(blocks), dim3(BPW * 32),
+                     (size_t)BPW * BRING * bop_nf<1>() * 64 * 8, grid, kp, B.eta, B.beta, B.phi,
+                     B.dt, opref(B.l1), opref(B.l2), opref(B.c12), opref(B.c21), z1,
+                     FRef{nullptr, nullptr, nullptr}, w, b, span, strips, nwarps, br[r][0], part,
+                     counter, out_norm, skip);
+        else
+          launch_pdl(k_block_op_strip<K_, 2, S_>, dim3(blocks), dim3(BPW * 32),
+                     (size_t)BPW * BRING * bop_nf<2>() * 64 * 8, grid, kp, B.eta, B.beta, B.phi,
+                     B.dt, opref(B.l1), opref(B.l2), opref(B.c12), opref(B.c21), z1, ref(z + N),
+                     w, b, span, strips, nwarps, br[r][0], part, counter, out_norm, skip);
+      }
     };
     auto launch = [&](auto KD) {
       if (grid.slab)

@@ -68,3 +68,15 @@ def test_nccl_transport_single_gpu_ring(tmp_path):
     assert r["rel"] <= 1e-12, r
     assert [s[0] for s in r["stats"]] == [s[0] for s in r["single_stats"]]
     assert r["halos"] > 0
+
+
+def test_nccl_ring_with_halo_overlap_matches(tmp_path):
+    """The interior/edge band split with the halos on a side stream
+    (IRKG_HALO_OVERLAP=1: fork/join inside the captured step graph) gives the
+    same step as the plain periodic run (forced 1-rank NCCL ring)."""
+    r = _run(tmp_path, 1, "--kind", "burgers", "--shape", "128,96", "--transport", "nccl",
+             env={"IRKG_FORCE_SLAB": "1", "IRKG_HALO_OVERLAP": "1"})
+    assert r["rel"] <= 1e-12, r
+    assert [s[0] for s in r["stats"]] == [s[0] for s in r["single_stats"]]
+    assert all(abs(a[1] - b[1]) <= 1 for a, b in zip(r["stats"], r["single_stats"]))
+    assert r["halos"] > 0
