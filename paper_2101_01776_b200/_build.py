@@ -14,6 +14,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libirkg.so")
+#: checked build: the same sources with -DIRKG_CHECKED (device bounds /
+#: invariant checks that trap; the compute-sanitizer stand-in)
+LIB_CHECKED = os.path.join(HERE, "libirkg_checked.so")
 SOURCES = ["kernels.cu", "cgs.cu", "stencil.cu", "jacobi.cu", "dae.cu", "comm.cu", "dirk.cu", "banded.cu", "mg.cu", "engine.cu"]
 HEADERS = ["kinds.cuh", "kernels.cuh", "engine.h", os.path.join("..", "..", "include", "irkg.h")]
 
@@ -50,14 +53,20 @@ def _stale():
     return not is_fresh()
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, checked=False):
+    if checked:
+        return _build_into(LIB_CHECKED, ["-DIRKG_CHECKED"], "_checked", verbose)
     if not force and not _stale():
         return LIB
+    return _build_into(LIB, [], "", verbose, write_hash=True)
+
+
+def _build_into(lib, extra, suffix, verbose, write_hash=False):
     from concurrent.futures import ThreadPoolExecutor
 
     def compile_one(src):
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(CSRC, src.replace(".cu", suffix + ".o"))
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         return src, obj, subprocess.run(cmd, capture_output=True, text=True)
 
     objs = []
@@ -69,19 +78,20 @@ def build(force=False, verbose=False):
             if verbose:
                 sys.stderr.write(res.stderr)
             objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L/usr/local/cuda/lib64", "-lcufft", "-Xlinker", "-rpath=/usr/local/cuda/lib64",
            "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, LIB)
-    with open(HASH_FILE, "w") as fh:
-        fh.write(source_hash())
-    return LIB
+    os.replace(tmp, lib)
+    if write_hash:
+        with open(HASH_FILE, "w") as fh:
+            fh.write(source_hash())
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    checked = "--checked" in sys.argv
+    print(build(force="--force" in sys.argv, verbose=not checked, checked=checked))

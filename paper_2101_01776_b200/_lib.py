@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libirkg.so")
+LIB_PATH = os.environ.get("IRKG_LIB") or os.path.join(HERE, "libirkg.so")
 
 MAX_STAGES = 8
 MAX_NEWTON = 512

@@ -228,6 +228,7 @@ struct TileArgs {
 };
 
 __device__ __forceinline__ void out_store(const TileArgs &A, long long i, double v) {
+  IRKG_DCHECK(i >= 0 && i < A.n);
   double *p = A.out + i;
   if (A.st_mode == 1) {
     __stcs(p, v);
@@ -278,6 +279,7 @@ __device__ __noinline__ void issue_slots(double *dst, const double *V, long long
                                          uint64_t *bar, bool with_w, int ef_from) {
   const uint32_t bytes = TR * 8u;
   const uint64_t pol = evict_first_policy();
+  IRKG_DCHECK(r0 >= 0 && (long long)r0 + TR <= pitch && (TR & 1) == 0);
 #pragma unroll 1
   for (int l = warp; l <= L - (with_w ? 0 : 1); l += CGS_NW) {
     const double *src = (l < L) ? V + (size_t)l * pitch + r0 : win + r0;
@@ -449,6 +451,7 @@ __device__ __forceinline__ bool tile_full(const TileArgs &A, int t) {
 template <int TRC>
 __device__ __forceinline__ void tile_issue(const TileArgs &A, int t, int s, bool with_w = true) {
   const int tid = threadIdx.x;
+  IRKG_DCHECK(s >= 0 && s < A.nst && t >= 0 && (long long)(t + 1) * TRC <= A.n);
   double *dst = A.ring + (size_t)s * (A.L + 1) * TRC;
   if (A.maps) {
     if (tid == 0) issue_boxed(dst, A.maps, A.win, t * TRC, TRC, A.L, &A.bars[s], with_w);
@@ -472,6 +475,7 @@ __device__ __forceinline__ void tile_issue_w(const TileArgs &A, int t, int s) {
 // partial tail tile (only the globally last one): generic loads, zero-padded
 template <int TRC>
 __device__ __forceinline__ void tile_load_tail(const TileArgs &A, double *buf, int r0, int rows) {
+  IRKG_DCHECK(rows > 0 && rows < TRC && (long long)r0 + rows == A.n);
   for (int l = 0; l <= A.L; ++l) {
     const double *src = (l < A.L) ? A.V + (size_t)l * A.pitch + r0 : A.win + r0;
     for (int r = threadIdx.x; r < TRC; r += CGS_BS) buf[l * TRC + r] = (r < rows) ? src[r] : 0.0;
@@ -651,6 +655,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
   // otherwise leave most of the shared memory idle)
   int nst = ring_doubles / ((L + 1) * TR);
   nst = nst > CGS_MAXST ? CGS_MAXST : nst;
+  IRKG_DCHECK(L >= 1 && L <= MAXR + 1 && nst >= 1 && nst * (L + 1) * TR <= ring_doubles);
   const int ntiles = (n + TR - 1) / TR;
   const int nd = (MODE == CGS_DOT) ? L + 1 : L;  // dot entries (DOT: + ||w||^2)
   if (TR <= 256 && vmaps) vmaps += (size_t)(__ffs(TR) - 6) * VM_B * sizeof(CUtensorMap);

@@ -500,6 +500,8 @@ __global__ void __launch_bounds__(JSPW * 32, 12 / JSPW)
     double *d = ring + slot * 3 * 64 + 2 * lane;
     if (!SLAB) {
       if (t < t1) {
+        IRKG_DCHECK(ioff >= 0 && ioff + 2 <= nloc && (ioff & 1) == 0);
+        IRKG_DCHECK(slot >= 0 && slot < JRING);
         cp_async16(d, pa + ioff);
         cp_async16(d + 64, pr + ioff);
         if (has_zc) cp_async16(d + 128, pz + ioff);

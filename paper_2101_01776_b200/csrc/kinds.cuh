@@ -21,6 +21,26 @@
 #pragma once
 #include <cuda_runtime.h>
 
+// Checked build (python -m paper_2101_01776_b200._build --checked, -DIRKG_CHECKED):
+// device-side bounds/invariant checks that trap with the failing line -- the
+// stand-in for compute-sanitizer, which this GPU pool does not allow.  They
+// compile to nothing in the production library.
+#ifdef IRKG_CHECKED
+#include <cstdio>
+#define IRKG_DCHECK(cond)                                                               \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      printf("IRKG_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__,   \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                              \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define IRKG_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
 namespace irkg {
 
 enum { KIND_NLDIFF = 0, KIND_BURGERS = 1, KIND_RAD = 2, KIND_ARAKAWA = 3 };
@@ -51,10 +71,18 @@ struct FRef {
 __device__ __forceinline__ const double *plane_ptr(const FRef &f, int s, int nl, int P, int slab) {
   if (!slab) {
     s = s < 0 ? s + nl : (s >= nl ? s - nl : s);
+    IRKG_DCHECK(s >= 0 && s < nl);
     return f.base + (size_t)s * P;
   }
-  if (s < 0) return f.lo + (size_t)(s + GH) * P;
-  if (s >= nl) return f.hi + (size_t)(s - nl) * P;
+  IRKG_DCHECK(s >= -GH && s < nl + GH);
+  if (s < 0) {
+    IRKG_DCHECK(f.lo != nullptr);
+    return f.lo + (size_t)(s + GH) * P;
+  }
+  if (s >= nl) {
+    IRKG_DCHECK(f.hi != nullptr);
+    return f.hi + (size_t)(s - nl) * P;
+  }
   return f.base + (size_t)s * P;
 }
 

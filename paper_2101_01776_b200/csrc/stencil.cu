@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(BPW * 32, 16 / BPW)
     auto issue_row_slot = [&](int t, int slot) {
       if (!SLAB) {
         if (t <= y1) {  // rows y0-1 .. y1 feed the band
+          IRKG_DCHECK(ioff >= 0 && ioff + 2 <= nloc && slot >= 0 && slot < BRING);
           double *d = ring + slot * NF * 64;
 #pragma unroll
           for (int f = 0; f < NF; ++f)
