@@ -291,6 +291,28 @@ int irkg_operator_apply(irkg_ctx *ctx, const irkg_opfield *l, const double *x_de
 /* OdeSystem.rhs (src/nonlinear.py:35-48): f = N(u, t) (autonomous kinds; one rank). */
 int irkg_rhs(irkg_ctx *ctx, const double *u_dev, double t, double *f_dev);
 
+/* Reverse-communication GMRES over a caller-supplied operator and right
+ * preconditioner: the reference's gmres(op, rhs, right_precond, rtol, maxit,
+ * restart, x0) (src/sparsela.py:176-280) with its LinearOperator plugin
+ * (src/sparsela.py:131-152).  The engine runs the restarted Arnoldi process
+ * (fused CGS2 sweeps, Givens, back-substitution, x += Z y with Z stored,
+ * true-residual recheck) and returns to the caller for every operator
+ * application: after irkg_rc_gmres_next() reports IRKG_RC_APPLY_PRECOND or
+ * IRKG_RC_APPLY_OP, the caller writes M^{-1} vin (resp. A vin) into vout and
+ * calls next() again; IRKG_RC_DONE ends the solve (x_dev holds x; the
+ * report comes from irkg_rc_gmres_report).  All vectors are n doubles on the
+ * device (n <= 2 * the context's N); x0_dev may be NULL (x0 = 0);
+ * solves_per_apply = 0 means no preconditioner.  Breakdown with a residual
+ * above rtol returns IRKG_ERR_BREAKDOWN from next(). */
+#define IRKG_RC_DONE 0
+#define IRKG_RC_APPLY_PRECOND 1
+#define IRKG_RC_APPLY_OP 2
+int irkg_rc_gmres_begin(irkg_ctx *ctx, long long n, const double *rhs_dev, const double *x0_dev,
+                        double *x_dev, double *vin_dev, double *vout_dev, double rtol, int maxit,
+                        int restart, int solves_per_apply);
+int irkg_rc_gmres_next(irkg_ctx *ctx, int *action);
+int irkg_rc_gmres_report(irkg_ctx *ctx, irkg_krylov_report *report);
+
 /* ---- index-1 DAE (vorticity/streamfunction, IRKG_KIND_ARAKAWA) ----
  * State uw = [u; w] (2N: vorticity then streamfunction), stage arrays
  * (s, 2N) with rows [k_i; l_i] -- the reference's composite layout

@@ -31,6 +31,7 @@ from .problems import (
 from .solver import (
     Block2x2System,
     DaeIntegrationResult,
+    LinearOperator,
     OperatorField,
     ShiftedSolver,
     StageLinearization,
@@ -42,6 +43,7 @@ from .solver import (
     combine,
     dae_integrate,
     dae_step,
+    gmres,
     integrate,
     newton_like_step,
     precond_block2x2,
@@ -79,6 +81,7 @@ __all__ = [
     "IrkitError",
     "KrylovBreakdownError",
     "KrylovReport",
+    "LinearOperator",
     "OperatorField",
     "PrecondSpec",
     "RunSpec",
@@ -101,6 +104,7 @@ __all__ = [
     "block_gmres",
     "fourier_u0",
     "gamma_star",
+    "gmres",
     "integrate",
     "make_tableau",
     "newton_like_step",

@@ -190,6 +190,9 @@ _SIGS = {
                                        C.POINTER(C.c_int), C.POINTER(OpField)]),
     "irkg_operator_apply": (_I, [_P, C.POINTER(OpField), _P, _P]),
     "irkg_rhs": (_I, [_P, _P, _D, _P]),
+    "irkg_rc_gmres_begin": (_I, [_P, C.c_longlong, _P, _P, _P, _P, _P, _D, _I, _I, _I]),
+    "irkg_rc_gmres_next": (_I, [_P, C.POINTER(C.c_int)]),
+    "irkg_rc_gmres_report": (_I, [_P, C.POINTER(KrylovReportC)]),
     "irkg_dae_stage_residual": (_I, [_P, _P, _P, _D, _D, _P, C.POINTER(_D)]),
     "irkg_dae_step": (_I, [_P, _P, _D, _D, C.POINTER(StepStatsC)]),
     "irkg_dae_step_host": (_I, [_P, _P, _D, _D, C.POINTER(StepStatsC)]),

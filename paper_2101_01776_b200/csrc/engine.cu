@@ -135,7 +135,7 @@ Engine::~Engine() {
   cudaStreamSynchronize(stream);
   void *bufs[] = {part, counter, scal_dev, ctrl_dev, W.H, W.cs, W.sn, W.g, W.alpha, W.y,
                   W.c1, W.c2, W.res, V, wbuf, zbuf, ubuf, tmp_x, tmp_t, U, F, Gs, Y, DK,
-                  Kst, RHS, ufield, opA, vmaps, zero_n};
+                  Kst, RHS, ufield, opA, vmaps, zero_n, rc.Z};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (ctrl_host) cudaFreeHost(ctrl_host);
@@ -1436,6 +1436,28 @@ int irkg_operator_apply(irkg_ctx *ctx, const irkg_opfield *l, const double *x_de
     e.block_op(B, x_dev, y_dev, nullptr, nullptr, nullptr);
     check(cudaStreamSynchronize(e.stream));
   });
+}
+
+int irkg_rc_gmres_begin(irkg_ctx *ctx, long long n, const double *rhs_dev, const double *x0_dev,
+                        double *x_dev, double *vin_dev, double *vout_dev, double rtol, int maxit,
+                        int restart, int solves_per_apply) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    e.rc_begin(n, rhs_dev, x0_dev, x_dev, vin_dev, vout_dev, rtol, maxit, restart,
+               solves_per_apply);
+  });
+}
+
+int irkg_rc_gmres_next(irkg_ctx *ctx, int *action) {
+  IRKG_GUARD({
+    Engine &e = *ctx->eng;
+    *action = e.rc_next();
+    if (*action != IRKG_RC_DONE) check(cudaStreamSynchronize(e.stream), "rc sync");
+  });
+}
+
+int irkg_rc_gmres_report(irkg_ctx *ctx, irkg_krylov_report *report) {
+  IRKG_GUARD(ctx->eng->rc_report(report));
 }
 
 int irkg_rhs(irkg_ctx *ctx, const double *u_dev, double t, double *f_dev) {

@@ -330,6 +330,25 @@ struct Engine {
   // strip operator launch only the bands that read no ghost plane
   // (band_sel 1) while the halo is in flight on comm_stream, then the edge
   // bands (band_sel 2) after the join
+  // reverse-communication GMRES (rcgmres.cu; irkg_rc_gmres_*)
+  enum RcPhase { RC_R0, RC_R0_DONE, RC_CYCLE, RC_PREC, RC_PREC_DONE, RC_OP, RC_OP_DONE,
+                 RC_CYCLE_END, RC_RESID, RC_DONE };
+  struct RcState {
+    bool active = false;
+    long long n = 0, zn = 0;
+    int zcap = 0;
+    double *Z = nullptr;  // stored preconditioned basis (restart x n)
+    const double *b = nullptr;
+    double *x = nullptr, *vin = nullptr, *vout = nullptr;
+    double rtol = 0.0;
+    int maxit = 0, restart = 0, spa = 0, j = 0, its = 0;
+    RcPhase phase = RC_DONE;
+  } rc;
+  void rc_copy(double *dst, const double *src, long long n);
+  void rc_begin(long long n, const double *b, const double *x0, double *x, double *vin,
+                double *vout, double rtol, int maxit, int restart, int spa);
+  int rc_next();
+  void rc_report(irkg_krylov_report *rep);
   int band_sel = 0;
   bool halo_overlap = true;
   cudaStream_t comm_stream = nullptr;

@@ -472,6 +472,102 @@ def block_gmres(sys2, rhs, spec=PrecondSpec(inner=4), rtol=1e-5, maxit=200, rest
     return _out(x, rhs), report
 
 
+class LinearOperator:
+    """Abstract linear action ``y = A x`` of dimension ``n`` on the device
+    (src/sparsela.py:131-152): ``apply`` maps a CUDA float64 tensor (n,) to
+    one; ``solves_per_apply`` is the preconditioner-work unit the Krylov
+    report counts (src/sparsela.py:192, 278)."""
+
+    def __init__(self, n, apply, solves_per_apply=1):
+        self.n = int(n)
+        self._apply = apply
+        self.solves_per_apply = solves_per_apply
+
+    def __call__(self, x):
+        return self._apply(x)
+
+    def matvec(self, x):
+        return self._apply(x)
+
+
+def _as_device_apply(op):
+    """src/sparsela.py:165-173 for device operands: a LinearOperator, an
+    OperatorField, or a dense square matrix (numpy or CUDA tensor)."""
+    if isinstance(op, LinearOperator):
+        return op.n, op.matvec
+    if isinstance(op, OperatorField):
+        return op.n, op.matvec
+    t = torch()
+    if isinstance(op, t.Tensor) or isinstance(op, np.ndarray):
+        a = as_device(op)
+        if a.dim() == 2 and a.shape[0] == a.shape[1]:
+            return int(a.shape[0]), (lambda x: a @ x)
+    raise TypeError(f"cannot interpret {type(op)!r} as a linear operator")
+
+
+_RC_HOSTS = {}
+
+
+def gmres(op, rhs, right_precond=None, rtol=1e-5, maxit=200, restart=200, x0=None):
+    """Restarted right-preconditioned GMRES over a caller's operator
+    (src/sparsela.py:176-280): the engine runs the Arnoldi process (fused
+    CGS2 sweeps, Givens, back-substitution, the true-residual recheck, Z
+    stored) and calls back ``op`` / ``right_precond`` on CUDA tensors
+    through the reverse-communication C entries (irkg_rc_gmres_*).
+    Returns ``(x, KrylovReport)``; breakdown above rtol raises
+    KrylovBreakdownError."""
+    n, apply_op = _as_device_apply(op)
+    t = torch()
+    b = as_device(rhs).reshape(-1)
+    if tuple(b.shape) != (n,):
+        raise ValueError(f"rhs has shape {tuple(b.shape)}, expected ({n},)")
+    if not (0.0 < rtol < 1.0):
+        raise ValueError(f"rtol must lie in (0, 1), got {rtol}")
+    spa = 0
+    apply_m = None
+    if right_precond is not None:
+        spa = int(getattr(right_precond, "solves_per_apply", 1))
+        apply_m = right_precond.matvec if hasattr(right_precond, "matvec") else right_precond
+    b = b.contiguous()
+    if float(t.linalg.vector_norm(b)) == 0.0:  # src/sparsela.py:196-198
+        return _out(t.zeros_like(b), rhs), KrylovReport(0, True, [0.0], 0)
+    key = (n, t.cuda.current_device())
+    host = _RC_HOSTS.get(key)
+    if host is None:
+        from .problems import GridProblem
+
+        host = _RC_HOSTS[key] = GridProblem("rad", (n,), name=f"krylov{n}")
+    ctx = context_for(host)
+    x = t.empty_like(b)
+    vin, vout = t.empty_like(b), t.empty_like(b)
+    xd = None if x0 is None else as_device(x0).reshape(-1).contiguous()
+    rc = ctx.lib.irkg_rc_gmres_begin(ctx.h, n, ptr(b), ptr(xd) if xd is not None else None,
+                                     ptr(x), ptr(vin), ptr(vout), float(rtol), int(maxit),
+                                     int(restart), spa)
+    if rc:
+        _raise(rc)
+    act = C.c_int()
+    while True:
+        rc = ctx.lib.irkg_rc_gmres_next(ctx.h, C.byref(act))
+        if rc:
+            _raise(rc)
+        if act.value == 0:
+            break
+        y = apply_m(vin) if act.value == 1 else apply_op(vin)
+        vout.copy_(as_device(y).reshape(-1))
+    res = (C.c_double * (int(maxit) + 4))()
+    rep = _lib.KrylovReportC()
+    rep.residuals = C.cast(res, C.POINTER(C.c_double))
+    rep.residual_capacity = len(res)
+    rc = ctx.lib.irkg_rc_gmres_report(ctx.h, C.byref(rep))
+    if rc:
+        _raise(rc)
+    report = KrylovReport(int(rep.iterations), bool(rep.converged),
+                          list(res[: min(rep.n_residuals, len(res))]),
+                          int(rep.precond_applications))
+    return _out(x, rhs), report
+
+
 class StageLinearization:
     """The s stage linearisations of ``sys`` at ``u + dt A0 K`` -- the device
     analogue of the ``stage_ops`` list of CSR matrices the reference passes
