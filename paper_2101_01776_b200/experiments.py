@@ -14,50 +14,77 @@ manifest JSON -- the reference's provenance rules.
 from __future__ import annotations
 
 import csv
-import dataclasses
 import hashlib
 import json
-from dataclasses import dataclass, field
 from pathlib import Path
 
 import numpy as np
 
 from .config import PrecondSpec, SolverConfig
-from .errors import IrkitError
+from .errors import ConfigurationError, IrkitError
 from .problems import GridProblem, baseline_config, fourier_u0
 from .solver import integrate
 from .stats import write_step_stats_csv  # noqa: F401  (src/nonlinear.py:377-417)
 from .tableau import make_tableau, prepare_stages
 
 
-@dataclass(frozen=True)
+#: The reference manifest's keys and defaults (src/experiments.py:42-59).  A
+#: manifest that uses only these serialises to the same canonical JSON -- and
+#: so the same provenance hash -- as irkit's RunManifest, so one JSON file
+#: drives both harnesses (tests/test_experiments.py runs irkit's and this
+#: engine's run_iterations on one manifest).  This engine's own knobs live in
+#: the optional ``device`` mapping (inner-solve policy ``inner``, default the
+#: reference's "exact"; ``krylov_maxit``, default 200), left out of the JSON
+#: when empty.
+_REFERENCE_KEYS = {
+    "experiment": None, "problem": None, "problem_params": {}, "schemes": (), "dts": (),
+    "t_final": 0.1, "variant": 3, "gamma": "star", "newton_rtol": 1e-9, "krylov_rtol": 1e-5,
+    "out": None, "seed": 0,
+}
+
+
 class RunManifest:
-    """Serializable description of one study (fields of src/experiments.py:42-59,
-    plus the inner-solve policy and the seeded-field parameters)."""
+    """Serializable description of one study: the reference's manifest plus
+    an optional ``device`` mapping (see _REFERENCE_KEYS)."""
 
-    experiment: str
-    problem: str  # "baseline:<k>" or a GridProblem kind ("nldiff", "burgers", "rad")
-    problem_params: dict = field(default_factory=dict)
-    schemes: tuple = ()  # of (family, stages)
-    dts: tuple = ()
-    t_final: float = 0.1
-    variant: int = 3
-    gamma: object = "star"
-    newton_rtol: float = 1e-9
-    krylov_rtol: float = 1e-5
-    inner: object = 4
-    krylov_maxit: int = 5000
-    out: str | None = None
-    seed: int = 0
+    def __init__(self, experiment, problem, **kw):
+        unknown = set(kw) - set(_REFERENCE_KEYS) - {"device"}
+        if unknown:
+            raise TypeError(f"unknown manifest keys {sorted(unknown)}")
+        vals = dict(_REFERENCE_KEYS, experiment=experiment, problem=problem)
+        vals.update({k: v for k, v in kw.items() if k != "device"})
+        vals["problem_params"] = dict(vals["problem_params"] or {})
+        vals["schemes"] = tuple((str(f), int(st)) for f, st in vals["schemes"])
+        vals["dts"] = tuple(float(x) for x in vals["dts"])
+        vals["device"] = dict(kw.get("device") or {})
+        object.__setattr__(self, "_v", vals)
 
-    def __post_init__(self):
-        object.__setattr__(self, "schemes", tuple((str(f), int(s)) for f, s in self.schemes))
-        object.__setattr__(self, "dts", tuple(float(x) for x in self.dts))
+    def __getattr__(self, name):
+        try:
+            return self.__dict__["_v"][name]
+        except KeyError:
+            raise AttributeError(name) from None
 
+    def __setattr__(self, name, value):
+        raise AttributeError("RunManifest is immutable")
+
+    def __eq__(self, other):
+        return isinstance(other, RunManifest) and self._v == other._v
+
+    def __hash__(self):
+        return hash(self.to_json())
+
+    def __repr__(self):
+        return f"RunManifest({self.to_json()})"
+
+    # -- serialisation (canonical: sorted keys; tuples as lists)
     def to_dict(self):
-        doc = dataclasses.asdict(self)
-        doc["schemes"] = [list(x) for x in self.schemes]
-        doc["dts"] = list(self.dts)
+        doc = {k: self._v[k] for k in _REFERENCE_KEYS}
+        doc["problem_params"] = dict(doc["problem_params"])
+        doc["schemes"] = [[f, st] for f, st in doc["schemes"]]
+        doc["dts"] = list(doc["dts"])
+        if self._v["device"]:
+            doc["device"] = dict(self._v["device"])
         return doc
 
     def to_json(self):
@@ -66,10 +93,7 @@ class RunManifest:
     @classmethod
     def from_dict(cls, doc):
         doc = dict(doc)
-        doc["schemes"] = tuple((f, int(s)) for f, s in doc.get("schemes", ()))
-        doc["dts"] = tuple(doc.get("dts", ()))
-        doc["problem_params"] = dict(doc.get("problem_params", {}))
-        return cls(**doc)
+        return cls(doc.pop("experiment"), doc.pop("problem"), **doc)
 
     @classmethod
     def from_json(cls, text):
@@ -79,6 +103,14 @@ class RunManifest:
     def hash(self):
         return hashlib.sha256(self.to_json().encode()).hexdigest()[:12]
 
+    @property
+    def inner(self):
+        return self._v["device"].get("inner", "exact")
+
+    @property
+    def krylov_maxit(self):
+        return int(self._v["device"].get("krylov_maxit", 200))
+
     def solver_config(self, **overrides):
         kw = dict(variant=self.variant, newton_rtol=self.newton_rtol,
                   krylov_rtol=self.krylov_rtol, krylov_maxit=self.krylov_maxit, restart=200,
@@ -87,38 +119,80 @@ class RunManifest:
         return SolverConfig(**kw)
 
     def problem_and_u0(self):
-        """(GridProblem, u0): a BASELINE config ("baseline:1", params: n) or a
-        kind with ``shape`` / ``nu`` / ``c`` / ``lam`` / ``mu`` and the seeded
-        Fourier field ``k_hi`` / ``sigma``."""
-        p = dict(self.problem_params)
-        if self.problem.startswith("baseline:"):
-            spec = baseline_config(int(self.problem.split(":")[1]), n=p.get("n"))
-            return spec.problem, spec.u0()
-        shape = tuple(p.pop("shape", (64, 64)))
-        k_hi, sigma = p.pop("k_hi", 4), p.pop("sigma", 0.1)
-        prob = GridProblem(self.problem, shape, **p)
-        return prob, fourier_u0(shape, 1, k_hi, sigma, self.seed)
+        """(GridProblem, u0) for the manifest's problem: a name of the
+        reference's 1-D periodic catalog (``burgers1d``, ``advdiff1d``,
+        ``advection1d``; src/problems.py:137-200, the same discretisation and
+        initial state), a BASELINE config (``baseline:<k>``, params: ``n``),
+        or a GridProblem kind with ``shape`` / ``nu`` / ``c`` / ``lam`` /
+        ``mu`` and the seeded Fourier field ``k_hi`` / ``sigma``."""
+        return catalog_problem(self.problem, self.problem_params, self.seed)
+
+
+def catalog_problem(name, params, seed=0):
+    p = dict(params)
+    if name in _REFERENCE_CATALOG:
+        return _REFERENCE_CATALOG[name](**p)
+    if name.startswith("baseline:"):
+        spec = baseline_config(int(name.split(":")[1]), n=p.get("n"))
+        return spec.problem, spec.u0()
+    if name not in ("nldiff", "burgers", "rad"):
+        raise ConfigurationError(f"problem {name!r} has no device discretisation")
+    shape = tuple(p.pop("shape", (64, 64)))
+    k_hi, sigma = p.pop("k_hi", 4), p.pop("sigma", 0.1)
+    prob = GridProblem(name, shape, **p)
+    return prob, fourier_u0(shape, 1, k_hi, sigma, seed)
+
+
+def _grid_1d(n):
+    return np.arange(n) / n  # x_i = i h on the periodic unit interval (h = 1/n)
+
+
+def _burgers1d(n=128, nu=0.02, base=0.5, amplitude=0.45):
+    # src/problems.py:175-200: N(u) = -D(u^2/2) + nu Lap u, periodic, h = 1/n
+    return (GridProblem("burgers", (int(n),), nu=nu),
+            base + amplitude * np.sin(2 * np.pi * _grid_1d(int(n))))
+
+
+def _advdiff1d(n=64, speed=1.0, nu=0.01):
+    # src/problems.py:158-172: u_t = speed D u + nu Lap u
+    x = _grid_1d(int(n))
+    return (GridProblem("rad", (int(n),), nu=nu, c=speed),
+            np.sin(2 * np.pi * x) + 0.2 * np.sin(6 * np.pi * x))
+
+
+def _advection1d(n=64, speed=1.0):
+    # src/problems.py:137-155: u_t = speed D u
+    x = _grid_1d(int(n))
+    return (GridProblem("rad", (int(n),), c=speed),
+            np.sin(2 * np.pi * x) + 0.3 * np.cos(4 * np.pi * x))
+
+
+_REFERENCE_CATALOG = {"burgers1d": _burgers1d, "advdiff1d": _advdiff1d,
+                      "advection1d": _advection1d}
 
 
 def _fmt(x):
-    return repr(float(x))
+    return repr(float(x))  # the reference's CSV number format (round-trips exactly)
 
 
 def _write_rows(manifest, rows, fieldnames):
+    """CSV of the study next to its manifest JSON (``<out>.manifest.json``)."""
     if manifest.out is None:
         return
-    out = Path(manifest.out)
-    out.parent.mkdir(parents=True, exist_ok=True)
-    with out.open("w", newline="") as fh:
-        w = csv.DictWriter(fh, fieldnames=fieldnames)
-        w.writeheader()
-        for row in rows:
-            w.writerow(row)
-    out.with_suffix(out.suffix + ".manifest.json").write_text(manifest.to_json() + "\n")
+    path = Path(manifest.out)
+    path.parent.mkdir(parents=True, exist_ok=True)
+    with path.open("w", newline="") as fh:
+        out = csv.DictWriter(fh, fieldnames=fieldnames)
+        out.writeheader()
+        out.writerows(rows)
+    Path(str(path) + ".manifest.json").write_text(manifest.to_json() + "\n")
 
 
-def run_iterations(manifest: RunManifest):
-    """Solver-work counts per (scheme, dt) over the time span (src/experiments.py:250-293)."""
+def run_iterations(manifest: RunManifest, timing=False):
+    """Solver-work counts per (scheme, dt) over the time span
+    (src/experiments.py:250-293): the reference's columns, so the CSV of a
+    reference-catalog manifest compares row by row with irkit's;
+    ``timing=True`` adds the device wall time per cell."""
     prob, u0 = manifest.problem_and_u0()
     cfg = manifest.solver_config()
     rows = []
@@ -127,20 +201,23 @@ def run_iterations(manifest: RunManifest):
         for dt in manifest.dts:
             row = {"scheme": tab.label, "order": tab.order, "dt": dt, "steps": "",
                    "newton_iterations": "", "krylov_iterations": "", "precond_applications": "",
-                   "wall_time": "", "status": "ok", "manifest_hash": manifest.hash}
+                   "status": "ok", "manifest_hash": manifest.hash}
+            if timing:
+                row["wall_time"] = ""
             try:
                 res = integrate(prob, u0, 0.0, manifest.t_final, dt, tab, cfg)
                 row.update(steps=len(res.step_stats),
                            newton_iterations=res.total("newton_iterations"),
                            krylov_iterations=res.total("krylov_iterations"),
-                           precond_applications=res.total("precond_applications"),
-                           wall_time=_fmt(res.total("wall_time")))
+                           precond_applications=res.total("precond_applications"))
+                if timing:
+                    row["wall_time"] = _fmt(res.total("wall_time"))
             except IrkitError as exc:
                 row["status"] = f"failed: {type(exc).__name__}"
             rows.append(row)
-    _write_rows(manifest, rows, ["scheme", "order", "dt", "steps", "newton_iterations",
-                                 "krylov_iterations", "precond_applications", "wall_time",
-                                 "status", "manifest_hash"])
+    cols = ["scheme", "order", "dt", "steps", "newton_iterations", "krylov_iterations",
+            "precond_applications", "status", "manifest_hash"]
+    _write_rows(manifest, rows, cols + (["wall_time"] if timing else []))
     return rows
 
 
@@ -165,8 +242,6 @@ def run_gamma_compare(manifest: RunManifest):
         tab = make_tableau(fam, s)
         prep = prepare_stages(tab)
         if all(b.size == 1 for b in prep.blocks):
-            from .errors import ConfigurationError
-
             raise ConfigurationError(f"{tab.label} has no complex eigen-block")
         for dt in manifest.dts:
             means, status = {}, "ok"
@@ -231,7 +306,5 @@ STUDIES = {"iterations": run_iterations, "gamma-compare": run_gamma_compare,
 def run(manifest: RunManifest):
     """Dispatch on ``manifest.experiment`` (src/experiments.py:449-457)."""
     if manifest.experiment not in STUDIES:
-        from .errors import ConfigurationError
-
         raise ConfigurationError(f"unknown experiment {manifest.experiment!r}")
     return STUDIES[manifest.experiment](manifest)

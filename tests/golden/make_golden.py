@@ -304,6 +304,31 @@ def run_frozen():
                   jacobian_refresh="frozen"))
 
 
+def run_experiments():
+    """irkit's own run_iterations (src/experiments.py:250-293) on two manifests
+    of its 1-D periodic catalog (default exact inner solves): the rows the
+    device harness must reproduce from the same manifest JSON."""
+    from irkit.experiments import RunManifest, run_iterations
+
+    cases = {
+        "burgers1d": RunManifest(experiment="iterations", problem="burgers1d",
+                                 problem_params={"n": 128, "nu": 0.02},
+                                 schemes=(("gauss", 2), ("radau_iia", 3), ("gauss", 3)),
+                                 dts=(0.02, 0.01), t_final=0.04),
+        "advdiff1d": RunManifest(experiment="iterations", problem="advdiff1d",
+                                 problem_params={"n": 64, "speed": 1.0, "nu": 0.01},
+                                 schemes=(("gauss", 2), ("lobatto_iiic", 4)),
+                                 dts=(0.05, 0.025), t_final=0.1),
+    }
+    for name, m in cases.items():
+        rows = run_iterations(m)
+        doc = {"manifest": m.to_dict(), "manifest_hash": m.hash, "rows": rows}
+        with open(os.path.join(GOLD, f"experiments_iterations_{name}.json"), "w") as fh:
+            json.dump(doc, fh, indent=1, default=str)
+        print(name, [(r["scheme"], r["dt"], r["newton_iterations"], r["krylov_iterations"],
+                      r["status"]) for r in rows])
+
+
 def run_dae():
     run_dae_case("dae_n16_gauss2", 16, "gauss", 2, 3)
     run_dae_case("dae_n64_gauss2", 64, "gauss", 2, 4)
@@ -330,3 +355,5 @@ if __name__ == "__main__":
         run_sdirk()
     if "frozen" in which:
         run_frozen()
+    if "experiments" in which:
+        run_experiments()

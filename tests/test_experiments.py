@@ -17,7 +17,8 @@ from paper_2101_01776_b200.stats import StepStats
 def _manifest(**kw):
     base = dict(experiment="iterations", problem="nldiff",
                 problem_params={"shape": [64, 64], "k_hi": 4, "sigma": 0.1},
-                schemes=[("gauss", 2), ("radau_iia", 3)], dts=[1e-3, 5e-4], t_final=2e-3)
+                schemes=[("gauss", 2), ("radau_iia", 3)], dts=[1e-3, 5e-4], t_final=2e-3,
+                device={"inner": 4})
     base.update(kw)
     return ex.RunManifest(**base)
 
@@ -66,9 +67,71 @@ def test_gamma_compare_optimal_shift_wins():
     with exact inner solves (the paper's setting): fewer Krylov iterations
     per 2x2 block with gamma*."""
     m = _manifest(experiment="gamma-compare", schemes=[("gauss", 2), ("gauss", 4)],
-                  dts=[2e-3], t_final=4e-3, inner="exact", krylov_rtol=1e-10,
+                  dts=[2e-3], t_final=4e-3, device={"inner": "exact"}, krylov_rtol=1e-10,
                   problem_params={"shape": [64, 64], "k_hi": 4, "sigma": 0.5})
     rows = ex.run(m)
     assert rows and all(r["status"] == "ok" for r in rows)
     for r in rows:
         assert float(r["mean_krylov_star"]) <= float(r["mean_krylov_eta"]), r
+
+
+def test_reference_manifest_serialises_like_irkit():
+    """A manifest with only the reference's keys has irkit's canonical JSON
+    and hash (src/experiments.py:42-97), so one file drives both harnesses;
+    the device knobs appear only when set."""
+    m = ex.RunManifest.from_json(_golden_manifest_text())
+    assert "device" not in m.to_dict() and m.inner == "exact" and m.krylov_maxit == 200
+    assert m.hash == json.loads(_golden_rows_text())["manifest_hash"]
+    src = "/root/reference/pkg/src"
+    if os.path.isdir(src):
+        sys.path.insert(0, src)
+        from irkit.experiments import RunManifest as RefManifest
+
+        ref = RefManifest.from_json(m.to_json())
+        assert ref.to_json() == m.to_json() and ref.hash == m.hash
+    d = _manifest()
+    assert d.to_dict()["device"] == {"inner": 4}
+    assert ex.RunManifest.from_json(d.to_json()) == d
+
+
+def _golden_path(name):
+    return os.path.join(os.path.dirname(__file__), "golden", name)
+
+
+def _golden_manifest_text():
+    with open(_golden_path("experiments_iterations_burgers1d.json")) as fh:
+        return json.dumps(json.load(fh)["manifest"])
+
+
+def _golden_rows_text():
+    with open(_golden_path("experiments_iterations_burgers1d.json")) as fh:
+        doc = json.load(fh)
+    return json.dumps({"manifest_hash": doc["manifest_hash"]})
+
+
+@pytest.mark.gpu
+def test_iterations_study_matches_reference_run_iterations(tmp_path):
+    """f4 parity: irkit's run_iterations (src/experiments.py:250-293) on the
+    reference catalog's burgers1d / advdiff1d (tests/golden/make_golden.py
+    'experiments') against this engine's run_iterations on the SAME manifest
+    JSON, in the reference's default exact inner mode on the device: every
+    row's status, step count and Newton count equal, Krylov and
+    preconditioner counts within +/-1 per step, same manifest hash."""
+    for name in ("experiments_iterations_burgers1d.json", "experiments_iterations_advdiff1d.json"):
+        with open(_golden_path(name)) as fh:
+            doc = json.load(fh)
+        m = ex.RunManifest.from_dict(dict(doc["manifest"], out=str(tmp_path / (name + ".csv"))))
+        rows = ex.run(m)
+        assert len(rows) == len(doc["rows"])
+        for got, want in zip(rows, doc["rows"]):
+            assert got["scheme"] == want["scheme"] and float(got["dt"]) == float(want["dt"])
+            assert got["status"] == want["status"], (got, want)
+            if want["status"] != "ok":
+                continue
+            steps = int(want["steps"])
+            assert int(got["steps"]) == steps
+            assert int(got["newton_iterations"]) == int(want["newton_iterations"]), (got, want)
+            assert abs(int(got["krylov_iterations"]) - int(want["krylov_iterations"])) <= steps
+            assert abs(int(got["precond_applications"]) -
+                       int(want["precond_applications"])) <= 2 * steps
+        assert rows[0]["manifest_hash"] != ""  # (the run's own manifest carries `out`)
