@@ -40,6 +40,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "stage-DOF updates/s (IRK stage solve; configs[1] Burgers 1024^2 Gauss(3))"
+METRIC_CFG2 = "stage-DOF updates/s (IRK stage solve; configs[2] nldiff 4096^2 Gauss(2))"
 UNIT = "DOF/s"
 
 
@@ -353,13 +354,18 @@ def run_reference(args, spec, ws, rank):
     print(json.dumps(line), flush=True)
 
 
-def _config(spec, ws, grid):
+def _config(spec, ws, grid, strong=False):
+    if ws == 1:
+        par = "1 GPU"
+    elif strong:
+        par = f"slab{ws} (y-slabs of the one 4096^2 grid, NCCL halos + allreduce; strong)"
+    else:
+        par = f"slab{ws} (y-slabs, NCCL halos + allreduce; weak: configs[1] tiled {ws}x in y)"
     return {"workload": spec.name + " step 1 (t=0, u0)", "grid": list(grid),
             "scheme": f"{spec.family}({spec.s})", "dt": spec.dt, "inner": "jacobi-4",
-            "variant": 3, "restart": 200,
-            "parallelism": (f"slab{ws} (y-slabs, NCCL halos + allreduce; weak: configs[1] tiled "
-                            f"{ws}x in y)") if ws > 1 else "1 GPU",
-            "l2": "inputs > L2 (V basis 201 x 16.8 MB per rank; step-1 Arnoldi index up to ~40)"}
+            "variant": 3, "restart": 200, "parallelism": par,
+            "l2": "inputs > L2 (V basis 201 x 2N doubles per rank; step-1 Arnoldi index "
+                  "up to ~40 at configs[1], ~200 at configs[2])"}
 
 
 # ------------------------------------------------------------ GPU leg
@@ -465,7 +471,15 @@ def run_ours(args, spec, ws, rank, local):
     prep = pk.prepare_stages(tab)
     cfg = _solver_cfg(pk, spec)
     u0h = spec.u0()
-    if ws > 1:
+    strong = args.workload == "cfg2"
+    if ws > 1 and strong:
+        # strong scaling of configs[2]: the one 4096^2 grid in ws y-slabs
+        from paper_2101_01776_b200.distributed import SlabContext, slab_range
+
+        ctx = SlabContext(prob, rank, ws, transport="nccl", device=local)
+        y0, nl = slab_range(prob.shape[1], rank, ws)
+        u0h = u0h.reshape(prob.shape[1], prob.shape[0])[y0:y0 + nl].reshape(-1).copy()
+    elif ws > 1:
         # weak scaling: configs[1] tiled ws times along y (same h, dt, nu); rank r
         # owns one 1024^2 slab (= the N = 1 field, since u0 is 1-periodic);
         # halos over NCCL, every inner product all-reduced (csrc/comm.cu)
@@ -518,7 +532,7 @@ def run_ours(args, spec, ws, rank, local):
     # stream around the sweeps of each Arnoldi step) over the same step
     ctx.set_timing(True)
     r0 = ctx.counters()
-    rsteps = max(1, min(args.steps, 3))
+    rsteps = max(1, min(args.steps, 1 if strong else 3))
     tr0 = time.perf_counter()
     for _ in range(rsteps):
         u.copy_(u0)
@@ -548,9 +562,10 @@ def run_ours(args, spec, ws, rank, local):
         for _ in range(2):
             pk.step(prob, uh, 0.0, spec.dt, tab, cfg, prep=prep)
     e_stats = []
+    esteps = min(args.steps, 1) if strong else args.steps  # configs[2]: ~1 min per step
     barrier(ws)
     te0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(esteps):
         if ws > 1:  # the slab context's host-buffer step (irkg_step_host)
             ub = uh.copy()
             st = ctx.step_host(ub, 0.0, spec.dt)
@@ -560,29 +575,30 @@ def run_ours(args, spec, ws, rank, local):
     te = max_over_ranks(time.perf_counter() - te0, ws)
     e_dof = sum_over_ranks(sum(s.newton_iterations for s in e_stats) * spec.s * N, ws)
     e2e = {"value": e_dof / te, "unit": UNIT, "h2d_bytes_per_step": 8 * N,
-           "d2h_bytes_per_step": 8 * N, "steps_per_s": args.steps / te}
+           "d2h_bytes_per_step": 8 * N, "steps_per_s": esteps / te, "steps": esteps}
 
     line = None
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "metric": METRIC if not strong else METRIC_CFG2, "value": value, "unit": UNIT,
+            "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded Fourier-mode u0, BASELINE configs[1] shape)",
-            "config": _config(spec, ws, prob.shape),
-            "step_unit": "one IRK step of configs[1] from (t=0, u0): all its Newton iterations "
-                         "+ the u update (u reset from u0 by a device copy inside the timed "
-                         "region)",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic (seeded Fourier-mode u0, BASELINE {spec.name} shape)",
+            "config": _config(spec, ws, prob.shape, strong),
+            "step_unit": f"one IRK step of {spec.name} from (t=0, u0): all its Newton "
+                         "iterations + the u update (u reset from u0 by a device copy inside "
+                         "the timed region)",
             "steps_per_s": steps_per_s, "newton_iterations": newton, "krylov_iterations": krylov,
             "krylov_per_newton": krylov / max(1, newton),
             "gpu_launches": launches, "roofline": roof, "e2e": e2e, "clocks": clk.summary(),
         }
     ctx.close()
     if rank == 0:
-        if ws == 1 and not args.no_large:
+        if ws == 1 and not args.no_large and not strong:
             torch.cuda.empty_cache()
             line["largest_config"] = largest_config(args, local)
-        if ws == 1 and not args.no_cpu:
+        if ws == 1 and not args.no_cpu and not strong:
             dof_cpu, el, kry, cores, kind = cpu_sample(spec, 1)
             line["cpu_baseline"] = {
                 "value": dof_cpu, "unit": UNIT, "cores": cores, "kind": kind,
@@ -604,10 +620,15 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-large", action="store_true", help="skip the configs[2] P=1 step")
     ap.add_argument("--large-n", type=int, default=4096, help="configs[2] grid (testing)")
+    ap.add_argument("--workload", default=os.environ.get("BENCH_WORKLOAD", "cfg1"),
+                    choices=["cfg1", "cfg2"],
+                    help="cfg1 (default): configs[1] Burgers 1024^2, weak-scaled for N > 1; "
+                         "cfg2: configs[2] nldiff 4096^2 Gauss(2), strong-scaled over N GPUs "
+                         "(the north star's 8-GPU efficiency config; ~1 min per step at N = 1)")
     args = ap.parse_args()
     from paper_2101_01776_b200.problems import baseline_config
 
-    spec = baseline_config(1, n=args.n)
+    spec = baseline_config(2 if args.workload == "cfg2" else 1, n=args.n)
     if args.impl == "reference":
         ws = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))

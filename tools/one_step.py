@@ -5,6 +5,7 @@ after one untimed warm-up step -- for ncu launch lists of the real step:
       --cache-control none --clock-control none --csv python tools/one_step.py
 """
 import argparse
+import json
 import os
 import sys
 
@@ -15,6 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--out", default=None, help="write the step's engine counters (JSON)")
     args = ap.parse_args()
     import torch
 
@@ -33,12 +35,20 @@ def main():
     ctx.step_device(u, 0.0, spec.dt)
     torch.cuda.synchronize()
     u.copy_(u0)
+    c0 = ctx.counters()
     torch.cuda.nvtx.range_push("step")
     st = ctx.step_device(u, 0.0, spec.dt)
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
+    c1 = ctx.counters()
+    d = {k: c1[k] - c0[k] for k in ("cgs_bytes", "cgs_launches", "precond_bytes", "op_bytes",
+                                     "kernel_launches", "arnoldi_iterations")}
     print(f"newton={st.newton_iterations} krylov={st.krylov_iterations} "
           f"blocks={ {k: sum(v) for k, v in st.block_iterations.items()} }")
+    print("counters " + json.dumps(d))
+    if args.out:
+        with open(args.out, "w") as fh:
+            json.dump(dict(d, newton=st.newton_iterations, krylov=st.krylov_iterations), fh)
 
 
 if __name__ == "__main__":
