@@ -167,6 +167,11 @@ typedef struct {
 typedef void (*irkg_allreduce_fn)(void *user, double *dev, int count);
 typedef void (*irkg_halo_fn)(void *user, const double *send_lo, const double *send_hi,
                              double *recv_lo, double *recv_hi, long long count);
+/* alltoall: block p (`count` doubles) of `send` goes to rank p, block p of
+ * `recv` arrives from rank p (device pointers; the slab -> pencil transposes
+ * of the DAE constraint solve, replacing _ConstraintSolver.solve,
+ * src/dae.py:108-126, across ranks). */
+typedef void (*irkg_alltoall_fn)(void *user, const double *send, double *recv, long long count);
 
 const char *irkg_last_error(void);
 const char *irkg_version(void);
@@ -182,6 +187,9 @@ int irkg_create(irkg_ctx **out, const irkg_problem *prob, int device, void *stre
 int irkg_create_callback(irkg_ctx **out, const irkg_problem *prob, int device, void *stream,
                          int rank, int nranks, irkg_allreduce_fn allreduce, irkg_halo_fn halo,
                          void *user);
+/* All-to-all of a callback-transport context (same `user` as its other
+ * callbacks); needed only by DAE contexts with nranks > 1. */
+int irkg_set_alltoall_callback(irkg_ctx *ctx, irkg_alltoall_fn alltoall);
 int irkg_destroy(irkg_ctx *ctx);
 int irkg_get_local_extent(irkg_ctx *ctx, int *n_local, int *y0, int *ny_local);
 int irkg_nccl_unique_id(void *out128);

@@ -138,6 +138,7 @@ class Counters(C.Structure):
 ALLREDUCE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_int)
 HALO_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                       C.c_longlong)
+ALLTOALL_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong)
 
 
 class OpField(C.Structure):
@@ -155,6 +156,7 @@ _SIGS = {
     "irkg_create_callback": (
         _I, [C.POINTER(_P), C.POINTER(Problem), _I, _P, _I, _I, ALLREDUCE_FN, HALO_FN, _P]
     ),
+    "irkg_set_alltoall_callback": (_I, [_P, ALLTOALL_FN]),
     "irkg_destroy": (_I, [_P]),
     "irkg_get_local_extent": (_I, [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
     "irkg_nccl_unique_id": (_I, [_P]),

@@ -119,12 +119,21 @@ struct NcclComm : Comm {
     }
     g_nccl.ck(g_nccl.GroupEnd(), "ncclGroupEnd");
   }
+  void alltoall(const double *send, double *recv, long long count, cudaStream_t st) override {
+    g_nccl.ck(g_nccl.GroupStart(), "ncclGroupStart");
+    for (int p = 0; p < nranks; ++p) {
+      g_nccl.ck(g_nccl.Send(send + (size_t)p * count, count, ncclFloat64, p, comm, st), "ncclSend");
+      g_nccl.ck(g_nccl.Recv(recv + (size_t)p * count, count, ncclFloat64, p, comm, st), "ncclRecv");
+    }
+    g_nccl.ck(g_nccl.GroupEnd(), "ncclGroupEnd");
+  }
   bool capturable() const override { return true; }
 };
 
 struct CallbackComm : Comm {
   irkg_allreduce_fn ar;
   irkg_halo_fn hf;
+  irkg_alltoall_fn a2a = nullptr;
   void *user;
   CallbackComm(int rank_, int nranks_, irkg_allreduce_fn a, irkg_halo_fn h, void *u)
       : ar(a), hf(h), user(u) {
@@ -140,7 +149,18 @@ struct CallbackComm : Comm {
     check(cudaStreamSynchronize(st), "sync");
     hf(user, send_lo, send_hi, recv_lo, recv_hi, count);
   }
+  void alltoall(const double *send, double *recv, long long count, cudaStream_t st) override {
+    if (!a2a)
+      throw SolveError(IRKG_ERR_CONFIG,
+                       "callback transport without an all-to-all (irkg_set_alltoall_callback)");
+    check(cudaStreamSynchronize(st), "sync");
+    a2a(user, send, recv, count);
+  }
 };
+
+void comm_set_alltoall(Comm *c, irkg_alltoall_fn fn) {
+  if (auto *cb = dynamic_cast<CallbackComm *>(c)) cb->a2a = fn;
+}
 
 Comm *make_nccl_comm(const void *id128, int rank, int nranks) {
   return new NcclComm(id128, rank, nranks);

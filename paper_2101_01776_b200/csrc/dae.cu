@@ -345,19 +345,33 @@ __global__ void k_dae_crhs(int n, int pin, double dt, double sigma_h2,
     c[p] = (pin && p == 0) ? accw[0] : accw[p] + dt * (sigma_h2 * yu[p]);
 }
 
+// first row and row count of rank r's slab (the rule of Engine::Engine /
+// distributed.slab_range)
+__host__ __device__ inline void slab_rows(int planes, int r, int nranks, int &p0, int &nl) {
+  const int base = planes / nranks, rem = planes % nranks;
+  nl = base + (r < rem ? 1 : 0);
+  p0 = r * base + (r < rem ? r : rem);
+}
+
 // Poisson step 1: f = c / (sigma h^2) off the pin; f_0 = -sum_{i != 0} f_i
-__global__ void k_pois_sum(int n, double inv, const double *__restrict__ c, double *part,
+// (pin: this rank's local point 0 is the global pinned point)
+__global__ void k_pois_sum(int n, int pin, double inv, const double *__restrict__ c, double *part,
                            unsigned *counter, double *out) {
   double acc = 0.0;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
-    if (p != 0) acc += inv * c[p];
+    if (!(pin && p == 0)) acc += inv * c[p];
   reduce2<DBS>(acc, 0.0, part, gridDim.x, counter, out);
 }
 
-__global__ void k_pois_rhs(int n, double inv, const double *__restrict__ c,
+// the pinned point's value on the rank that owns it, 0 elsewhere (summed over ranks)
+__global__ void k_pois_pin(int pin, const double *__restrict__ v, double *out) {
+  *out = pin ? v[0] : 0.0;
+}
+
+__global__ void k_pois_rhs(int n, int pin, double inv, const double *__restrict__ c,
                            const double *__restrict__ sum, double *__restrict__ f) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
-    f[p] = (p == 0) ? -sum[0] : inv * c[p];
+    f[p] = (pin && p == 0) ? -sum[0] : inv * c[p];
 }
 
 // divide the half spectrum by the periodic Laplacian eigenvalues (mode 0 -> 0)
@@ -374,14 +388,94 @@ __global__ void k_pois_scale(int nx, int ny, double ih2x, double ih2y, cufftDoub
   }
 }
 
-// y = yt - yt_0 + c_0 / sigma;  out = post * y  (yt, c global; out = points
-// [off, off + n) of the global vector)
-__global__ void k_pois_fix(int n, long long off, double post, double inv_sigma,
-                           const double *__restrict__ yt, const double *__restrict__ c,
+// the same division on a pencil: `cols` lines of ny values, line kc = wavenumber kx0 + kc
+__global__ void k_pois_scale_cols(int nx, int ny, int kx0, int cols, double ih2x, double ih2y,
+                                  cufftDoubleComplex *F) {
+  const long long tot = (long long)cols * ny;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < tot;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int kx = kx0 + (int)(q / ny), ky = (int)(q % ny);
+    const double sx = sin(M_PI * kx / nx), sy = sin(M_PI * ky / ny);
+    const double lam = -4.0 * ih2x * sx * sx - 4.0 * ih2y * sy * sy;
+    const double inv = (kx == 0 && ky == 0) ? 0.0 : 1.0 / (lam * (double)nx * (double)ny);
+    F[q].x *= inv;
+    F[q].y *= inv;
+  }
+}
+
+// Transposes of the slab -> pencil FFT.  All-to-all block d (sent to / received
+// from rank d) holds nylmax x C complex values, row-major [row][wavenumber].
+// rows -> send: block d = my rows x the wavenumbers rank d owns
+__global__ void k_tr_pack_rows(int nranks, int nyl, int nxh, int C, int nylmax,
+                               const cufftDoubleComplex *__restrict__ F,
+                               cufftDoubleComplex *__restrict__ S) {
+  const long long blk = (long long)nylmax * C, tot = blk * nranks;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int d = (int)(i / blk);
+    const long long r = i % blk;
+    const int iy = (int)(r / C), kc = (int)(r % C), kx = d * C + kc;
+    cufftDoubleComplex v = {0.0, 0.0};
+    if (iy < nyl && kx < nxh) v = F[(size_t)iy * nxh + kx];
+    S[i] = v;
+  }
+}
+
+// recv -> pencil lines: block s = rank s's rows x my wavenumbers; line kc holds all gny rows
+__global__ void k_tr_unpack_cols(int nranks, int gny, int C, int cols, int nylmax,
+                                 const cufftDoubleComplex *__restrict__ R,
+                                 cufftDoubleComplex *__restrict__ Lb) {
+  const long long blk = (long long)nylmax * C, tot = blk * nranks;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(i / blk);
+    const long long r = i % blk;
+    const int iy = (int)(r / C), kc = (int)(r % C);
+    int p0, nl;
+    slab_rows(gny, s, nranks, p0, nl);
+    if (iy < nl && kc < cols) Lb[(size_t)kc * gny + p0 + iy] = R[i];
+  }
+}
+
+// pencil lines -> send: block d = rank d's rows x my wavenumbers
+__global__ void k_tr_pack_cols(int nranks, int gny, int C, int cols, int nylmax,
+                               const cufftDoubleComplex *__restrict__ Lb,
+                               cufftDoubleComplex *__restrict__ S) {
+  const long long blk = (long long)nylmax * C, tot = blk * nranks;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int d = (int)(i / blk);
+    const long long r = i % blk;
+    const int iy = (int)(r / C), kc = (int)(r % C);
+    int p0, nl;
+    slab_rows(gny, d, nranks, p0, nl);
+    cufftDoubleComplex v = {0.0, 0.0};
+    if (iy < nl && kc < cols) v = Lb[(size_t)kc * gny + p0 + iy];
+    S[i] = v;
+  }
+}
+
+// recv -> rows: block s = my rows x the wavenumbers rank s owns
+__global__ void k_tr_unpack_rows(int nranks, int nyl, int nxh, int C, int nylmax,
+                                 const cufftDoubleComplex *__restrict__ R,
+                                 cufftDoubleComplex *__restrict__ F) {
+  const long long blk = (long long)nylmax * C, tot = blk * nranks;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(i / blk);
+    const long long r = i % blk;
+    const int iy = (int)(r / C), kc = (int)(r % C), kx = s * C + kc;
+    if (iy < nyl && kx < nxh) F[(size_t)iy * nxh + kx] = R[i];
+  }
+}
+
+// y = yt - yt_0 + c_0 / sigma;  out = post * y  (yt0, c0: values at the global pinned point)
+__global__ void k_pois_fix(int n, double post, double inv_sigma, const double *__restrict__ yt,
+                           const double *__restrict__ yt0, const double *__restrict__ c0,
                            double *__restrict__ out) {
-  const double y0 = yt[0], pin = c[0] * inv_sigma;
+  const double y0 = yt0[0], pin = c0[0] * inv_sigma;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
-    out[p] = post * ((yt[off + p] - y0) + pin);
+    out[p] = post * ((yt[p] - y0) + pin);
 }
 
 // composite true residual of the reordered 4x4 block (src/dae.py:238-253, 307-314):
@@ -421,29 +515,54 @@ __global__ void k_dae_block_res(Grid g, double nu, double h2, double eta, double
 
 void Engine::dae_init() {
   if (!dae) return;
-  // the constraint solve runs on the global grid (slab mode: gathered rhs,
-  // solved redundantly on every rank -- see constraint_solve)
   const int gny = gplanes;
-  const long long ng = (long long)grid.nx * gny;
   dalloc_raw((void **)&ACC, sizeof(double) * 4 * N);
   dalloc_raw((void **)&XU, sizeof(double) * 2 * N);
   dalloc_raw((void **)&CR, sizeof(double) * N);
-  dalloc_raw((void **)&PT, sizeof(double) * ng);
-  if (slab()) dalloc_raw((void **)&CG, sizeof(double) * ng);
-  dalloc_raw((void **)&fft_buf, sizeof(cufftDoubleComplex) * (size_t)gny * (grid.nx / 2 + 1));
+  dalloc_raw((void **)&PT, sizeof(double) * N);
   h2 = (prob.length / grid.nx) * ((prob.length_y > 0.0 ? prob.length_y : prob.length) / gny);
+  const int nxh = grid.nx / 2 + 1;
   cufftHandle p1, p2;
-  if (cufftPlan2d(&p1, gny, grid.nx, CUFFT_D2Z) != CUFFT_SUCCESS ||
-      cufftPlan2d(&p2, gny, grid.nx, CUFFT_Z2D) != CUFFT_SUCCESS)
-    throw CudaError("cufftPlan2d failed");
+  if (!slab()) {
+    dalloc_raw((void **)&fft_buf, sizeof(cufftDoubleComplex) * (size_t)gny * nxh);
+    if (cufftPlan2d(&p1, gny, grid.nx, CUFFT_D2Z) != CUFFT_SUCCESS ||
+        cufftPlan2d(&p2, gny, grid.nx, CUFFT_Z2D) != CUFFT_SUCCESS)
+      throw CudaError("cufftPlan2d failed");
+    fft_fwd = (int)p1;
+    fft_inv = (int)p2;
+    return;
+  }
+  // slab -> pencil layout: rank r transforms x-wavenumbers [r C, (r+1) C)
+  tr_C = (nxh + nranks - 1) / nranks;
+  tr_cols = std::max(0, std::min(tr_C, nxh - rank * tr_C));
+  tr_nylmax = (gny + nranks - 1) / nranks;
+  const size_t blk = (size_t)tr_nylmax * tr_C;  // complex values per all-to-all block
+  dalloc_raw((void **)&fft_buf, sizeof(cufftDoubleComplex) * (size_t)grid.ny * nxh);
+  dalloc_raw((void **)&tr_send, sizeof(cufftDoubleComplex) * blk * nranks);
+  dalloc_raw((void **)&tr_recv, sizeof(cufftDoubleComplex) * blk * nranks);
+  dalloc_raw((void **)&tr_lines, sizeof(cufftDoubleComplex) * (size_t)tr_C * gny);
+  int nrow = grid.nx, ncol = gny;
+  if (cufftPlanMany(&p1, 1, &nrow, nullptr, 1, grid.nx, nullptr, 1, nxh, CUFFT_D2Z, grid.ny) !=
+          CUFFT_SUCCESS ||
+      cufftPlanMany(&p2, 1, &nrow, nullptr, 1, nxh, nullptr, 1, grid.nx, CUFFT_Z2D, grid.ny) !=
+          CUFFT_SUCCESS)
+    throw CudaError("cufftPlanMany (rows) failed");
   fft_fwd = (int)p1;
   fft_inv = (int)p2;
+  if (tr_cols > 0) {
+    cufftHandle p3;
+    if (cufftPlanMany(&p3, 1, &ncol, nullptr, 1, gny, nullptr, 1, gny, CUFFT_Z2Z, tr_cols) !=
+        CUFFT_SUCCESS)
+      throw CudaError("cufftPlanMany (columns) failed");
+    fft_col = (int)p3;
+  }
 }
 
 void Engine::dae_fini() {
   if (fft_fwd >= 0) cufftDestroy((cufftHandle)fft_fwd);
   if (fft_inv >= 0) cufftDestroy((cufftHandle)fft_inv);
-  void *bufs[] = {ACC, XU, CR, PT, CG, fft_buf};
+  if (fft_col >= 0) cufftDestroy((cufftHandle)fft_col);
+  void *bufs[] = {ACC, XU, CR, PT, fft_buf, tr_send, tr_recv, tr_lines};
   for (void *b : bufs)
     if (b) cudaFree(b);
 }
@@ -451,40 +570,77 @@ void Engine::dae_fini() {
 int Engine::dae_grid() const { return grid.ny < sms * 8 ? grid.ny : sms * 8; }
 
 // out = post * (sigma G_w)^{-1} c  -- _ConstraintSolver.solve, src/dae.py:122-126.
-// Slab mode: the ranks' slabs of c are gathered into the global vector (an
-// all-reduce of the zero-padded slab: exact, transport-agnostic) and every
-// rank runs the same global FFT solve, keeping its own slab of the result.
-// A constraint solve is 2 per 2x2 block per Newton iteration, against
-// hundreds of GMRES iterations, so the redundant O(N_global) FFT is cheap and
-// avoids a distributed transpose; the pinned row stays exactly the global one.
 void Engine::constraint_solve(double sigma, const double *c, double *out, double post) {
   if (sigma == 0.0) throw SolveError(IRKG_ERR_INDEX, "constraint Jacobian is singular");
-  const int gny = gplanes;
-  const long long ng = (long long)grid.nx * gny;
-  const double *cg = c;
-  long long off = 0;
   if (slab()) {
-    off = (long long)p0 * grid.nx;
-    check(cudaMemsetAsync(CG, 0, sizeof(double) * ng, stream), "gather");
-    check(cudaMemcpyAsync(CG + off, c, sizeof(double) * N, cudaMemcpyDeviceToDevice, stream),
-          "gather");
-    allreduce(CG, (int)ng);
-    cg = CG;
+    constraint_solve_slab(sigma, c, out, post);
+    return;
   }
-  const int n = (int)ng;
+  const int n = (int)N;
   const double inv = 1.0 / (sigma * h2);
-  k_pois_sum<<<dae_grid(), DBS, 0, stream>>>(n, inv, cg, part, counter, &scal_dev[4]);
-  k_pois_rhs<<<grid_for(ng), 256, 0, stream>>>(n, inv, cg, &scal_dev[4], PT);
+  k_pois_sum<<<dae_grid(), DBS, 0, stream>>>(n, 1, inv, c, part, counter, &scal_dev[4]);
+  k_pois_rhs<<<grid_for(N), 256, 0, stream>>>(n, 1, inv, c, &scal_dev[4], PT);
   cufftSetStream((cufftHandle)fft_fwd, stream);
   cufftSetStream((cufftHandle)fft_inv, stream);
   if (cufftExecD2Z((cufftHandle)fft_fwd, PT, (cufftDoubleComplex *)fft_buf) != CUFFT_SUCCESS)
     throw CudaError("cufftExecD2Z failed");
-  k_pois_scale<<<grid_for((long long)gny * (grid.nx / 2 + 1)), 256, 0, stream>>>(
-      grid.nx, gny, grid.ih2[0], grid.ih2[1], (cufftDoubleComplex *)fft_buf);
+  k_pois_scale<<<grid_for((long long)grid.ny * (grid.nx / 2 + 1)), 256, 0, stream>>>(
+      grid.nx, grid.ny, grid.ih2[0], grid.ih2[1], (cufftDoubleComplex *)fft_buf);
   if (cufftExecZ2D((cufftHandle)fft_inv, (cufftDoubleComplex *)fft_buf, PT) != CUFFT_SUCCESS)
     throw CudaError("cufftExecZ2D failed");
-  k_pois_fix<<<grid_for(N), 256, 0, stream>>>((int)N, off, post, 1.0 / sigma, PT, cg, out);
+  k_pois_fix<<<grid_for(N), 256, 0, stream>>>(n, post, 1.0 / sigma, PT, PT, c, out);
   count(4);
+}
+
+// The same solve on y-slabs: a slab -> pencil transpose FFT.  Every rank
+// transforms its own rows along x, one all-to-all gives rank r the
+// x-wavenumbers [r C, (r+1) C) with all of y (blocks padded to the largest
+// slab), the y transforms and the division by the Laplacian's eigenvalues
+// run on those pencils, and the way back mirrors it: O(N/P) work and
+// 2 x 16 N/P bytes on the links per rank and solve, no global vector
+// anywhere.  The zero-mean shift and the pinned row (global point 0, owned by
+// the rank with grid.pin) travel in two small all-reduces.
+void Engine::constraint_solve_slab(double sigma, const double *c, double *out, double post) {
+  const int n = (int)N, nx = grid.nx, nyl = grid.ny, gny = gplanes, nxh = nx / 2 + 1;
+  const double inv = 1.0 / (sigma * h2);
+  auto *FB = (cufftDoubleComplex *)fft_buf;
+  auto *SB = (cufftDoubleComplex *)tr_send, *RB = (cufftDoubleComplex *)tr_recv;
+  auto *LB = (cufftDoubleComplex *)tr_lines;
+  const long long blk = (long long)tr_nylmax * tr_C;
+  // scal[4] = sum_{i != 0} f_i, scal[5] = c at global point 0 (pin rank only)
+  k_pois_sum<<<dae_grid(), DBS, 0, stream>>>(n, grid.pin, inv, c, part, counter, &scal_dev[4]);
+  k_pois_pin<<<1, 1, 0, stream>>>(grid.pin, c, &scal_dev[5]);
+  allreduce(&scal_dev[4], 2);
+  k_pois_rhs<<<grid_for(N), 256, 0, stream>>>(n, grid.pin, inv, c, &scal_dev[4], PT);
+  cufftSetStream((cufftHandle)fft_fwd, stream);
+  cufftSetStream((cufftHandle)fft_inv, stream);
+  if (cufftExecD2Z((cufftHandle)fft_fwd, PT, FB) != CUFFT_SUCCESS)
+    throw CudaError("cufftExecD2Z (rows) failed");
+  const int gp = grid_for((long long)nranks * blk);
+  k_tr_pack_rows<<<gp, 256, 0, stream>>>(nranks, nyl, nxh, tr_C, tr_nylmax, FB, SB);
+  comm->alltoall(tr_send, tr_recv, 2 * blk, stream);
+  k_tr_unpack_cols<<<gp, 256, 0, stream>>>(nranks, gny, tr_C, tr_cols, tr_nylmax, RB, LB);
+  if (tr_cols > 0) {
+    cufftSetStream((cufftHandle)fft_col, stream);
+    if (cufftExecZ2Z((cufftHandle)fft_col, LB, LB, CUFFT_FORWARD) != CUFFT_SUCCESS)
+      throw CudaError("cufftExecZ2Z failed");
+    k_pois_scale_cols<<<grid_for((long long)tr_cols * gny), 256, 0, stream>>>(
+        nx, gny, rank * tr_C, tr_cols, grid.ih2[0], grid.ih2[1], LB);
+    if (cufftExecZ2Z((cufftHandle)fft_col, LB, LB, CUFFT_INVERSE) != CUFFT_SUCCESS)
+      throw CudaError("cufftExecZ2Z failed");
+  }
+  k_tr_pack_cols<<<gp, 256, 0, stream>>>(nranks, gny, tr_C, tr_cols, tr_nylmax, LB, SB);
+  comm->alltoall(tr_send, tr_recv, 2 * blk, stream);
+  k_tr_unpack_rows<<<gp, 256, 0, stream>>>(nranks, nyl, nxh, tr_C, tr_nylmax, RB, FB);
+  if (cufftExecZ2D((cufftHandle)fft_inv, FB, PT) != CUFFT_SUCCESS)
+    throw CudaError("cufftExecZ2D (rows) failed");
+  // scal[8] = yt at global point 0
+  k_pois_pin<<<1, 1, 0, stream>>>(grid.pin, PT, &scal_dev[8]);
+  allreduce(&scal_dev[8], 1);
+  k_pois_fix<<<grid_for(N), 256, 0, stream>>>(n, post, 1.0 / sigma, PT, &scal_dev[8],
+                                              &scal_dev[5], out);
+  count(9);
+  counters.halo_exchanges += 2;
 }
 
 void Engine::ara_jacobi_chain(const Op &L, double alpha, double dt, int inner, const VecIn &vin,

@@ -111,6 +111,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   if (const char *e = getenv("IRKG_GRAPHS")) use_graphs = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_L2_MB")) l2_budget = atoi(e) > 0 ? ((size_t)atoi(e) << 20) : 0;
   if (const char *e = getenv("IRKG_FUSED_JACOBI")) fused_jacobi = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_FUSED_JACOBI3D")) fused_jacobi3d = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_JSPAN")) jspan_override = atoi(e);
   if (const char *e = getenv("IRKG_PAIR_JACOBI")) pair_jacobi = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_JACOBI_SPLIT")) jacobi_split = (atoi(e) != 0);
@@ -1145,6 +1146,12 @@ int irkg_create_callback(irkg_ctx **out, const irkg_problem *prob, int device, v
     auto *c = new irkg_ctx;
     c->eng = new Engine(*prob, device, (cudaStream_t)stream, rank, nranks, comm);
     *out = c;
+  });
+}
+
+int irkg_set_alltoall_callback(irkg_ctx *ctx, irkg_alltoall_fn alltoall) {
+  IRKG_GUARD({
+    if (ctx->eng->comm) comm_set_alltoall(ctx->eng->comm, alltoall);
   });
 }
 

@@ -58,9 +58,14 @@ struct Comm {
     for (int i = 0; i < nx; ++i)
       halo(x[i].send_lo, x[i].send_hi, x[i].recv_lo, x[i].recv_hi, x[i].count, st);
   }
+  // personalised all-to-all: block p of `send` (count doubles) goes to rank p,
+  // block p of `recv` arrives from rank p (the pencil transposes of the DAE
+  // constraint solve, dae.cu)
+  virtual void alltoall(const double *send, double *recv, long long count, cudaStream_t st) = 0;
   // enqueues only device work (no host round trip): graph-capturable
   virtual bool capturable() const { return false; }
 };
+void comm_set_alltoall(Comm *c, irkg_alltoall_fn fn);
 Comm *make_nccl_comm(const void *id128, int rank, int nranks);
 Comm *make_callback_comm(int rank, int nranks, irkg_allreduce_fn a, irkg_halo_fn h, void *u);
 void nccl_unique_id(void *out128);
@@ -247,9 +252,18 @@ struct Engine {
   bool dae = false;
   double h2 = 0.0;
   double *ACC = nullptr, *XU = nullptr, *CR = nullptr, *PT = nullptr;
-  double *CG = nullptr;  // slab mode: the gathered global constraint rhs (PT is global then)
   void *fft_buf = nullptr;
   int fft_fwd = -1, fft_inv = -1;
+  // slab mode: the constraint solve as a slab -> pencil transpose FFT.  Rows
+  // (x) are transformed where they live, an all-to-all hands every rank a
+  // pencil of tr_cols x-wavenumbers with all of y, the y transforms and the
+  // eigenvalue division run there, and the way back mirrors it.
+  int tr_C = 0;       // x-wavenumbers per rank (the last ranks may own fewer / none)
+  int tr_cols = 0;    // ... owned by this rank
+  int tr_nylmax = 0;  // most rows any rank owns (all-to-all blocks are padded to it)
+  int fft_col = -1;
+  double *tr_send = nullptr, *tr_recv = nullptr, *tr_lines = nullptr;
+  void constraint_solve_slab(double sigma, const double *c, double *out, double post);
   void dae_init();
   void dae_fini();
   int dae_grid() const;
@@ -282,6 +296,11 @@ struct Engine {
   bool jacobi_chain_fused(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
                           int in_off, const double *zc, double cpl, double *x_out,
                           const GCtrl *skip);
+  // jacobi3d.cu (3.5-D blocked inner solves, 3-D grids; IRKG_FUSED_JACOBI3D=0: K launches)
+  bool fused_jacobi3d = true;
+  bool jacobi_chain_fused3d(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
+                            int in_off, const double *zc, double cpl, double *x_out,
+                            const GCtrl *skip);
 
   // PDL launch of an Arnoldi-body kernel (IRKG_PDL=0: ordinary launch)
   bool use_pdl = true;

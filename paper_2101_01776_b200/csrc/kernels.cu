@@ -714,6 +714,7 @@ void Engine::jacobi_chain(const Op &L, double alpha, double dt, int inner, const
     return;
   }
   if (jacobi_chain_fused(L, alpha, dt, inner, vin, in_off, zc, cpl, x_out, skip)) return;
+  if (jacobi_chain_fused3d(L, alpha, dt, inner, vin, in_off, zc, cpl, x_out, skip)) return;
   const int gb = grid_for(N);
   double *tbuf = zc ? tmp_t : nullptr;
   // sweep i (1-based) writes into out if (inner - i) even, else tmp_x

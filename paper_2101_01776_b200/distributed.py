@@ -57,6 +57,19 @@ def gather(local_vecs, shape):
     return out
 
 
+def pencil_layout(nx, ny, nranks):
+    """Slab -> pencil layout of the DAE constraint solve (csrc/dae.cu
+    ``constraint_solve_slab``): ``(C, nylmax, cols)`` with C x-wavenumbers of
+    the half spectrum (nx//2 + 1) per rank, all-to-all blocks padded to
+    ``nylmax`` rows, and ``cols[r]`` the wavenumbers rank r actually owns
+    (``[r*C, r*C + cols[r])``; the last ranks may own fewer or none)."""
+    nxh = int(nx) // 2 + 1
+    c = -(-nxh // int(nranks))
+    nylmax = -(-int(ny) // int(nranks))
+    cols = [max(0, min(c, nxh - r * c)) for r in range(int(nranks))]
+    return c, nylmax, cols
+
+
 def _cuda_view(ptr, count):
     """A float64 CUDA tensor aliasing device memory at ``ptr`` (no copy)."""
     t = torch()
@@ -84,6 +97,7 @@ class TorchDistTransport:
         self.group = group
         self.ar = _lib.ALLREDUCE_FN(self._allreduce)
         self.halo = _lib.HALO_FN(self._halo)
+        self.a2a = _lib.ALLTOALL_FN(self._alltoall)
 
     def _allreduce(self, user, ptr, count):
         t = torch()
@@ -91,6 +105,14 @@ class TorchDistTransport:
         h = v.cpu()
         self.dist.all_reduce(h, group=self.group)
         v.copy_(h)
+        t.cuda.synchronize()
+
+    def _alltoall(self, user, send, recv, count):
+        t = torch()
+        h = _cuda_view(send, count * self.nranks).cpu()
+        o = t.empty_like(h)
+        self.dist.all_to_all_single(o, h, group=self.group)
+        _cuda_view(recv, count * self.nranks).copy_(o)
         t.cuda.synchronize()
 
     def _halo(self, user, send_lo, send_hi, recv_lo, recv_hi, count):
@@ -135,6 +157,8 @@ class SlabContext(Context):
             rc = self.lib.irkg_create_callback(
                 C.byref(h), C.byref(p), dev, C.c_void_p(self.stream.cuda_stream), self.rank,
                 self.nranks, self._transport.ar, self._transport.halo, None)
+            if rc == 0:
+                rc = self.lib.irkg_set_alltoall_callback(h, self._transport.a2a)
         elif transport == "nccl":
             import torch.distributed as dist
 

@@ -22,7 +22,7 @@ import torch.multiprocessing as mp
 
 from oracle import irk
 from oracle.problems import build_problem
-from paper_2101_01776_b200.distributed import gather, scatter, slab_range
+from paper_2101_01776_b200.distributed import gather, pencil_layout, scatter, slab_range
 
 
 def test_slab_ranges_tile_the_axis():
@@ -252,3 +252,102 @@ def test_two_rank_gloo_dae_slabs_and_gathered_constraint_solve():
     assert ok_lu and ok_gw
     assert exact_gather
     assert rel <= 1e-13, rel
+
+
+def _pencil_worker(rank, nranks, port, shape, queue):
+    """The slab -> pencil transpose FFT of the constraint solve
+    (csrc/dae.cu constraint_solve_slab) restated with numpy FFTs and a gloo
+    all-to-all: rows transformed on the slabs, padded blocks exchanged, the y
+    transforms and the eigenvalue division on pencils, and back; the zero-mean
+    shift and the pinned row through two small all-reduces.  Compared with the
+    global sparse solve of the reference's constraint matrix."""
+    import scipy.sparse.linalg as spla
+
+    from oracle.problems import DaeProblemDef
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=nranks)
+    try:
+        nx, ny = shape
+        pd = DaeProblemDef(shape, 1e-3)
+        rng = np.random.default_rng(11)
+        u = rng.standard_normal(pd.dim)
+        w = rng.standard_normal(pd.dim)
+        _, _, _, gw = pd.blocks_csr(u, w, 0.0)
+        c = rng.standard_normal(pd.dim)
+        sigma = 0.7
+        h2 = (1.0 / nx) * (1.0 / ny)
+        ih2 = (nx * nx, ny * ny)
+        p0, nl = slab_range(ny, rank, nranks)
+        cl = scatter(c, shape, rank, nranks).copy()
+        pin = p0 == 0
+        C_, nylmax, cols = pencil_layout(nx, ny, nranks)
+        nxh = nx // 2 + 1
+        inv = 1.0 / (sigma * h2)
+        f = inv * cl
+        part = np.array([f.sum() - (f[0] if pin else 0.0), cl[0] if pin else 0.0])
+        tot = _allreduce(part)
+        if pin:
+            f[0] = -tot[0]
+        F = np.fft.rfft(f.reshape(nl, nx), axis=1)                  # (nl, nxh)
+        send = np.zeros((nranks, nylmax, C_), dtype=complex)
+        for d in range(nranks):
+            k0 = d * C_
+            send[d, :nl, :cols[d]] = F[:, k0:k0 + cols[d]]
+        recv = np.zeros_like(send)
+        ts, tr = torch.from_numpy(send.view(np.float64).reshape(-1)), \
+            torch.from_numpy(recv.view(np.float64).reshape(-1))
+        dist.all_to_all_single(tr, ts)
+        lines = np.zeros((C_, ny), dtype=complex)
+        for s_ in range(nranks):
+            q0, ql = slab_range(ny, s_, nranks)
+            lines[:cols[rank], q0:q0 + ql] = recv[s_, :ql, :cols[rank]].T
+        L = np.fft.fft(lines[:cols[rank]], axis=1)
+        kx = rank * C_ + np.arange(cols[rank])[:, None]
+        ky = np.arange(ny)[None, :]
+        lam = -4.0 * ih2[0] * np.sin(np.pi * kx / nx) ** 2 - 4.0 * ih2[1] * np.sin(np.pi * ky / ny) ** 2
+        with np.errstate(divide="ignore"):
+            scale = np.where((kx == 0) & (ky == 0), 0.0, 1.0 / lam)
+        lines[:cols[rank]] = np.fft.ifft(L * scale, axis=1)
+        for d in range(nranks):
+            q0, ql = slab_range(ny, d, nranks)
+            send[d] = 0.0
+            send[d, :ql, :cols[rank]] = lines[:cols[rank], q0:q0 + ql].T
+        dist.all_to_all_single(tr, ts)
+        for s_ in range(nranks):
+            k0 = s_ * C_
+            F[:, k0:k0 + cols[s_]] = recv[s_, :nl, :cols[s_]]
+        yt = np.fft.irfft(F, n=nx, axis=1).reshape(-1)
+        yt0 = _allreduce(np.array([yt[0] if pin else 0.0]))[0]
+        y_loc = (yt - yt0) + tot[1] / sigma
+        parts = [None] * nranks
+        dist.all_gather_object(parts, y_loc)
+        if rank == 0:
+            y_ref = spla.spsolve((sigma * gw).tocsc(), c)
+            rel = float(np.linalg.norm(gather(parts, shape) - y_ref) / np.linalg.norm(y_ref))
+            queue.put(rel)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nranks,shape", [(2, (12, 14)), (3, (16, 10)), (3, (6, 7))])
+def test_gloo_pencil_transpose_constraint_solve(nranks, shape):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pencil_worker, args=(r, nranks, port, shape, q))
+             for r in range(nranks)]
+    for p in procs:
+        p.start()
+    rel = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    assert rel <= 1e-12, rel
+
+
+def test_pencil_layout_covers_the_half_spectrum():
+    for nx, ny, p in [(2048, 2048, 8), (40, 40, 2), (32, 36, 3), (6, 7, 3), (10, 4, 8)]:
+        c, nylmax, cols = pencil_layout(nx, ny, p)
+        assert sum(cols) == nx // 2 + 1
+        assert all(0 <= k <= c for k in cols)
+        assert nylmax >= max(slab_range(ny, r, p)[1] for r in range(p))

@@ -43,6 +43,9 @@ def _run(tmp_path, nproc, *args, env=None):
          "--dt", "2e-4"]),
     (3, ["--kind", "nldiff", "--shape", "16,14,24", "--family", "gauss", "--stages", "2",
          "--dt", "1e-3"]),
+    # in-plane extents >= 32: the 3.5-D blocked chain (csrc/jacobi3d.cu) on z-slabs with ghost planes
+    (2, ["--kind", "nldiff", "--shape", "32,34,16", "--family", "gauss", "--stages", "2",
+         "--dt", "1e-3"]),
     # the vorticity DAE: 9-point stencils on slabs + the gathered constraint solve
     (2, ["--kind", "arakawa", "--shape", "40,40", "--family", "gauss", "--stages", "2",
          "--dt", "2e-3"]),

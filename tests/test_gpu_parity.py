@@ -249,6 +249,50 @@ def test_fused_jacobi_chain_matches_oracle(kind, shape, params, inner):
     assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
 
 
+FUSED3D_CASES = [
+    ("nldiff", (32, 32, 10), {}),
+    ("nldiff", (58, 40, 13), {}),       # ragged last tiles in x and y, ragged z bands
+    ("burgers", (34, 32, 9), {"nu": 0.02}),
+    ("rad", (32, 36, 12), {"nu": 0.02, "c": 0.3, "lam": -0.4, "mu": 0.2}),
+]
+
+
+@pytest.mark.parametrize("kind,shape,params", FUSED3D_CASES)
+@pytest.mark.parametrize("inner", [1, 2, 4, 6])
+def test_fused_jacobi_chain_3d_matches_oracle(kind, shape, params, inner):
+    """The 3.5-D blocked inner solve (csrc/jacobi3d.cu: 32x32 in-plane tiles
+    sliding along z, all k sweeps in one pass) equals k separate damped-Jacobi
+    sweeps of the reference (src/irk_core.py:117-123)."""
+    prob = GridProblem(kind, shape, **params)
+    pd, _ = _oracle_sys(prob)
+    rng = np.random.default_rng(10 + inner)
+    U = rng.standard_normal((1, pd.dim))
+    field = pk.OperatorField.linearize(prob, U)
+    lmat = pd.linearize_csr(U[0], 0.0)
+    r = rng.standard_normal(pd.dim)
+    got = pk.ShiftedSolver(3.1, None, field, 2e-3, inner).solve(r)
+    want = irk.ShiftedSolver(3.1, lmat, 2e-3, inner).solve(r)
+    assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
+
+
+def test_fused_block_precond_3d_matches_oracle():
+    """Block lower-triangular 2x2 preconditioner on a 3-D grid: both fused
+    chains (the second with the coupling field) against the oracle."""
+    prob = GridProblem("nldiff", (40, 32, 11))
+    pd, _ = _oracle_sys(prob)
+    rng = np.random.default_rng(5)
+    U = rng.standard_normal((2, pd.dim))
+    f1 = pk.OperatorField.linearize(prob, U[:1])
+    f2 = pk.OperatorField.linearize(prob, U[1:])
+    l1, l2 = pd.linearize_csr(U[0], 0.0), pd.linearize_csr(U[1], 0.0)
+    eta, beta, phi, dt = 2.681083, 3.050430, -1.104613, 1e-3
+    r = rng.standard_normal(2 * pd.dim)
+    sysb = pk.Block2x2System(eta, beta, phi, None, f1, f2, dt)
+    got = pk.precond_block2x2(sysb, pk.PrecondSpec(inner=4), r)
+    want = irk.block2x2_precond(eta, beta, phi, l1, l2, dt, "star", 4)(r)
+    assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
+
+
 @pytest.mark.parametrize("kind,shape,params", FUSED_CASES[:3])
 def test_fused_block_precond_matches_oracle(kind, shape, params):
     prob = GridProblem(kind, shape, **params)

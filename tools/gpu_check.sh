@@ -13,7 +13,7 @@ timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench exit $?
 timeout 600 python tools/phase_probe.py > $O/probe.txt 2>&1
 if [ "${SKIP_NCU:-0}" != "1" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu > $O/ncu_launch.log 2>&1; echo "ncu exit $?" >> $O/ncu_launch.log
+  python bench.py --steps 2 --warmup 3 --no-cpu --no-large > $O/ncu_launch.log 2>&1; echo "ncu exit $?" >> $O/ncu_launch.log
 python tools/launch_summary.py $O/launches.csv > $O/launch_summary.txt 2>&1
 # CGS sweeps at a pinned Arnoldi index (j = 8): per-launch DRAM traffic vs algorithmic bytes
 timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "probe6/" -k regex:k_cgs -s 6 -c 3 \

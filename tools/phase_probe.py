@@ -18,6 +18,8 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--js", default="0,2,4,8,12,16,24,32")
+    ap.add_argument("--short", action="store_true",
+                    help="inner solves and block operator only (no graph-mode / CGS rows)")
     ap.add_argument("--block1", action="store_true",
                     help="probe a 1x1 block (eta = 4.644371, configs[1]'s real eigenvalue)")
     args = ap.parse_args()
@@ -65,6 +67,8 @@ def main():
     for name, ph in [("precond (2 chains)", 0), ("jacobi chain 1", 1), ("jacobi chain 2", 2),
                      ("block operator", 3), ("stage mix (s,N)", 9), ("backsolve", 11)]:
         print(f"{name:22s} {probe(ph, 4) - pin:8.2f} us")
+    if args.short:
+        return
     # graph mode: 8 steps j0..j0+7 of the captured WHILE loop (exit test
     # disabled on the stale probe state), per Arnoldi step
     for j0 in (0, 8, 16, 32, 100, 180):
