@@ -554,6 +554,11 @@ def run_ours(args, spec, ws, rank, local):
             "algorithmic_bytes_per_launch": cgs_bytes / max(1, cgs_launch),
             "avg_launch_us": 1e3 * cgs_ms / max(1, cgs_launch),
             "share_of_step": (cgs_ms * 1e-3) / tr if tr > 0 else None}
+    if traffic and cgs_ms > 0 and cgs_launch > 0:
+        # the committed warm-L2 ncu DRAM bytes per launch over the live launch time: the
+        # part of `achieved` that really crossed HBM (the rest hit the L2-persisting slots)
+        roof["dram_achieved"] = traffic / (cgs_ms * 1e-3 / cgs_launch) / 1e9
+        roof["dram_frac"] = roof["dram_achieved"] / peak
 
     # e2e: the public API with host buffers (H2D of u + D2H of u_next per step),
     # the caller's state in page-locked memory (pk.step returns u_next pinned too)
