@@ -158,6 +158,8 @@ __global__ void __launch_bounds__(T3THREADS, 1)
   auto refill = [&](int t, int slot) {
     if (!SLAB) {
       if (t < t1) {
+        IRKG_DCHECK(goff >= 0 && goff + nxy <= nloc && slot >= 0 && slot < JR);
+        IRKG_DCHECK(q[0] >= 0 && q[0] < nxy && q[1] >= 0 && q[1] < nxy);
         double *d = ring + (size_t)slot * 3 * T3P + tid;
         const double *pa = ar.base + goff, *pr = pr_base + goff;
         cp_async8(d, pa + q[0]);
@@ -242,6 +244,7 @@ __global__ void __launch_bounds__(T3THREADS, 1)
     refill(t + JR, SLOT);
     cp_async_commit3();
 
+    IRKG_DCHECK(own[0] < T3P && own[1] < T3P && nbi[0][0] < T3P && nbi[1][3] < T3P);
     double *wr = (U & 1) ? buf_o : buf_e;        // planes produced now
     const double *rd = (U & 1) ? buf_e : buf_o;  // produced in the previous step
     double xn[2], pn[2];
@@ -312,7 +315,10 @@ __global__ void __launch_bounds__(T3THREADS, 1)
     if (zo >= z0 && zo < z1) {
 #pragma unroll
       for (int c = 0; c < 2; ++c)
-        if (valid[c]) x_out[(size_t)zo * nxy + q[c]] = xn[c];
+        if (valid[c]) {
+          IRKG_DCHECK(zo >= 0 && zo < nz && (long long)zo * nxy + q[c] < nloc);
+          x_out[(size_t)zo * nxy + q[c]] = xn[c];
+        }
     }
     if (K > 1) __syncthreads();
   };

@@ -83,3 +83,17 @@ def test_nccl_ring_with_halo_overlap_matches(tmp_path):
     assert [s[0] for s in r["stats"]] == [s[0] for s in r["single_stats"]]
     assert all(abs(a[1] - b[1]) <= 1 for a, b in zip(r["stats"], r["single_stats"]))
     assert r["halos"] > 0
+
+
+def test_nccl_ring_dae_transposed_constraint_solve(tmp_path):
+    """The DAE step over the native NCCL transport on a forced 1-rank slab:
+    9-point stencils through NCCL ghost planes and the constraint solve's
+    slab -> pencil transposes through NcclComm::alltoall (grouped self
+    send/recv); must equal the plain single-rank run (2-D cuFFT solve)."""
+    r = _run(tmp_path, 1, "--kind", "arakawa", "--shape", "40,36", "--family", "gauss",
+             "--stages", "2", "--dt", "2e-3", "--transport", "nccl",
+             env={"IRKG_FORCE_SLAB": "1"})
+    assert r["rel"] <= 1e-12, r
+    assert [s[0] for s in r["stats"]] == [s[0] for s in r["single_stats"]]
+    assert all(abs(a[1] - b[1]) <= 1 for a, b in zip(r["stats"], r["single_stats"]))
+    assert r["halos"] > 0
