@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "libirkg.so")
 #: checked build: the same sources with -DIRKG_CHECKED (device bounds /
 #: invariant checks that trap; the compute-sanitizer stand-in)
 LIB_CHECKED = os.path.join(HERE, "libirkg_checked.so")
-SOURCES = ["kernels.cu", "cgs.cu", "stencil.cu", "jacobi.cu", "jacobi3d.cu", "dae.cu", "comm.cu", "dirk.cu", "banded.cu", "mg.cu", "rcgmres.cu", "engine.cu"]
+SOURCES = ["kernels.cu", "cgs.cu", "stencil.cu", "jacobi.cu", "jacobi3d.cu", "dae.cu", "arachain.cu", "comm.cu", "dirk.cu", "banded.cu", "mg.cu", "rcgmres.cu", "engine.cu"]
 HEADERS = ["kinds.cuh", "kernels.cuh", "engine.h", os.path.join("..", "..", "include", "irkg.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -646,6 +646,7 @@ void Engine::constraint_solve_slab(double sigma, const double *c, double *out, d
 void Engine::ara_jacobi_chain(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
                               int in_off, const double *zc, double cpl, double *x_out,
                               const GCtrl *skip) {
+  if (ara_chain_fused(L, alpha, dt, inner, vin, in_off, zc, cpl, x_out, skip)) return;
   const int gb = dae_grid();
   double *tbuf = zc ? tmp_t : nullptr;
   auto dst = [&](int i) { return ((inner - i) % 2 == 0) ? x_out : tmp_x; };
@@ -872,7 +873,7 @@ void Engine::dae_newton(const double *uw, double *K2, double t, double dt, irkg_
       count(1);
       if (slab())  // operator fields feed the 9-point stencils
         for (int o = 0; o < nops; ++o)
-          if (!op_zero[o]) exchange(R_OP + o, opA + (size_t)o * N, 1);
+          if (!op_zero[o]) exchange(R_OP + o, opA + (size_t)o * N, jhalo());
       stats->jacobian_assemblies += s;
       have_ops = true;
     }

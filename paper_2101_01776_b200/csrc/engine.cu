@@ -112,6 +112,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   if (const char *e = getenv("IRKG_L2_MB")) l2_budget = atoi(e) > 0 ? ((size_t)atoi(e) << 20) : 0;
   if (const char *e = getenv("IRKG_FUSED_JACOBI")) fused_jacobi = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_FUSED_JACOBI3D")) fused_jacobi3d = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_FUSED_ARA")) fused_ara = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_JSPAN")) jspan_override = atoi(e);
   if (const char *e = getenv("IRKG_PAIR_JACOBI")) pair_jacobi = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_JACOBI_SPLIT")) jacobi_split = (atoi(e) != 0);

@@ -296,6 +296,10 @@ struct Engine {
   bool jacobi_chain_fused(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
                           int in_off, const double *zc, double cpl, double *x_out,
                           const GCtrl *skip);
+  // arachain.cu (temporally blocked inner solves of the vorticity DAE; IRKG_FUSED_ARA=0: K launches)
+  bool fused_ara = true;
+  bool ara_chain_fused(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
+                       int in_off, const double *zc, double cpl, double *x_out, const GCtrl *skip);
   // jacobi3d.cu (3.5-D blocked inner solves, 3-D grids; IRKG_FUSED_JACOBI3D=0: K launches)
   bool fused_jacobi3d = true;
   bool jacobi_chain_fused3d(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
