@@ -113,6 +113,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   if (const char *e = getenv("IRKG_FUSED_JACOBI")) fused_jacobi = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_FUSED_JACOBI3D")) fused_jacobi3d = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_FUSED_ARA")) fused_ara = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_ARA_WARP")) ara_warp_form = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_JSPAN")) jspan_override = atoi(e);
   if (const char *e = getenv("IRKG_PAIR_JACOBI")) pair_jacobi = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_JACOBI_SPLIT")) jacobi_split = (atoi(e) != 0);

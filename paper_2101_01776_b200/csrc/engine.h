@@ -298,6 +298,7 @@ struct Engine {
                           const GCtrl *skip);
   // arachain.cu (temporally blocked inner solves of the vorticity DAE; IRKG_FUSED_ARA=0: K launches)
   bool fused_ara = true;
+  bool ara_warp_form = true;  // IRKG_ARA_WARP=0: the CTA-strip kernel on every grid
   bool ara_chain_fused(const Op &L, double alpha, double dt, int inner, const VecIn &vin,
                        int in_off, const double *zc, double cpl, double *x_out, const GCtrl *skip);
   // jacobi3d.cu (3.5-D blocked inner solves, 3-D grids; IRKG_FUSED_JACOBI3D=0: K launches)

@@ -91,14 +91,15 @@ def test_dae_full_size_first_step_properties():
     assert st.constraint_solves == 2 * st.newton_iterations
 
 
-@pytest.mark.parametrize("shape", [(64, 40), (300, 70), (24, 16), (258, 33)])
+@pytest.mark.parametrize("shape", [(64, 40), (300, 70), (24, 16), (258, 33), (65, 30), (301, 41)])
 @pytest.mark.parametrize("inner", [1, 2, 4, 6])
 def test_fused_arakawa_jacobi_chain_matches_oracle(shape, inner):
     """The temporally blocked inner solve of the DAE's differential operator
-    (csrc/arachain.cu: 256-column strips sliding along y, all k sweeps in one
-    pass) equals k separate damped-Jacobi sweeps of the reference
-    (src/irk_core.py:117-123) on L_u = -J(psi, .) + nu Lap; strips narrower
-    and wider than the grid, ragged bands."""
+    (csrc/arachain.cu, all k sweeps in one pass: warp strips of column pairs
+    for even nx >= 64, 256-column CTA strips otherwise) equals k separate
+    damped-Jacobi sweeps of the reference (src/irk_core.py:117-123) on
+    L_u = -J(psi, .) + nu Lap; strips narrower and wider than the grid,
+    ragged bands, odd extents."""
     prob = pk.VorticityProblem(shape, nu=2e-3)
     pd = DaeProblemDef(prob.shape, prob.nu)
     rng = np.random.default_rng(20 + inner)
