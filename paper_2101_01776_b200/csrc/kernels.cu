@@ -58,9 +58,14 @@ __global__ void k_norm2(int n, const double *__restrict__ x, double *part, int G
   __shared__ double sm[32];
   if (ctrl && ctrl->cycle_done) return;
   double acc = 0.0;
-  for (int p = blockIdx.x * BS + threadIdx.x; p < n; p += G * BS) {
-    double v = x[p];
-    acc += v * v;
+  // four loads in flight per thread; summed in the order of the plain strided loop
+  const long long st = (long long)G * BS;
+  for (long long p = blockIdx.x * BS + threadIdx.x; p < n; p += 4 * st) {
+    double v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = (p + j * st < n) ? x[p + j * st] : 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc += v[j] * v[j];
   }
   acc = block_sum<BS>(acc, sm);
   if (threadIdx.x == 0) part[blockIdx.x] = acc;
@@ -102,78 +107,89 @@ struct Vx {
   }
 };
 
-template <int V>
-__global__ void k_newton_update(int n, int s, StageConsts QR, StageConsts A, double dt,
+// S = the stage count as a template parameter: with a runtime s the register
+// arrays were sized for MAXS = 8 stages (119-128 registers: two CTAs of 256
+// threads per SM, and these passes ran at half the copy bandwidth).
+template <int V, int S>
+__global__ void k_newton_update(int n, StageConsts QR, StageConsts A, double dt,
                                 const double *__restrict__ Y, const double *__restrict__ u,
                                 double *__restrict__ K, double *__restrict__ U) {
   pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
   const int np = n / V;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < np; q += gridDim.x * blockDim.x) {
     const size_t p = (size_t)q * V;
-    double yv[MAXS][V], kv[MAXS][V], up[V];
+    double yv[S][V], kv[S][V], up[V];
 #pragma unroll
-    for (int k = 0; k < MAXS; ++k)
-      if (k < s) Vx<V>::ld(Y + (size_t)k * n + p, yv[k]);
+    for (int k = 0; k < S; ++k) Vx<V>::ld(Y + (size_t)k * n + p, yv[k]);
 #pragma unroll
-    for (int i = 0; i < MAXS; ++i) {
-      if (i < s) {
-        Vx<V>::ld(K + (size_t)i * n + p, kv[i]);
-#pragma unroll
-        for (int e = 0; e < V; ++e) {
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < MAXS; ++k)
-            if (k < s) acc += QR.a[i * MAXS + k] * yv[k][e];
-          kv[i][e] = kv[i][e] + acc;
-        }
-        Vx<V>::st(K + (size_t)i * n + p, kv[i]);
-      }
-    }
+    for (int i = 0; i < S; ++i) Vx<V>::ld(K + (size_t)i * n + p, kv[i]);
     Vx<V>::ld(u + p, up);
 #pragma unroll
-    for (int i = 0; i < MAXS; ++i) {
-      if (i < s) {
-        double o[V];
+    for (int i = 0; i < S; ++i) {
 #pragma unroll
-        for (int e = 0; e < V; ++e) {
-          double acc = 0.0;
+      for (int e = 0; e < V; ++e) {
+        double acc = 0.0;
 #pragma unroll
-          for (int j = 0; j < MAXS; ++j)
-            if (j < s) acc += A.a[i * MAXS + j] * kv[j][e];
-          o[e] = up[e] + dt * acc;
-        }
-        Vx<V>::st(U + (size_t)i * n + p, o);
+        for (int k = 0; k < S; ++k) acc += QR.a[i * MAXS + k] * yv[k][e];
+        kv[i][e] = kv[i][e] + acc;
       }
+      Vx<V>::st(K + (size_t)i * n + p, kv[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      double o[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < S; ++j) acc += A.a[i * MAXS + j] * kv[j][e];
+        o[e] = up[e] + dt * acc;
+      }
+      Vx<V>::st(U + (size_t)i * n + p, o);
     }
   }
 }
 
-template <int V>
-__global__ void k_stage_values(int n, int s, const double *__restrict__ u,
-                               const double *__restrict__ K, StageConsts A, double dt,
-                               double *__restrict__ U) {
+// UNR consecutive 32-point chunks per warp and trip: at small S a thread
+// otherwise has only S loads in flight
+template <int V, int S, int UNR>
+__global__ void k_stage_values(int n, const double *__restrict__ u, const double *__restrict__ K,
+                               StageConsts A, double dt, double *__restrict__ U) {
   pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
   const int np = n / V;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < np; q += gridDim.x * blockDim.x) {
-    const size_t p = (size_t)q * V;
-    double kv[MAXS][V], up[V];
+  const int lane = threadIdx.x & 31;
+  const int wst = (gridDim.x * blockDim.x) >> 5;
+  for (int c0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * UNR; c0 * 32 < np;
+       c0 += UNR * wst) {
+    const int q0 = c0 * 32 + lane;
+    double kv[UNR][S][V], up[UNR][V];
 #pragma unroll
-    for (int j = 0; j < MAXS; ++j)
-      if (j < s) Vx<V>::ld(K + (size_t)j * n + p, kv[j]);
-    Vx<V>::ld(u + p, up);
+    for (int r = 0; r < UNR; ++r) {
+      const int q = q0 + r * 32;
+      if (q < np) {
+        const size_t p = (size_t)q * V;
 #pragma unroll
-    for (int i = 0; i < MAXS; ++i) {
-      if (i < s) {
-        double o[V];
+        for (int j = 0; j < S; ++j) Vx<V>::ld(K + (size_t)j * n + p, kv[r][j]);
+        Vx<V>::ld(u + p, up[r]);
+      }
+    }
 #pragma unroll
-        for (int e = 0; e < V; ++e) {
-          double acc = 0.0;
+    for (int r = 0; r < UNR; ++r) {
+      const int q = q0 + r * 32;
+      if (q < np) {
+        const size_t p = (size_t)q * V;
 #pragma unroll
-          for (int j = 0; j < MAXS; ++j)
-            if (j < s) acc += A.a[i * MAXS + j] * kv[j][e];
-          o[e] = up[e] + dt * acc;
+        for (int i = 0; i < S; ++i) {
+          double o[V];
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < S; ++j) acc += A.a[i * MAXS + j] * kv[r][j][e];
+            o[e] = up[r][e] + dt * acc;
+          }
+          Vx<V>::st(U + (size_t)i * n + p, o);
         }
-        Vx<V>::st(U + (size_t)i * n + p, o);
       }
     }
   }
@@ -239,31 +255,43 @@ __global__ void k_opfields(int n, KindParams kp, OpWeights W, const double *__re
 
 // out_i = sum_k M[i][k] in_k  (pointwise s x s mix; g = Q^T F, dk = (Q R0) y)
 // mode 0: out = M in; mode 1: out += M in (Newton update K += dk)
-template <int V>
-__global__ void k_stage_mix(int n, int s, StageConsts M, const double *__restrict__ in,
+template <int V, int S, int UNR>
+__global__ void k_stage_mix(int n, StageConsts M, const double *__restrict__ in,
                             double *__restrict__ out, int accumulate) {
   pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
   const int np = n / V;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < np; q += gridDim.x * blockDim.x) {
-    const size_t p = (size_t)q * V;
-    double v[MAXS][V];
+  const int lane = threadIdx.x & 31;
+  const int wst = (gridDim.x * blockDim.x) >> 5;
+  for (int c0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * UNR; c0 * 32 < np;
+       c0 += UNR * wst) {
+    const int q0 = c0 * 32 + lane;
+    double v[UNR][S][V];
 #pragma unroll
-    for (int k = 0; k < MAXS; ++k)
-      if (k < s) Vx<V>::ld(in + (size_t)k * n + p, v[k]);
+    for (int r = 0; r < UNR; ++r) {
+      const int q = q0 + r * 32;
+      if (q < np) {
 #pragma unroll
-    for (int i = 0; i < MAXS; ++i) {
-      if (i < s) {
-        double o[V];
-        if (accumulate) Vx<V>::ld(out + (size_t)i * n + p, o);
+        for (int k = 0; k < S; ++k) Vx<V>::ld(in + (size_t)k * n + (size_t)q * V, v[r][k]);
+      }
+    }
 #pragma unroll
-        for (int e = 0; e < V; ++e) {
-          double acc = 0.0;
+    for (int r = 0; r < UNR; ++r) {
+      const int q = q0 + r * 32;
+      if (q < np) {
+        const size_t p = (size_t)q * V;
 #pragma unroll
-          for (int k = 0; k < MAXS; ++k)
-            if (k < s) acc += M.a[i * MAXS + k] * v[k][e];
-          o[e] = accumulate ? o[e] + acc : acc;
+        for (int i = 0; i < S; ++i) {
+          double o[V];
+          if (accumulate) Vx<V>::ld(out + (size_t)i * n + p, o);
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < S; ++k) acc += M.a[i * MAXS + k] * v[r][k][e];
+            o[e] = accumulate ? o[e] + acc : acc;
+          }
+          Vx<V>::st(out + (size_t)i * n + p, o);
         }
-        Vx<V>::st(out + (size_t)i * n + p, o);
       }
     }
   }
@@ -517,10 +545,28 @@ __global__ void k_vcombine(int n, const double *__restrict__ V, long long pitch,
   }
 }
 
+// y += a x; V values per access, 4 accesses of each vector in flight per thread
+template <int V>
 __global__ void k_axpy(int n, double a, const double *__restrict__ x, double *__restrict__ y) {
   pdl_wait();  // (PDL launch; no early trigger: a bandwidth kernel keeps its SMs)
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
-    y[r] = y[r] + a * x[r];
+  const int np = n / V;
+  const int st = gridDim.x * blockDim.x;
+  for (int q0 = blockIdx.x * blockDim.x + threadIdx.x; q0 < np; q0 += 4 * st) {
+    double xv[4][V], yv[4][V];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (q0 + r * st < np) {
+        Vx<V>::ld(x + (size_t)(q0 + r * st) * V, xv[r]);
+        Vx<V>::ld(y + (size_t)(q0 + r * st) * V, yv[r]);
+      }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (q0 + r * st < np) {
+#pragma unroll
+        for (int e = 0; e < V; ++e) yv[r][e] = yv[r][e] + a * xv[r][e];
+        Vx<V>::st(y + (size_t)(q0 + r * st) * V, yv[r]);
+      }
+  }
 }
 
 // True residual bookkeeping after x += Z y (src/sparsela.py:263-272).
@@ -563,6 +609,21 @@ static void dispatch_kd(int kind, int ndim, F f) {
 
 // pair (double2) path of the stage-space kernels: even row length and
 // 16-byte-aligned stage rows
+// the stage count as a compile-time constant (register arrays of exactly s rows)
+template <class F>
+static void dispatch_stages(int s, F f) {
+  switch (s) {
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 3: f(std::integral_constant<int, 3>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 5: f(std::integral_constant<int, 5>{}); break;
+    case 6: f(std::integral_constant<int, 6>{}); break;
+    case 7: f(std::integral_constant<int, 7>{}); break;
+    default: f(std::integral_constant<int, 8>{}); break;
+  }
+}
+
 static bool pair_ok(long long n, const void *a, const void *b, const void *c, const void *d) {
   auto al = [](const void *p) { return ((uintptr_t)p & 15u) == 0; };
   return n % 2 == 0 && al(a) && al(b) && al(c) && al(d);
@@ -601,12 +662,16 @@ void Engine::newton_update(const double *QR_rowmajor_s, double dt, const double 
       QR.a[i * MAXS + j] = QR_rowmajor_s[i * s + j];
       A.a[i * MAXS + j] = tab.a0[i * IRKG_MAX_STAGES + j];
     }
-  if (pair_ok(N, Yv, u, K, Uo))
-    launch_pdl(k_newton_update<2>, dim3(grid_for(N / 2)), dim3(256), 0, (int)N, s, QR, A, dt, Yv, u,
-               K, Uo);
-  else
-    launch_pdl(k_newton_update<1>, dim3(grid_for(N)), dim3(256), 0, (int)N, s, QR, A, dt, Yv, u, K,
-               Uo);
+  const bool pair = pair_ok(N, Yv, u, K, Uo);
+  dispatch_stages(s, [&](auto SC) {
+    constexpr int S_ = decltype(SC)::value;
+    if (pair)
+      launch_pdl(k_newton_update<2, S_>, dim3(grid_for(N / 2)), dim3(256), 0, (int)N, QR, A, dt, Yv,
+                 u, K, Uo);
+    else
+      launch_pdl(k_newton_update<1, S_>, dim3(grid_for(N)), dim3(256), 0, (int)N, QR, A, dt, Yv, u,
+                 K, Uo);
+  });
   count(1);
 }
 
@@ -627,10 +692,17 @@ void Engine::stage_values_n(const double *u, const double *K, double dt, double 
   A.s = s;
   for (int i = 0; i < s; ++i)
     for (int j = 0; j < s; ++j) A.a[i * MAXS + j] = tab.a0[i * IRKG_MAX_STAGES + j];
-  if (pair_ok(n, u, K, Uo, Uo))
-    launch_pdl(k_stage_values<2>, dim3(grid_for(n / 2)), dim3(256), 0, (int)n, s, u, K, A, dt, Uo);
-  else
-    launch_pdl(k_stage_values<1>, dim3(grid_for(n)), dim3(256), 0, (int)n, s, u, K, A, dt, Uo);
+  const bool pair = pair_ok(n, u, K, Uo, Uo);
+  dispatch_stages(s, [&](auto SC) {
+    constexpr int S_ = decltype(SC)::value;
+    constexpr int UNR = S_ <= 2 ? 4 : (S_ <= 4 ? 2 : 1);
+    if (pair)
+      launch_pdl(k_stage_values<2, S_, UNR>, dim3(grid_for(n / 2)), dim3(256), 0, (int)n, u, K, A,
+                 dt, Uo);
+    else
+      launch_pdl(k_stage_values<1, S_, UNR>, dim3(grid_for(n)), dim3(256), 0, (int)n, u, K, A, dt,
+                 Uo);
+  });
   count(1);
 }
 
@@ -665,12 +737,17 @@ void Engine::stage_mix_n(const double *M_rowmajor_s, const double *in, double *o
   M.s = s;
   for (int i = 0; i < s; ++i)
     for (int k = 0; k < s; ++k) M.a[i * MAXS + k] = M_rowmajor_s[i * s + k];
-  if (pair_ok(n, in, out, out, out))
-    launch_pdl(k_stage_mix<2>, dim3(grid_for(n / 2)), dim3(256), 0, (int)n, s, M, in, out,
-               accumulate ? 1 : 0);
-  else
-    launch_pdl(k_stage_mix<1>, dim3(grid_for(n)), dim3(256), 0, (int)n, s, M, in, out,
-               accumulate ? 1 : 0);
+  const bool pair = pair_ok(n, in, out, out, out);
+  dispatch_stages(s, [&](auto SC) {
+    constexpr int S_ = decltype(SC)::value;
+    constexpr int UNR = S_ <= 2 ? 4 : (S_ <= 4 ? 2 : 1);
+    if (pair)
+      launch_pdl(k_stage_mix<2, S_, UNR>, dim3(grid_for(n / 2)), dim3(256), 0, (int)n, M, in, out,
+                 accumulate ? 1 : 0);
+    else
+      launch_pdl(k_stage_mix<1, S_, UNR>, dim3(grid_for(n)), dim3(256), 0, (int)n, M, in, out,
+                 accumulate ? 1 : 0);
+  });
   count(1);
 }
 
@@ -828,7 +905,10 @@ void Engine::vcombine(long long n, const double *coef, double *out) {
   count(1);
 }
 void Engine::axpy(long long n, double a, const double *x, double *y) {
-  launch_pdl(k_axpy, dim3(grid_for(n)), dim3(256), 0, (int)n, a, x, y);
+  if (pair_ok(n, x, y, y, y))
+    launch_pdl(k_axpy<2>, dim3(grid_for(n / 2)), dim3(256), 0, (int)n, a, x, y);
+  else
+    launch_pdl(k_axpy<1>, dim3(grid_for(n)), dim3(256), 0, (int)n, a, x, y);
   count(1);
 }
 void Engine::cycle_end() {
