@@ -156,9 +156,28 @@ constexpr int DBS = 256;
 
 }  // namespace
 
-#define ROWS_LOOP(g)                                                  \
-  for (int iy = blockIdx.x; iy < (g).ny; iy += gridDim.x)             \
-    for (int ix = threadIdx.x; ix < (g).nx; ix += blockDim.x)
+// Traversal of the 9-point kernels: the grid is cut into column strips of DBS
+// points and bands of rows; a CTA walks its band row by row with one column
+// per thread, so rows iy-1, iy, iy+1 of its strip stay in L1 and a 9-point
+// load misses once per field and point.  (One grid row per CTA trip made every
+// input row cross L2 -> SM three times, for three different CTAs.)
+struct RowsIter {
+  int strips, bands, rows;  // rows per band
+};
+__device__ __forceinline__ RowsIter rows_iter(const Grid &g) {
+  RowsIter r;
+  r.strips = (g.nx + DBS - 1) / DBS;
+  r.bands = max(1, min(g.ny, (int)gridDim.x / r.strips));
+  r.rows = (g.ny + r.bands - 1) / r.bands;
+  return r;
+}
+#define ROWS_LOOP(g)                                                                       \
+  for (int sb_ = blockIdx.x, ns_ = rows_iter(g).strips, nr_ = rows_iter(g).rows,           \
+           nt_ = rows_iter(g).strips * rows_iter(g).bands;                                 \
+       sb_ < nt_; sb_ += gridDim.x)                                                        \
+    for (int ix = (sb_ % ns_) * DBS + threadIdx.x, iy = (sb_ / ns_) * nr_,                 \
+             ye_ = min((g).ny, (sb_ / ns_ + 1) * nr_);                                     \
+         iy < ye_ && ix < (g).nx; ++iy)
 
 // stage fields U_i, W_i (rows of UW) with their ghost planes
 struct DaeStageRefs {

@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--top", type=int, default=15)
+    ap.add_argument("--steps", type=int, default=1, help="steps inside the profiled region")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -44,7 +45,8 @@ def main():
     adv(0.0)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        st = adv(spec.dt)
+        for k in range(args.steps):
+            st = adv((k + 1) * spec.dt)
         torch.cuda.synchronize()
     ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
     ev.sort(key=lambda e: e.time_range.start)
