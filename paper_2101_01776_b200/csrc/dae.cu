@@ -156,11 +156,17 @@ constexpr int DBS = 256;
 
 }  // namespace
 
-// Traversal of the 9-point kernels: the grid is cut into column strips of DBS
-// points and bands of rows; a CTA walks its band row by row with one column
-// per thread, so rows iy-1, iy, iy+1 of its strip stay in L1 and a 9-point
-// load misses once per field and point.  (One grid row per CTA trip made every
-// input row cross L2 -> SM three times, for three different CTAs.)
+// Traversals of the 9-point kernels.  ROWS_LOOP: one grid row per CTA trip.
+// STRIP_LOOP: column strips of DBS points x bands of rows, a CTA walking its
+// band row by row with one column per thread, so rows iy-1, iy, iy+1 of its
+// strip stay in L1.  Measured at 2048^2 (profiles/r2s4_cfg4_traversal_ab.txt):
+// the strips help the stage residual (few fields live per strip: 164 -> 97 us)
+// and hurt the 2x2 block operator (six fields: 78 -> 111 us) -- each kernel
+// keeps the traversal that is faster for it.
+#define ROWS_LOOP(g)                                                  \
+  for (int iy = blockIdx.x; iy < (g).ny; iy += gridDim.x)             \
+    for (int ix = threadIdx.x; ix < (g).nx; ix += blockDim.x)
+
 struct RowsIter {
   int strips, bands, rows;  // rows per band
 };
@@ -171,7 +177,7 @@ __device__ __forceinline__ RowsIter rows_iter(const Grid &g) {
   r.rows = (g.ny + r.bands - 1) / r.bands;
   return r;
 }
-#define ROWS_LOOP(g)                                                                       \
+#define STRIP_LOOP(g)                                                                      \
   for (int sb_ = blockIdx.x, ns_ = rows_iter(g).strips, nr_ = rows_iter(g).rows,           \
            nt_ = rows_iter(g).strips * rows_iter(g).bands;                                 \
        sb_ < nt_; sb_ += gridDim.x)                                                        \
@@ -190,7 +196,7 @@ __global__ void k_dae_residual(Grid g, double nu, double h2, int s, DaeStageRefs
                                double *part, unsigned *counter, double *out) {
   const int n = g.n;
   double acc = 0.0;
-  ROWS_LOOP(g) {
+  STRIP_LOOP(g) {
     const int p = iy * g.nx + ix;
     const XO o = xo_of(g, ix);
     for (int i = 0; i < s; ++i) {
