@@ -83,7 +83,7 @@ void Engine::dirk_step(double *u, double t, double dt, irkg_step_stats *stats) {
         throw SolveError(IRKG_ERR_STEP_FAILURE, msg);
       }
       opfields(U, w1, opA);  // L at the current stage value
-      if (slab()) exchange(R_OP, opA, jhalo());
+      if (slab()) exchange(R_OP, opA, inhalo());
       stats->jacobian_assemblies += 1;
       BlockSpec B{};
       B.size = 1;

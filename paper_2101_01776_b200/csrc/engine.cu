@@ -129,6 +129,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   // (profiles/r2_slab_probe_overlap.txt: 1.41x -> 1.73x of the plain path)
   halo_overlap = nranks > 1;
   if (const char *e = getenv("IRKG_HALO_OVERLAP")) halo_overlap = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_EXT_HALO")) ext_halo = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_BOP_WPS")) bop_wps = atoi(e) > 0 ? atoi(e) : 8;
   for (int i = 0; i < MAXS; ++i)
     for (int j = 0; j < MAXS; ++j) od_slot[i][j] = -1;
@@ -349,7 +350,9 @@ void Engine::arnoldi_iteration_slab(const BlockSpec &B, long long n, int j_host)
     if (timing) check(cudaEventRecord(ev1, stream));
     return;
   }
-  const int H = jhalo();
+  const bool ext = ext_halo_ok() && B.inner == cfg.inner;
+  const int K1 = jhalo();              // stencil reach of one chain
+  const int H = ext ? inhalo() : K1;   // depth of the v_j halo
   const long long P = plane_size();
   const int nl = local_planes();
   const int halves = B.size;
@@ -371,7 +374,50 @@ void Engine::arnoldi_iteration_slab(const BlockSpec &B, long long n, int j_host)
   }
   counters.halo_exchanges += halves;
   const bool ovl = overlap_ok();
-  if (!ovl) {
+  cudaStream_t main = stream;
+  auto on_comm = [&](auto &&f) {  // exchange() / halo_batch enqueue on `stream`
+    stream = comm_stream;
+    f();
+    stream = main;
+  };
+  // every halo goes out on comm_stream while the bands that read no ghost
+  // plane run; the edge bands follow the join (one split per stencil)
+  auto overlapped = [&](auto &&send, auto &&compute) {
+    fork_comm();
+    send();
+    band_sel = 1;
+    compute();
+    join_comm();
+    band_sel = 2;
+    compute();
+    band_sel = 0;
+  };
+  if (ext) {
+    // communication-avoiding step: one halo round (v_j, depth 2(K-1)+1); the
+    // chains compute the ghost rows of z1 (K rows: chain 2's reach + the
+    // operator's) and z2 (1 row) themselves, so neither needs an exchange
+    auto chain1 = [&] {
+      chain_ext = B.size == 2 ? K1 + 1 : 1;
+      chain_out_role = R_Z0;
+      jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vslot, 0, nullptr, 0.0, zbuf, ctrl_dev);
+      chain_ext = 0;
+    };
+    if (ovl)
+      overlapped([&] { on_comm([&] { comm->halo_batch(halves, xf, stream); }); }, chain1);
+    else {
+      comm->halo_batch(halves, xf, stream);
+      chain1();
+    }
+    if (B.size == 2) {
+      chain_ext = 1;
+      chain_out_role = R_Z1;
+      jacobi_chain(B.l2, B.gamma, B.dt, B.inner, &vslot, (int)N, zbuf, B.beta * B.beta / B.phi,
+                   zbuf + N, ctrl_dev);
+      chain_ext = 0;
+    }
+    counters.op_bytes += 8.0 * N * B.size * 3.0;
+    block_op_s(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev);
+  } else if (!ovl) {
     comm->halo_batch(halves, xf, stream);
     jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vslot, 0, nullptr, 0.0, zbuf, ctrl_dev);
     if (B.size == 2) {
@@ -385,24 +431,6 @@ void Engine::arnoldi_iteration_slab(const BlockSpec &B, long long n, int j_host)
     counters.op_bytes += 8.0 * N * B.size * 3.0;
     block_op_s(B, zbuf, wbuf, nullptr, nullptr, ctrl_dev);
   } else {
-    // every halo goes out on comm_stream while the bands that read no ghost
-    // plane run; the edge bands follow the join (one split per stencil)
-    auto overlapped = [&](auto &&send, auto &&compute) {
-      fork_comm();
-      send();
-      band_sel = 1;
-      compute();
-      join_comm();
-      band_sel = 2;
-      compute();
-      band_sel = 0;
-    };
-    cudaStream_t main = stream;
-    auto on_comm = [&](auto &&f) {  // exchange() / halo_batch enqueue on `stream`
-      stream = comm_stream;
-      f();
-      stream = main;
-    };
     overlapped([&] { on_comm([&] { comm->halo_batch(halves, xf, stream); }); },
                [&] { jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vslot, 0, nullptr, 0.0, zbuf,
                                   ctrl_dev); });
@@ -429,6 +457,15 @@ void Engine::arnoldi_iteration_slab(const BlockSpec &B, long long n, int j_host)
 bool Engine::overlap_ok() const {
   return halo_overlap && slab() && comm->capturable() && ndim == 2 && fused_jacobi &&
          pair_jacobi && jacobi_split && strip_op && grid.nx % 2 == 0 && grid.nx >= 64;
+}
+
+// The 2-D fused chain can compute the ghost rows of its result itself
+// (jacobi.cu, chain_ext) when the deeper input halo fits the ghost buffers.
+bool Engine::ext_halo_ok() const {
+  return ext_halo && slab() && ndim == 2 && prob.kind != KIND_ARAKAWA && fused_jacobi &&
+         pair_jacobi && jacobi_split && grid.nx % 2 == 0 && grid.nx >= 64 && cfg.inner >= 1 &&
+         cfg.inner <= 6 && 2 * (cfg.inner - 1) + 1 <= GH && grid.ny >= 2 * (cfg.inner - 1) + 1 &&
+         grid.ny >= 2 * cfg.inner;
 }
 
 void Engine::fork_comm() {
@@ -477,7 +514,7 @@ void Engine::drop_graphs() {
 Engine::CycleGraph &Engine::cycle_graph(const BlockSpec &B, long long n, bool loop) {
   char key[512];
   snprintf(key, sizeof key, "%c%d|%d|%a|%a|%a|%a|%a|%d|%p|%a|%d|%p|%a|%d|%p|%a|%d|%p|%a|%d|%lld|%p|%d",
-           loop ? 'W' : 'S', loop ? graph_unroll : 1, B.size, B.eta, B.beta, B.phi, B.gamma, B.dt, B.inner,
+           loop ? 'W' : 'S', loop ? graph_unroll : slab_batch, B.size, B.eta, B.beta, B.phi, B.gamma, B.dt, B.inner,
            (const void *)B.l1.a, B.l1.sigma, B.l1.present, (const void *)B.l2.a, B.l2.sigma,
            B.l2.present, (const void *)B.c12.a, B.c12.sigma, B.c12.present,
            (const void *)B.c21.a, B.c21.sigma, B.c21.present, n, (void *)V, vcap);
@@ -513,7 +550,7 @@ Engine::CycleGraph &Engine::cycle_graph(const BlockSpec &B, long long n, bool lo
     // the WHILE body holds `graph_unroll` Arnoldi steps: the conditional
     // re-launch of the body costs several us per trip, and a step after the
     // exit test fired is inert (every kernel checks cycle_done)
-    for (int u = 0; u < (loop ? graph_unroll : 1); ++u) arnoldi_iteration(B, n);
+    for (int u = 0; u < (loop ? graph_unroll : slab_batch); ++u) arnoldi_iteration(B, n);
   } catch (...) {
     cond_active = false;
     stream = saved;
@@ -581,20 +618,20 @@ KrylovOut Engine::gmres(const BlockSpec &B, const double *rhs, double *x, double
       // step is one graph launch (captured NCCL halos + all-reduces)
       const bool g1 = use_graphs && !timing && comm->capturable() && prob.kind != KIND_ARAKAWA;
       if (g1) {
-        // steps go out in batches without a host round trip in between; a
-        // step launched after the exit test fired is inert (every kernel
-        // checks cycle_done; the NCCL rounds move stale, unused values)
+        // one graph launch = slab_batch steps, no host round trip in between; a
+        // step after the exit test fired (or past the cycle length: the column
+        // finish sets cycle_done at j + 1 >= m) is inert -- every kernel checks
+        // cycle_done, the NCCL rounds move stale, unused values
         CycleGraph &cg = cycle_graph(B, n, false);
         int launched = 0;
         while (launched < m) {
-          const int b = std::min(slab_batch, m - launched);
-          for (int k = 0; k < b; ++k) check(cudaGraphLaunch(cg.ex, stream), "cudaGraphLaunch");
-          launched += b;
+          check(cudaGraphLaunch(cg.ex, stream), "cudaGraphLaunch");
+          launched += slab_batch;
           read_ctrl();
           if (ctrl_host->cycle_done) break;
         }
         const int its = ctrl_host->j + 1;
-        counters.kernel_launches += (long long)cg.body_kernels * launched;
+        counters.kernel_launches += (long long)cg.body_kernels * (launched / slab_batch);
         counters.cgs_launches += 3LL * its;
         counters.arnoldi_iterations += its;
       }
@@ -714,7 +751,7 @@ void Engine::build_linearization(const double *Ust) {
   opfields(Ust, weights, opA);
   if (slab())  // operator fields feed stencils (fused Jacobi halo: K-1 planes)
     for (int o = 0; o < nops; ++o)
-      if (!op_zero[o]) exchange(R_OP + o, opA + (size_t)o * N, jhalo());
+      if (!op_zero[o]) exchange(R_OP + o, opA + (size_t)o * N, inhalo());
 }
 
 void Engine::build_weights() {
@@ -835,7 +872,7 @@ void Engine::set_variant_jacobian(const irkg_opfield *diag, int n_off, const int
   }
   if (slab())
     for (int o = 0; o < nops; ++o)
-      if (!op_zero[o]) exchange(R_OP + o, opA + (size_t)o * N, jhalo());
+      if (!op_zero[o]) exchange(R_OP + o, opA + (size_t)o * N, inhalo());
 }
 
 // N(u) for one state (OdeSystem.rhs): the stage residual kernel with one

@@ -203,6 +203,9 @@ struct Engine {
   StageGhosts stage_ghosts(const double *Ub, long long stride, int nst = -1) const;
   void free_ghosts();
   int jhalo() const { return cfg.inner > 1 ? cfg.inner - 1 : 1; }
+  // halo depth of the inner solves' inputs (v_j, operator fields): K-1, or 2(K-1)+1 when
+  // the chains compute their results' ghost rows themselves (ext_halo_ok)
+  int inhalo() const { return ext_halo_ok() ? 2 * (cfg.inner - 1) + 1 : jhalo(); }
 
   Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_ = 0, int nranks_ = 1,
          Comm *comm_ = nullptr, bool force_slab = false);
@@ -379,12 +382,20 @@ struct Engine {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // bands [lo, hi) of nb bands of `span` rows (local ny) read only local rows
   // when the stencil reaches h rows beyond the band
-  void interior_bands(int nb, int span, int h, int &lo, int &hi) const {
+  // (bands start at row ylo <= 0 when the chain also computes ghost rows)
+  void interior_bands(int nb, int span, int h, int &lo, int &hi, int ylo = 0) const {
     lo = 0;
-    while (lo < nb && lo * span < h) ++lo;
+    while (lo < nb && ylo + lo * span < h) ++lo;
     hi = nb;
-    while (hi > lo && std::min(grid.ny, hi * span) + h > grid.ny) --hi;
+    while (hi > lo && ylo + hi * span + h > grid.ny) --hi;
   }
+  // Extended-halo chains (slab mode, 2-D fused chain): a chain also computes
+  // chain_ext rows beyond the slab on either side, from a deeper halo of its
+  // input, into the ghost planes of role chain_out_role -- the Arnoldi step
+  // then exchanges only v_j (depth 2(K-1)+1) instead of v_j, z1 and z2
+  int chain_ext = 0, chain_out_role = 0;
+  bool ext_halo = true;  // IRKG_EXT_HALO=0: exchange z1 / z2 instead
+  bool ext_halo_ok() const;
   bool overlap_ok() const;  // the slab step can split its stencils
   void fork_comm();
   void join_comm();  // counted in the per-device persisting-limit refcount

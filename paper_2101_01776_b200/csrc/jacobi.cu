@@ -433,7 +433,8 @@ template <int KIND, int K, bool SLAB>
 __global__ void __launch_bounds__(JSPW * 32, 12 / JSPW)
     k_jacobi_sp2d(Grid g, Op L, JacCoef jc, VecIn vin, int in_off, FRef zcr, double cpl,
                   double *__restrict__ x_out, int span, int strips, int nwarps, int band0,
-                  GCtrl *flag_ctrl, const GCtrl *skip) {
+                  GCtrl *flag_ctrl, const GCtrl *skip, int ylo, int yhi, double *out_lo,
+                  double *out_hi) {
   constexpr int H = K - 1;
   constexpr int HS = (H + 1) & ~1;
   constexpr int WC = 64 - 2 * HS;
@@ -454,8 +455,12 @@ __global__ void __launch_bounds__(JSPW * 32, 12 / JSPW)
   int c0 = x0 - HS + li;
   c0 = c0 < 0 ? c0 + nx : (c0 >= nx ? c0 - nx : c0);
   const bool valid = li >= HS && li < 64 - HS && x0 - HS + li < nx;
-  const int y0 = band * span;
-  const int y1 = min(ny, y0 + span);
+  // output rows [ylo, yhi): the local rows [0, ny), or (slab mode, extended
+  // halo) E rows beyond them on either side, computed redundantly from a
+  // deeper halo of the input and stored into the output's ghost planes -- the
+  // consumer then needs no halo exchange of this chain's result
+  const int y0 = ylo + band * span;
+  const int y1 = min(yhi, y0 + span);
 
   // sliding windows (index K-1 / 2 = newest row)
   double AW[K][2];      // a, rows t-K+1 .. t
@@ -632,8 +637,16 @@ __global__ void __launch_bounds__(JSPW * 32, 12 / JSPW)
       }
     }
     const int yo = t - H;
-    if (valid && yo >= y0 && yo < y1)
-      *reinterpret_cast<double2 *>(x_out + (size_t)yo * nx + c0) = make_double2(xn[0], xn[1]);
+    if (valid && yo >= y0 && yo < y1) {
+      double *orow;
+      if (!SLAB || (yo >= 0 && yo < ny))
+        orow = x_out + (size_t)yo * nx;
+      else if (yo < 0)
+        orow = out_lo + (size_t)(GH + yo) * nx;
+      else
+        orow = out_hi + (size_t)(yo - ny) * nx;
+      *reinterpret_cast<double2 *>(orow + c0) = make_double2(xn[0], xn[1]);
+    }
   };
   for (int tg = t0; tg < t1; tg += JRING) {
 #pragma unroll
@@ -679,7 +692,22 @@ bool Engine::jacobi_chain_fused(const Op &L, double alpha, double dt, int inner,
     }
     if (jspan_override > 0) span = jspan_override;
     if (span > grid.ny) span = grid.ny;
-    const int nb = (grid.ny + span - 1) / span;
+    // slab mode, extended halo: E rows beyond the slab on either side (chain_ext)
+    const int E = (grid.slab && jacobi_split) ? chain_ext : 0;
+    const int ylo = -E, yhi = grid.ny + E;
+    double *out_lo = nullptr, *out_hi = nullptr;
+    if (E > 0) {
+      Ghost &og = role(chain_out_role);
+      if (og.field && og.field != x_out) {
+        auto it = owner.find(og.field);
+        if (it != owner.end() && it->second == chain_out_role) owner.erase(it);
+      }
+      og.field = x_out;
+      owner[x_out] = chain_out_role;
+      out_lo = og.lo;
+      out_hi = og.hi;
+    }
+    const int nb = (grid.ny + 2 * E + span - 1) / span;
     const int nwarps = strips * nb;
     const int blocks = (nwarps + JPW - 1) / JPW;
     // band ranges to launch: all, or (slab halo overlap, band_sel) the
@@ -687,7 +715,7 @@ bool Engine::jacobi_chain_fused(const Op &L, double alpha, double dt, int inner,
     int br[2][2] = {{0, nb}, {0, 0}};
     if (band_sel != 0) {
       int lo, hi;
-      interior_bands(nb, span, inner - 1, lo, hi);
+      interior_bands(nb, span, inner - 1, lo, hi, ylo);
       if (band_sel == 1) {
         br[0][0] = lo;
         br[0][1] = hi;
@@ -749,7 +777,7 @@ bool Engine::jacobi_chain_fused(const Op &L, double alpha, double dt, int inner,
           launch_pdl(kfn, dim3((nw + JSPW - 1) / JSPW), dim3(JSPW * 32),
                      (size_t)JSPW * JRING * 3 * 64 * sizeof(double), grid, Lr, jc, vin, in_off,
                      zc ? ref(zc) : FRef{nullptr, nullptr, nullptr}, cpl, x_out, span, strips,
-                     nw, br[r][0], ctrl_dev, skip);
+                     nw, br[r][0], ctrl_dev, skip, ylo, yhi, out_lo, out_hi);
         }
       };
       if (grid.slab)

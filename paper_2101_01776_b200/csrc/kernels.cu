@@ -829,11 +829,12 @@ void Engine::precond(const BlockSpec &B, const void *vin_p, double *z, const GCt
     precond_mg(B, vin, z, skip);
     return;
   }
+  const bool ext = ext_halo_ok() && B.inner == cfg.inner;
   if (slab()) {
     // the input must be a fixed pointer here (the multi-rank loop resolves
     // slot j on the host); exchange the halves' boundary planes
     if (vin.ctrl) throw SolveError(IRKG_ERR_CONFIG, "internal: slot-indexed input in slab mode");
-    const int H = jhalo();
+    const int H = ext ? inhalo() : jhalo();
     exchange(R_VIN0, vin.base, H);
     vin.lo[0] = role(R_VIN0).lo;
     vin.hi[0] = role(R_VIN0).hi;
@@ -842,6 +843,20 @@ void Engine::precond(const BlockSpec &B, const void *vin_p, double *z, const GCt
       vin.lo[1] = role(R_VIN1).lo;
       vin.hi[1] = role(R_VIN1).hi;
     }
+  }
+  if (ext) {
+    // the chains compute the ghost rows of z1 / z2 themselves (see arnoldi_iteration_slab)
+    chain_ext = B.size == 2 ? jhalo() + 1 : 1;
+    chain_out_role = R_Z0;
+    jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vin, 0, nullptr, 0.0, z, skip);
+    if (B.size == 2) {
+      chain_ext = 1;
+      chain_out_role = R_Z1;
+      jacobi_chain(B.l2, B.gamma, B.dt, B.inner, &vin, (int)N, z, B.beta * B.beta / B.phi, z + N,
+                   skip);
+    }
+    chain_ext = 0;
+    return;
   }
   if (B.size == 1) {
     jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vin, 0, nullptr, 0.0, z, skip);

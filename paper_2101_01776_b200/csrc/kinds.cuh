@@ -56,8 +56,9 @@ struct Grid {
   int pin;         // 1: this rank holds global point 0 (the DAE constraint's pinned row)
 };
 
-// Depth of the ghost-plane buffers (>= Jacobi halo K-1 for K <= 6, and 1).
-constexpr int GH = 6;
+// Depth of the ghost-plane buffers (>= Jacobi halo K-1 for K <= 6, and the
+// extended halo 2(K-1)+1 of the communication-avoiding 2-D chains for K <= 4).
+constexpr int GH = 8;
 
 // A field and its ghost planes along the slab (slowest) axis.  In slab mode
 // plane -d (1 <= d <= GH) is lo + (GH - d) * P and plane nl + e is hi + e * P;

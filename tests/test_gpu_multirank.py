@@ -43,6 +43,11 @@ def _run(tmp_path, nproc, *args, env=None):
          "--dt", "2e-4"]),
     (3, ["--kind", "nldiff", "--shape", "16,14,24", "--family", "gauss", "--stages", "2",
          "--dt", "1e-3"]),
+    # nx >= 64: the communication-avoiding step (one v_j halo of depth 2(K-1)+1, the chains
+    # compute the ghost rows of z1 / z2 themselves); ragged slabs of 17 / 17 / 16 rows
+    (3, ["--kind", "burgers", "--shape", "64,50", "--family", "gauss", "--stages", "3"]),
+    (3, ["--kind", "nldiff", "--shape", "96,50", "--family", "radau_iia", "--stages", "2",
+         "--dt", "2e-4"]),
     # in-plane extents >= 32: the 3.5-D blocked chain (csrc/jacobi3d.cu) on z-slabs with ghost planes
     (2, ["--kind", "nldiff", "--shape", "32,34,16", "--family", "gauss", "--stages", "2",
          "--dt", "1e-3"]),
@@ -71,6 +76,15 @@ def test_nccl_transport_single_gpu_ring(tmp_path):
     assert r["rel"] <= 1e-12, r
     assert [s[0] for s in r["stats"]] == [s[0] for s in r["single_stats"]]
     assert r["halos"] > 0
+
+
+def test_slab_step_with_exchanged_z_halos_matches(tmp_path):
+    """IRKG_EXT_HALO=0: the step that exchanges the halos of z1 and z2 instead of
+    computing their ghost rows (the path 3-D grids and narrow 2-D grids take)."""
+    r = _run(tmp_path, 2, "--kind", "burgers", "--shape", "64,64", "--family", "gauss",
+             "--stages", "3", env={"IRKG_EXT_HALO": "0"})
+    assert r["rel"] <= 1e-12, r
+    assert all(abs(a[1] - b[1]) <= 1 for a, b in zip(r["stats"], r["single_stats"]))
 
 
 def test_nccl_ring_with_halo_overlap_matches(tmp_path):

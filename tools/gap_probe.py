@@ -11,6 +11,44 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
+def summarise(prof, top=15):
+    """Kernel totals, busy / idle time and the largest idle gaps of a profiled region."""
+    import collections
+    ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
+    ev.sort(key=lambda e: e.time_range.start)
+    t0, t1 = ev[0].time_range.start, max(e.time_range.end for e in ev)
+    busy = 0.0
+    gaps = []
+    end = ev[0].time_range.start
+    prev = None
+    for e in ev:
+        s, f = e.time_range.start, e.time_range.end
+        if s > end:
+            gaps.append((s - end, prev.name[:50] if prev else "-", e.name[:50]))
+        busy += max(0.0, f - max(s, end))
+        if f > end:
+            end, prev = f, e
+    print(f"span {(t1 - t0) / 1e3:.2f} ms  busy {busy / 1e3:.2f} ms  idle {(t1 - t0 - busy) / 1e3:.2f} ms")
+    import collections
+    kt = collections.defaultdict(lambda: [0, 0.0])
+    for e in ev:
+        kt[e.name[:60]][0] += 1
+        kt[e.name[:60]][1] += e.time_range.end - e.time_range.start
+    print("kernel totals:")
+    for n, (c, tot) in sorted(kt.items(), key=lambda kv: -kv[1][1])[:top + 10]:
+        print(f"  {tot / 1e3:8.3f} ms {100 * tot / busy:5.1f}%  {c:4d} x {tot / c:8.1f} us  {n}")
+    gaps.sort(reverse=True)
+    for g, a, b in gaps[:top]:
+        print(f"  gap {g:9.1f} us  after {a:50s} before {b}")
+    by = collections.defaultdict(lambda: [0, 0.0])
+    for g, a, b in gaps:
+        by[(a, b)][0] += 1
+        by[(a, b)][1] += g
+    print("gap totals by (after, before):")
+    for (a, b), (c, tot) in sorted(by.items(), key=lambda kv: -kv[1][1])[:top]:
+        print(f"  {tot:9.1f} us in {c:4d} gaps  {a:40s} -> {b}")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
@@ -48,41 +86,8 @@ def main():
         for k in range(args.steps):
             st = adv((k + 1) * spec.dt)
         torch.cuda.synchronize()
-    ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
-    ev.sort(key=lambda e: e.time_range.start)
-    t0, t1 = ev[0].time_range.start, max(e.time_range.end for e in ev)
-    busy = 0.0
-    gaps = []
-    end = ev[0].time_range.start
-    prev = None
-    for e in ev:
-        s, f = e.time_range.start, e.time_range.end
-        if s > end:
-            gaps.append((s - end, prev.name[:50] if prev else "-", e.name[:50]))
-        busy += max(0.0, f - max(s, end))
-        if f > end:
-            end, prev = f, e
-    print(f"newton={st.newton_iterations} krylov={st.krylov_iterations} kernels={len(ev)}")
-    print(f"span {(t1 - t0) / 1e3:.2f} ms  busy {busy / 1e3:.2f} ms  idle {(t1 - t0 - busy) / 1e3:.2f} ms")
-    import collections
-    kt = collections.defaultdict(lambda: [0, 0.0])
-    for e in ev:
-        kt[e.name[:60]][0] += 1
-        kt[e.name[:60]][1] += e.time_range.end - e.time_range.start
-    print("kernel totals:")
-    for n, (c, tot) in sorted(kt.items(), key=lambda kv: -kv[1][1])[:args.top + 10]:
-        print(f"  {tot / 1e3:8.3f} ms {100 * tot / busy:5.1f}%  {c:4d} x {tot / c:8.1f} us  {n}")
-    gaps.sort(reverse=True)
-    for g, a, b in gaps[:args.top]:
-        print(f"  gap {g:9.1f} us  after {a:50s} before {b}")
-    by = collections.defaultdict(lambda: [0, 0.0])
-    for g, a, b in gaps:
-        by[(a, b)][0] += 1
-        by[(a, b)][1] += g
-    print("gap totals by (after, before):")
-    for (a, b), (c, tot) in sorted(by.items(), key=lambda kv: -kv[1][1])[:args.top]:
-        print(f"  {tot:9.1f} us in {c:4d} gaps  {a:40s} -> {b}")
-
+    print(f"newton={st.newton_iterations} krylov={st.krylov_iterations}")
+    summarise(prof, args.top)
 
 if __name__ == "__main__":
     main()

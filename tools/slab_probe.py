@@ -11,12 +11,15 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--profile", action="store_true",
+                    help="CUPTI kernel totals and idle gaps of one more slab step")
     args = ap.parse_args()
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29533")
@@ -60,6 +63,16 @@ def main():
         res[mode] = (ms / args.steps, kry, u.double().norm().item())
         print(f"{mode:6s} {ms / args.steps:9.2f} ms/step  krylov={kry}  "
               f"{1e3 * ms / kry:8.1f} us/iteration  |u|={res[mode][2]:.15e}", flush=True)
+        if args.profile and mode == "slab":
+            from torch.profiler import ProfilerActivity, profile
+
+            from gap_probe import summarise
+
+            with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+                st = ctx.step_device(u, t, spec.dt)
+                torch.cuda.synchronize()
+            print(f"profiled slab step: newton={st.newton_iterations} krylov={st.krylov_iterations}")
+            summarise(prof, 25)
         del ctx
     print(f"slab/plain time ratio {res['slab'][0] / res['plain'][0]:.3f}")
     dist.destroy_process_group()
