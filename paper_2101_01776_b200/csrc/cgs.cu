@@ -526,9 +526,17 @@ __device__ __forceinline__ double fold_partials(const double *pl, int G, int lan
 
 // One sweep's tile loop (grid-stride over row tiles, NST tiles in flight).
 // LMAX > 0: the row-owner tile work (DOT / UPD_DOT with L <= LMAX).
-template <int MODE, int TRC, int LMAX = 0>
+// sync_point(): what the sweep must wait for before it touches w and the
+// previous sweep's results -- pdl_wait() in a sweep of its own launch; in the
+// fused three-sweep kernel the previous phase's partial stores + a grid barrier
+struct PdlSync {
+  __device__ __forceinline__ void operator()() const { pdl_wait(); }
+};
+
+template <int MODE, int TRC, int LMAX = 0, class SyncF = PdlSync>
 __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q], double &nrm,
-                                          const GWork &W, const double *cin, const double *pin) {
+                                          const GWork &W, const double *cin, const double *pin,
+                                          SyncF sync_point = SyncF()) {
   const int G = A.G, ntiles = A.ntiles;
   const int t0 = blockIdx.x;
   const int NST = A.nst;
@@ -546,7 +554,7 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
       else if (threadIdx.x == 0)
         mbar_arrive(&A.bars[i]);  // the tail tile: generic loads at consumption
     }
-  pdl_wait();
+  sync_point();
   fence_proxy_async_global();  // w was written through the generic proxy
   for (int i = 0; i < NST; ++i)
     if (t0 + i * G < ntiles && tile_full<TRC>(A, ph(t0 + i * G)))
@@ -618,6 +626,50 @@ __device__ __forceinline__ void cgs_tiles(const TileArgs &A, double (&acc)[CGS_Q
     if (++s == NST) {
       s = 0;
       phase ^= 1u;
+    }
+  }
+}
+
+// per-CTA partials of one sweep -> part[l * G + cta]
+template <int MODE>
+__device__ __forceinline__ void cgs_write_partials(int ro, int L, int nd, double (&acc)[CGS_Q],
+                                                   double nrm, double *red, double *part, int G) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (ro && MODE != CGS_UPD_NORM) {
+    // row-owner: every thread holds a partial of every entry; warp sums into
+    // shared memory, then one thread per entry adds the warps in order
+#pragma unroll
+    for (int l = 0; l < 17; ++l) {
+      if (l <= L && l < nd) {
+        const double v = wsum(l == L ? nrm : acc[l]);
+        if (lane == 0) red[warp * 17 + l] = v;
+      }
+    }
+    __syncthreads();
+    if (tid < nd) {
+      double tot = 0.0;
+      for (int w = 0; w < CGS_NW; ++w) tot += red[w * 17 + tid];
+      part[(size_t)tid * G + blockIdx.x] = tot;
+    }
+  } else if (MODE != CGS_UPD_NORM) {
+    const int nq = (nd + CGS_NW - 1) / CGS_NW;
+#pragma unroll
+    for (int q = 0; q < CGS_Q; ++q) {
+      if (q >= nq) break;  // skip the dead slot blocks (cold code at small j)
+      const int l = warp + CGS_NW * q;
+      if (l < nd) {  // warp-uniform
+        const double v = wsum(acc[q]);
+        if (lane == 0) part[(size_t)l * G + blockIdx.x] = v;
+      }
+    }
+  } else {
+    double v = wsum(nrm);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < CGS_NW; ++w) tot += red[w];
+      part[blockIdx.x] = tot;
     }
   }
 }
@@ -706,44 +758,7 @@ __global__ void __launch_bounds__(CGS_BS, 2)
     default: cgs_tiles<MODE, 1024>(A, acc, nrm, W, cin, pin); break;
   }
 
-  // per-CTA partials -> part[l * G + cta]
-  if (ro && MODE != CGS_UPD_NORM) {
-    // row-owner: every thread holds a partial of every entry; warp sums into
-    // shared memory, then one thread per entry adds the warps in order
-#pragma unroll
-    for (int l = 0; l < 17; ++l) {
-      if (l <= L && l < nd) {
-        const double v = wsum(l == L ? nrm : acc[l]);
-        if (lane == 0) red[warp * 17 + l] = v;
-      }
-    }
-    __syncthreads();
-    if (tid < nd) {
-      double tot = 0.0;
-      for (int w = 0; w < CGS_NW; ++w) tot += red[w * 17 + tid];
-      part[(size_t)tid * G + blockIdx.x] = tot;
-    }
-  } else if (MODE != CGS_UPD_NORM) {
-    const int nq = (nd + CGS_NW - 1) / CGS_NW;
-#pragma unroll
-    for (int q = 0; q < CGS_Q; ++q) {
-      if (q >= nq) break;  // skip the dead slot blocks (cold code at small j)
-      const int l = warp + CGS_NW * q;
-      if (l < nd) {  // warp-uniform
-        const double v = wsum(acc[q]);
-        if (lane == 0) part[(size_t)l * G + blockIdx.x] = v;
-      }
-    }
-  } else {
-    double v = wsum(nrm);
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    if (tid == 0) {
-      double tot = 0.0;
-      for (int w = 0; w < CGS_NW; ++w) tot += red[w];
-      part[blockIdx.x] = tot;
-    }
-  }
+  cgs_write_partials<MODE>(ro, L, nd, acc, nrm, red, part, G);
   if (defer) return;  // the next sweep's CTAs fold these partials themselves
   // last-CTA ticket, the grid-sync pattern: the CTA barrier orders every
   // thread's partial store before thread 0's fence + atomic (fence
@@ -782,6 +797,172 @@ __global__ void __launch_bounds__(CGS_BS, 2)
     arnoldi_finish_block(W, sm);
     if (tid == 0 && use_cond > 0) cudaGraphSetConditional(cond, ctrl->cycle_done ? 0u : 1u);
   }
+  if (tid == 0) *counter = 0u;
+}
+
+// ---------------------------------------------------------------------------
+// The three sweeps of one orthogonalisation in ONE launch (single rank).  Same
+// tiles, same per-CTA partials and folds as the three k_cgs launches (results
+// bit-identical), with a grid barrier where a launch boundary was: all G = 2 x
+// #SM CTAs are co-resident (two per SM by construction: the launcher checks the
+// occupancy).  What it buys at short vectors, where a sweep is ~30 us of which
+// ~5 are ramp and tail: the next sweep's first basis tiles are issued BEFORE
+// the barrier (they depend on nothing the previous sweep computes), so they
+// stream in while the partials are exchanged, and two launch transitions go.
+__device__ __forceinline__ void mbar_inval(uint64_t *bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// monotone ticket barrier over all G CTAs (gbar never resets: every launch
+// passes the same number of barriers with every CTA, so it is a multiple of G
+// at launch boundaries); traps instead of hanging if a CTA never arrives
+__device__ __forceinline__ void cgs_grid_barrier(unsigned long long *gbar, int G) {
+  __syncthreads();  // every thread's stores ordered before thread 0's fence + ticket
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long old = atomicAdd(gbar, 1ULL);
+    const unsigned long long target = (old / (unsigned long long)G + 1ULL) * (unsigned long long)G;
+    const long long t0 = clock64();
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(gbar) : "memory");
+      if (v < target && clock64() - t0 > (1LL << 32)) __trap();  // ~2 s: a CTA is not resident
+    } while (v < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+struct GridSync {
+  unsigned long long *gbar;
+  int G;
+  __device__ __forceinline__ void operator()() const { cgs_grid_barrier(gbar, G); }
+};
+
+__device__ __forceinline__ void cgs_ring_reset(uint64_t *bars, int nst) {
+  __syncthreads();  // every tile of the finished sweep is consumed
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nst; ++i) {
+      mbar_inval(&bars[i]);
+      mbar_init(&bars[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+struct Cgs3Args {
+  TileArgs dot, upd, nrmA;
+  double *pdot, *pupd, *pnorm;
+};
+
+template <int TRC, int LMAX>
+__device__ __forceinline__ void cgs3_run(const Cgs3Args &C, const GWork &W, int L, int G,
+                                         unsigned long long *gbar, double *red) {
+  double nrm = 0.0;
+  double acc[CGS_Q];
+#pragma unroll
+  for (int q = 0; q < CGS_Q; ++q) acc[q] = 0.0;
+  // sweep 1: c1 = V^T w, ||w||^2 (slot-owner dots, as k_cgs<DOT> with the default masks)
+  cgs_tiles<CGS_DOT, TRC, 0>(C.dot, acc, nrm, W, nullptr, nullptr);
+  cgs_write_partials<CGS_DOT>(0, L, L + 1, acc, nrm, red, C.pdot, G);
+  cgs_ring_reset(C.dot.bars, C.dot.nst);
+  nrm = 0.0;
+#pragma unroll
+  for (int q = 0; q < CGS_Q; ++q) acc[q] = 0.0;
+  // sweep 2: w1 = w - V c1, c2 = V^T w1
+  cgs_tiles<CGS_UPD_DOT, TRC, LMAX>(C.upd, acc, nrm, W, W.c1, C.pdot, GridSync{gbar, G});
+  cgs_write_partials<CGS_UPD_DOT>(LMAX, L, L, acc, nrm, red, C.pupd, G);
+  cgs_ring_reset(C.dot.bars, C.dot.nst);
+  nrm = 0.0;
+#pragma unroll
+  for (int q = 0; q < CGS_Q; ++q) acc[q] = 0.0;
+  // sweep 3: s_{j+1} = w1 - V c2, ||s_{j+1}||^2
+  cgs_tiles<CGS_UPD_NORM, TRC, LMAX>(C.nrmA, acc, nrm, W, W.c2, C.pupd, GridSync{gbar, G});
+  cgs_write_partials<CGS_UPD_NORM>(LMAX, L, L, acc, nrm, red, C.pnorm, G);
+}
+
+__global__ void __launch_bounds__(CGS_BS, 2)
+    k_cgs3(int n, double *__restrict__ V, long long pitch, GWork W, double *wbuf, double *part,
+           int G, unsigned *counter, unsigned long long *gbar, int ring_doubles, int use_cond,
+           cudaGraphConditionalHandle cond, const char *__restrict__ vmaps, int trmax,
+           int ef_from) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bars[CGS_MAXST];
+  __shared__ double cs[MAXR + 1];
+  __shared__ double red[CGS_BS];
+  __shared__ bool is_last;
+
+  GCtrl *ctrl = W.ctrl;
+  if (ctrl->cycle_done) {  // (uniform over the grid: only this kernel's own finish sets it)
+    if (use_cond > 0 && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const int L = ctrl->j + 1;
+  const int trmax_raw = trmax;
+  const int cgs_rev_mask = (trmax >> 16) & 0xff;
+  trmax &= 0xffff;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // tile geometry: exactly k_cgs's rule (it depends on L alone)
+  int TR = trmax;
+  while (TR > 32 && 2 * (L + 1) * TR > ring_doubles) TR >>= 1;
+  int nst = ring_doubles / ((L + 1) * TR);
+  nst = nst > CGS_MAXST ? CGS_MAXST : nst;
+  IRKG_DCHECK(L >= 1 && L <= MAXR + 1 && nst >= 1 && nst * (L + 1) * TR <= ring_doubles);
+  const int ntiles = (n + TR - 1) / TR;
+  const char *vm = vmaps;
+  if (TR <= 256 && vm) vm += (size_t)(__ffs(TR) - 6) * VM_B * sizeof(CUtensorMap);
+  if (tid == 0) {
+    for (int i = 0; i < nst; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // row-owner update sweeps for short bases in tall tiles (mask 6: the launcher
+  // routes every other IRKG_CGS_RO setting to the three-launch path)
+  const int ro = TR >= CGS_BS ? (L <= 4 ? 4 : L <= 8 ? 8 : L <= 16 ? 16 : 0) : 0;
+  const int m1d = (trmax_raw >> 28) & 7;
+  auto args = [&](int mode, double *out) {
+    const bool one_d = ((m1d >> mode) & 1) && TR >= (mode == CGS_DOT ? 128 : 256);
+    return TileArgs{n, L, G, ntiles, V, pitch, wbuf, out, sm, nst, bars, cs, red,
+                    (TR <= 256 && !one_d) ? vm : nullptr, (cgs_rev_mask >> mode) & 1,
+                    ef_from & 0xffff, 0};
+  };
+  Cgs3Args C{args(CGS_DOT, nullptr), args(CGS_UPD_DOT, wbuf),
+             args(CGS_UPD_NORM, V + (size_t)L * pitch), part + (size_t)(MAXR + 2) * G,
+             part + 2 * (size_t)(MAXR + 2) * G, part};
+  switch (TR * 100 + ro) {
+    case 25604: cgs3_run<256, 4>(C, W, L, G, gbar, red); break;
+    case 25608: cgs3_run<256, 8>(C, W, L, G, gbar, red); break;
+    case 25616: cgs3_run<256, 16>(C, W, L, G, gbar, red); break;
+    case 51204: cgs3_run<512, 4>(C, W, L, G, gbar, red); break;
+    case 51208: cgs3_run<512, 8>(C, W, L, G, gbar, red); break;
+    case 51216: cgs3_run<512, 16>(C, W, L, G, gbar, red); break;
+    case 102404: cgs3_run<1024, 4>(C, W, L, G, gbar, red); break;
+    case 102408: cgs3_run<1024, 8>(C, W, L, G, gbar, red); break;
+    case 102416: cgs3_run<1024, 16>(C, W, L, G, gbar, red); break;
+    case 3200: cgs3_run<32, 0>(C, W, L, G, gbar, red); break;
+    case 6400: cgs3_run<64, 0>(C, W, L, G, gbar, red); break;
+    case 12800: cgs3_run<128, 0>(C, W, L, G, gbar, red); break;
+    case 25600: cgs3_run<256, 0>(C, W, L, G, gbar, red); break;
+    case 51200: cgs3_run<512, 0>(C, W, L, G, gbar, red); break;
+    default: cgs3_run<1024, 0>(C, W, L, G, gbar, red); break;
+  }
+  // last-CTA ticket: fold ||s_{j+1}||^2 and finish the Hessenberg column (as k_cgs<UPD_NORM>)
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    is_last = (atomicAdd(counter, 1u) == (unsigned)(G - 1));
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (warp == 0) {
+    const double v = fold_partials(part, G, lane);
+    if (lane == 0) ctrl->hn2 = v;
+  }
+  __syncthreads();
+  arnoldi_finish_block(W, sm);
+  if (tid == 0 && use_cond > 0) cudaGraphSetConditional(cond, ctrl->cycle_done ? 0u : 1u);
   if (tid == 0) *counter = 0u;
 }
 
@@ -869,6 +1050,28 @@ int Engine::cgs_stage_doubles() const {
   return 2 * (st < 6656 ? 6656 : st);
 }
 
+// The fused three-sweep kernel needs every CTA resident (grid barriers): two
+// CTAs per SM for G = 2 x #SM, checked once with the occupancy calculator;
+// IRKG_CGS_FUSED=0, a non-default IRKG_CGS_RO mask, the phase probe's partial
+// orthogonalisations (1 or 2 sweeps) and the multi-rank path use the three launches.
+bool Engine::cgs_fused_ok(size_t smem, int trm) {
+  if (!cgs_fused || ((trm >> 24) & 7) != 6) return false;
+  if (cgs_fused_occ < 0 || cgs_fused_smem != smem) {
+    check(cudaFuncSetAttribute(k_cgs3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+          "smem attr");
+    max_carveout((const void *)k_cgs3);
+    int nb = 0;
+    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cgs3, CGS_BS, smem), "occupancy");
+    cgs_fused_occ = nb;
+    cgs_fused_smem = smem;
+    if (!gbar) {
+      dalloc_raw((void **)&gbar, sizeof(unsigned long long));
+      check(cudaMemset(gbar, 0, sizeof(unsigned long long)), "memset");
+    }
+  }
+  return (long long)cgs_fused_occ * sms >= G;
+}
+
 // One Arnoldi orthogonalisation: 3 fused sweeps; the last also finishes the
 // Hessenberg column (Givens, estimate, exit test) in its final CTA.
 void Engine::cgs(long long n, int nsweeps) {
@@ -889,6 +1092,13 @@ void Engine::cgs(long long n, int nsweeps) {
   const int trm = cgs_trmax();
   const double *cnull = nullptr;
   double *dnull = nullptr;
+  if (nsweeps == 3 && cgs_fused_ok(smem, trm)) {
+    // one launch for the three sweeps (grid barriers in between)
+    launch_pdl_l2(true, k_cgs3, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W, wbuf, part, G,
+                  counter, gbar, stage, uc, cond_handle, maps, trm, ef);
+    count(1);
+    return;
+  }
   // DOT and UPD_DOT leave per-CTA partials in their own regions of `part`;
   // the next sweep folds them in every CTA (no last-CTA fold between sweeps)
   double *pdot = part + (size_t)(MAXR + 2) * G, *pupd = part + 2 * (size_t)(MAXR + 2) * G;

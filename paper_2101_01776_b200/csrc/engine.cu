@@ -130,6 +130,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   halo_overlap = nranks > 1;
   if (const char *e = getenv("IRKG_HALO_OVERLAP")) halo_overlap = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_EXT_HALO")) ext_halo = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_CGS_FUSED")) cgs_fused = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_BOP_WPS")) bop_wps = atoi(e) > 0 ? atoi(e) : 8;
   for (int i = 0; i < MAXS; ++i)
     for (int j = 0; j < MAXS; ++j) od_slot[i][j] = -1;
@@ -137,7 +138,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
 
 Engine::~Engine() {
   cudaStreamSynchronize(stream);
-  void *bufs[] = {part, counter, scal_dev, ctrl_dev, W.H, W.cs, W.sn, W.g, W.alpha, W.y,
+  void *bufs[] = {gbar, part, counter, scal_dev, ctrl_dev, W.H, W.cs, W.sn, W.g, W.alpha, W.y,
                   W.c1, W.c2, W.res, V, wbuf, zbuf, ubuf, tmp_x, tmp_t, U, F, Gs, Y, DK,
                   Kst, RHS, ufield, opA, vmaps, zero_n, rc.Z};
   for (void *b : bufs)

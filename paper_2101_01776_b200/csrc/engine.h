@@ -236,6 +236,15 @@ struct Engine {
   void drop_graphs();
   int cgs_stage_doubles() const;  // CGS shared-memory ring per CTA (doubles)
   void cgs(long long n, int nsweeps = 3);  // cgs.cu
+  // the three sweeps in one launch with grid barriers (k_cgs3, IRKG_CGS_FUSED=1).  Off by
+  // default: bit-identical, faster in isolation at j <= 4 (37.8 vs 46.5 us at j = 2) but not
+  // at the step's mean Arnoldi index -- configs[1] 27.36 vs 27.01 ms/step on the same box
+  // (profiles/r2s4_cgs_fused_ab.txt)
+  bool cgs_fused = false;
+  int cgs_fused_occ = -1;
+  size_t cgs_fused_smem = 0;
+  unsigned long long *gbar = nullptr;
+  bool cgs_fused_ok(size_t smem, int trm);
   // stencil.cu (register-sliding 2-D / 3-D kernels)
   dim3 slide_grid(int &span) const;
   void jac_sweep_s(const Op &L, double alpha, double dt, const VecIn &vin, int in_off,

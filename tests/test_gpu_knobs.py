@@ -1,8 +1,8 @@
 """Scheduling knobs change when and how the engine's kernels run, never what
 they compute: one IRK step of a Burgers problem must be bit-identical (state
 and Newton/Krylov counts) with CUDA graphs off, programmatic dependent launch
-off, one Arnoldi step per WHILE-body trip, and without the L2 persisting
-window / evict-first hints.  (Each variant runs in a fresh process: the
+off, one Arnoldi step per WHILE-body trip, without the L2 persisting
+window / evict-first hints, and with the three CGS2 sweeps fused into one launch.  (Each variant runs in a fresh process: the
 knobs are read when the engine is created.)"""
 
 import json
@@ -41,6 +41,10 @@ VARIANTS = {
     "no_pdl": {"IRKG_PDL": "0"},
     "unroll1": {"IRKG_GRAPH_UNROLL": "1"},
     "no_l2_policy": {"IRKG_L2_MB": "0", "IRKG_CGS_EF": "0"},
+    # the three CGS2 sweeps in one launch (k_cgs3: same tiles, same partial sums and
+    # folds, grid barriers where the launch boundaries were)
+    "cgs_one_launch": {"IRKG_CGS_FUSED": "1"},
+    "cgs_one_launch_no_graphs": {"IRKG_CGS_FUSED": "1", "IRKG_GRAPHS": "0", "IRKG_PDL": "0"},
 }
 
 
