@@ -177,3 +177,45 @@ def test_block_gmres_ring_slot_reuse_after_tail_tile():
     assert rep.converged and repo.converged
     assert abs(rep.iterations - repo.iterations) <= 1, (rep.iterations, repo.iterations)
     assert np.linalg.norm(x - xo) <= 1e-7 * np.linalg.norm(xo)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_linear_problem_takes_one_newton_iteration_and_variants_agree(variant):
+    """Mirrors pkg/tests/test_nonlinear.py:138-157 of the reference: on a linear
+    problem every linearization variant is the exact Jacobian -- one Newton
+    iteration, and the same step for all variants (to the Krylov tolerance)."""
+    prob = GridProblem("rad", (40, 24), nu=0.02, c=0.3, lam=-0.7, mu=0.0)
+    u0 = pk.fourier_u0(prob.shape, 1, 3, 0.3, 5)
+    tab = pk.make_tableau("gauss", 3)
+
+    def run(v):
+        cfg = pk.SolverConfig(variant=v, newton_rtol=1e-9, krylov_rtol=1e-12, krylov_maxit=2000,
+                              precond=pk.PrecondSpec(inner=4))
+        return pk.step(prob, u0, 0.0, 1e-2, tab, cfg)
+
+    u, st = run(variant)
+    u3, _ = run(3)
+    assert st.newton_iterations == 1
+    assert np.linalg.norm(u - u3) <= 1e-11 * np.linalg.norm(u3)
+
+
+def test_dahlquist_closed_forms():
+    """Mirrors pkg/tests/test_nonlinear.py:221-267: u' = lam u (rad kind with
+    nu = c = mu = 0, every grid point an independent scalar problem).  Backward
+    Euler (Radau IIA, s = 1) multiplies by 1 / (1 - dt lam), the implicit midpoint
+    rule (Gauss, s = 1) by (1 + dt lam / 2) / (1 - dt lam / 2); ten steps give the
+    tenth power; Gauss(2) is the (2, 2) Pade approximant of exp."""
+    lam, dt = -1.0, 0.1
+    prob = GridProblem("rad", (32,), nu=0.0, c=0.0, lam=lam, mu=0.0)
+    u0 = np.linspace(0.5, 1.5, 32)
+    cfg = pk.SolverConfig(newton_rtol=1e-12, krylov_rtol=1e-12, precond=pk.PrecondSpec(inner=1))
+    z = dt * lam
+    for family, s, per in [("radau_iia", 1, 1.0 / (1.0 - z)),
+                           ("gauss", 1, (1.0 + z / 2) / (1.0 - z / 2)),
+                           ("gauss", 2, (1 + z / 2 + z * z / 12) / (1 - z / 2 + z * z / 12))]:
+        tab = pk.make_tableau(family, s)
+        u1, st = pk.step(prob, u0, 0.0, dt, tab, cfg)
+        assert np.max(np.abs(u1 - per * u0)) <= 1e-11, (family, s)
+        res = pk.integrate(prob, u0, 0.0, 10 * dt, dt, tab, cfg)
+        assert np.max(np.abs(res.u_final - per ** 10 * u0)) <= 1e-10, (family, s)
+        assert len(res.step_stats) == 10
