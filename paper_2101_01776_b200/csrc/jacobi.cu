@@ -459,8 +459,10 @@ __global__ void __launch_bounds__(JSPW * 32, 12 / JSPW)
   // halo) E rows beyond them on either side, computed redundantly from a
   // deeper halo of the input and stored into the output's ghost planes -- the
   // consumer then needs no halo exchange of this chain's result
-  const int y0 = ylo + band * span;
-  const int y1 = min(yhi, y0 + span);
+  // (single rank: ylo = 0, yhi = ny, folded at compile time -- the recompiled kernel with the
+  // run-time bounds cost 1.6 us per launch inside the step graph, 2 % of a configs[1] step)
+  const int y0 = (SLAB ? ylo : 0) + band * span;
+  const int y1 = min(SLAB ? yhi : ny, y0 + span);
 
   // sliding windows (index K-1 / 2 = newest row)
   double AW[K][2];      // a, rows t-K+1 .. t
