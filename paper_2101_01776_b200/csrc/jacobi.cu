@@ -429,8 +429,11 @@ struct JacCoef {
   double xym, xyp;    // the y-terms regrouped: xym x_m + xyp x_p
 };
 
+#ifndef IRKG_JSP_MINB
+#define IRKG_JSP_MINB 12  // resident one-warp CTAs per SM the compiler must allow (register cap)
+#endif
 template <int KIND, int K, bool SLAB>
-__global__ void __launch_bounds__(JSPW * 32, 12 / JSPW)
+__global__ void __launch_bounds__(JSPW * 32, IRKG_JSP_MINB / JSPW)
     k_jacobi_sp2d(Grid g, Op L, JacCoef jc, VecIn vin, int in_off, FRef zcr, double cpl,
                   double *__restrict__ x_out, int span, int strips, int nwarps, int band0,
                   GCtrl *flag_ctrl, const GCtrl *skip, int ylo, int yhi, double *out_lo,
