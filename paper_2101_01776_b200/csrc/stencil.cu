@@ -328,8 +328,11 @@ constexpr int bop_nf() {
   return SIZE == 1 ? 2 : 6;  // ring fields: z1, a1 [, z2, a2, c12, c21]
 }
 
+#ifndef IRKG_BOP_MINB
+#define IRKG_BOP_MINB 16  // resident one-warp CTAs per SM the compiler must allow (register cap)
+#endif
 template <int KIND, int SIZE, bool SLAB>
-__global__ void __launch_bounds__(BPW * 32, 16 / BPW)
+__global__ void __launch_bounds__(BPW * 32, IRKG_BOP_MINB / BPW)
     k_block_op_strip(Grid g, KindParams kp, double eta, double beta, double phi, double dt,
                      Op l1, Op l2, Op c12, Op c21, FRef z1r, FRef z2r, double *__restrict__ w,
                      const double *__restrict__ b, int span, int strips, int nwarps, int band0,
