@@ -56,6 +56,9 @@ def _run(tmp_path, nproc, *args, env=None):
          "--dt", "2e-3"]),
     (3, ["--kind", "arakawa", "--shape", "32,36", "--family", "gauss", "--stages", "4",
          "--dt", "2e-3"]),
+    # nx >= 64: the warp-strip Arakawa chain (csrc/arachain.cu k_ara_sp2d) on slabs with ghost rows
+    (2, ["--kind", "arakawa", "--shape", "64,48", "--family", "gauss", "--stages", "2",
+         "--dt", "2e-3"]),
 ])
 def test_slab_partition_matches_single_rank(tmp_path, nproc, args):
     r = _run(tmp_path, nproc, *args)
