@@ -44,7 +44,7 @@ def main():
     dae = args.kind == "arakawa"
     if dae:
         # vorticity/streamfunction DAE (configs[4] form): state [omega; psi],
-        # each slab-partitioned; the constraint solve gathers across ranks
+        # each slab-partitioned; the constraint solve is a slab -> pencil transpose FFT
         prob = pk.VorticityProblem(shape, nu=1e-3)
         w0, p0 = pk.vorticity_initial_state(prob, seed=3)
         u0 = np.concatenate([w0, p0])
