@@ -199,7 +199,10 @@ def _dae_worker(rank, nranks, port, shape, queue):
     differential operator on slabs with one full ghost plane each side (the
     corners come with the planes), and the constraint solve on the gathered
     right-hand side -- each rank's slab zero-padded into the global vector and
-    all-reduced (exact), solved globally, own slab kept."""
+    all-reduced (exact), solved globally, own slab kept.  (The device path
+    replaced the gather by the slab -> pencil transpose FFT restated in
+    _pencil_worker below; the gathered form stays as the P-independence check
+    of the slab operators and of the pinned row.)"""
     import scipy.sparse.linalg as spla
 
     from oracle.problems import DaeProblemDef
