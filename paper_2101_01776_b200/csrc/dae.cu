@@ -19,6 +19,8 @@
 // Weighted sums collapse to a = sum_k w_k Psi_k (J is linear in psi), sigma.
 #include <cufft.h>
 
+#include <cstddef>
+
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -843,7 +845,9 @@ void Engine::dae_transformed_solve(double dt, const double *rhs, double *dk,
                                                     part, counter, &scal_dev[6]);
     count(1);
     allreduce(&scal_dev[6], 2);
-    double rb[2];
+    // (through the pinned control-block mirror: a pageable destination staged the copy)
+    double *rb = &ctrl_host->rr;  // rr, scalar: two adjacent doubles of the host mirror
+    static_assert(offsetof(GCtrl, scalar) == offsetof(GCtrl, rr) + sizeof(double), "GCtrl layout");
     check(cudaMemcpyAsync(rb, &scal_dev[6], 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
     check(cudaStreamSynchronize(stream));
     if (rb[1] > 0.0) {
