@@ -16,7 +16,10 @@ namespace irkg {
 
 namespace {
 
-constexpr int SBX = 128;  // threads per CTA
+#ifndef IRKG_SBX
+#define IRKG_SBX 128
+#endif
+constexpr int SBX = IRKG_SBX;  // threads per CTA (3-D: a 32 x SBX/32 in-plane tile)
 
 // Geometry of the slide: plane size P, number of planes NS, in-plane extents.
 struct Slide {
