@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--dt", type=float, default=5e-4)
     ap.add_argument("--nsteps", type=int, default=2)
     ap.add_argument("--transport", default="callback")
+    ap.add_argument("--inner", type=int, default=4)
     ap.add_argument("--out", required=True)
     args = ap.parse_args()
 
@@ -72,7 +73,7 @@ def main():
 
     tab = pk.make_tableau(args.family, args.stages)
     prep = pk.prepare_stages(tab)
-    cfg = pk.SolverConfig(krylov_maxit=5000, precond=pk.PrecondSpec(inner=4))
+    cfg = pk.SolverConfig(krylov_maxit=5000, precond=pk.PrecondSpec(inner=args.inner))
 
     ctx = SlabContext(prob, rank, ws, transport=args.transport)
     ctx.set_prep(prep)

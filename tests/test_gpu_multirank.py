@@ -48,6 +48,12 @@ def _run(tmp_path, nproc, *args, env=None):
     (3, ["--kind", "burgers", "--shape", "64,50", "--family", "gauss", "--stages", "3"]),
     (3, ["--kind", "nldiff", "--shape", "96,50", "--family", "radau_iia", "--stages", "2",
          "--dt", "2e-4"]),
+    # other sweep counts: K = 2 (v_j halo of 3 planes) and K = 6 (2(K-1)+1 = 11 planes exceed the
+    # ghost buffers: the step falls back to exchanging z1 / z2)
+    (2, ["--kind", "burgers", "--shape", "64,48", "--family", "gauss", "--stages", "2",
+         "--inner", "2"]),
+    (2, ["--kind", "nldiff", "--shape", "64,48", "--family", "gauss", "--stages", "2",
+         "--dt", "2e-4", "--inner", "6"]),
     # in-plane extents >= 32: the 3.5-D blocked chain (csrc/jacobi3d.cu) on z-slabs with ghost planes
     (2, ["--kind", "nldiff", "--shape", "32,34,16", "--family", "gauss", "--stages", "2",
          "--dt", "1e-3"]),
