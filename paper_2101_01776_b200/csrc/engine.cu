@@ -398,7 +398,7 @@ void Engine::arnoldi_iteration_slab(const BlockSpec &B, long long n, int j_host)
     // chains compute the ghost rows of z1 (K rows: chain 2's reach + the
     // operator's) and z2 (1 row) themselves, so neither needs an exchange
     auto chain1 = [&] {
-      chain_ext = B.size == 2 ? K1 + 1 : 1;
+      chain_ext = B.size == 2 ? B.inner : 1;  // chain 2's reach K-1, plus the operator's row
       chain_out_role = R_Z0;
       jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vslot, 0, nullptr, 0.0, zbuf, ctrl_dev);
       chain_ext = 0;

@@ -846,7 +846,7 @@ void Engine::precond(const BlockSpec &B, const void *vin_p, double *z, const GCt
   }
   if (ext) {
     // the chains compute the ghost rows of z1 / z2 themselves (see arnoldi_iteration_slab)
-    chain_ext = B.size == 2 ? jhalo() + 1 : 1;
+    chain_ext = B.size == 2 ? B.inner : 1;  // chain 2's reach K-1, plus the operator's row
     chain_out_role = R_Z0;
     jacobi_chain(B.l1, B.eta, B.dt, B.inner, &vin, 0, nullptr, 0.0, z, skip);
     if (B.size == 2) {

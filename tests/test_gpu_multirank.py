@@ -52,6 +52,8 @@ def _run(tmp_path, nproc, *args, env=None):
     # ghost buffers: the step falls back to exchanging z1 / z2)
     (2, ["--kind", "burgers", "--shape", "64,48", "--family", "gauss", "--stages", "2",
          "--inner", "2"]),
+    (2, ["--kind", "burgers", "--shape", "64,48", "--family", "gauss", "--stages", "2",
+         "--inner", "1"]),
     (2, ["--kind", "nldiff", "--shape", "64,48", "--family", "gauss", "--stages", "2",
          "--dt", "2e-4", "--inner", "6"]),
     # in-plane extents >= 32: the 3.5-D blocked chain (csrc/jacobi3d.cu) on z-slabs with ghost planes
