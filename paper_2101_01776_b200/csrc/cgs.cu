@@ -1054,8 +1054,9 @@ int Engine::cgs_stage_doubles() const {
 // CTAs per SM for G = 2 x #SM, checked once with the occupancy calculator;
 // IRKG_CGS_FUSED=0, a non-default IRKG_CGS_RO mask, the phase probe's partial
 // orthogonalisations (1 or 2 sweeps) and the multi-rank path use the three launches.
-bool Engine::cgs_fused_ok(size_t smem, int trm) {
+bool Engine::cgs_fused_ok(size_t smem, int trm, long long n) {
   if (!cgs_fused || ((trm >> 24) & 7) != 6) return false;
+  if (cgs_fused_maxn > 0 && n > cgs_fused_maxn) return false;  // short vectors only
   if (cgs_fused_occ < 0 || cgs_fused_smem != smem) {
     check(cudaFuncSetAttribute(k_cgs3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
           "smem attr");
@@ -1092,7 +1093,7 @@ void Engine::cgs(long long n, int nsweeps) {
   const int trm = cgs_trmax();
   const double *cnull = nullptr;
   double *dnull = nullptr;
-  if (nsweeps == 3 && cgs_fused_ok(smem, trm)) {
+  if (nsweeps == 3 && cgs_fused_ok(smem, trm, n)) {
     // one launch for the three sweeps (grid barriers in between)
     launch_pdl_l2(true, k_cgs3, dim3(G), dim3(CGS_BS), smem, (int)n, V, vpitch, W, wbuf, part, G,
                   counter, gbar, stage, uc, cond_handle, maps, trm, ef);

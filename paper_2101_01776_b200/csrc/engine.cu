@@ -131,6 +131,7 @@ Engine::Engine(const irkg_problem &p, int dev, cudaStream_t st, int rank_, int n
   if (const char *e = getenv("IRKG_HALO_OVERLAP")) halo_overlap = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_EXT_HALO")) ext_halo = (atoi(e) != 0);
   if (const char *e = getenv("IRKG_CGS_FUSED")) cgs_fused = (atoi(e) != 0);
+  if (const char *e = getenv("IRKG_CGS_FUSED_MAXN")) cgs_fused_maxn = atoll(e);
   if (const char *e = getenv("IRKG_BOP_WPS")) bop_wps = atoi(e) > 0 ? atoi(e) : 8;
   for (int i = 0; i < MAXS; ++i)
     for (int j = 0; j < MAXS; ++j) od_slot[i][j] = -1;

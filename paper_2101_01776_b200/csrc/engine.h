@@ -244,7 +244,8 @@ struct Engine {
   int cgs_fused_occ = -1;
   size_t cgs_fused_smem = 0;
   unsigned long long *gbar = nullptr;
-  bool cgs_fused_ok(size_t smem, int trm);
+  long long cgs_fused_maxn = 0;  // IRKG_CGS_FUSED_MAXN: fuse only sweeps over at most this many rows
+  bool cgs_fused_ok(size_t smem, int trm, long long n);
   // stencil.cu (register-sliding 2-D / 3-D kernels)
   dim3 slide_grid(int &span) const;
   void jac_sweep_s(const Op &L, double alpha, double dt, const VecIn &vin, int in_off,
