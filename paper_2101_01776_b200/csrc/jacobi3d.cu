@@ -267,8 +267,6 @@ __global__ void __launch_bounds__(T3THREADS, 1)
 #pragma unroll
     for (int m = 2; m <= K; ++m) {
       // sweep m-1's newest plane enters its window and its shared plane
-      constexpr int dummy = 0;
-      (void)dummy;
       double *wp = wr + (size_t)(m - 2) * 2 * NPL * T3P;
       const double *rp = rd + (size_t)(m - 2) * 2 * NPL * T3P;
       const int IN = U;                          // index of sweep m-1's plane rho + 1
