@@ -6,7 +6,9 @@
 // (src/dae.py's blocks; csrc/dae.cu ara_lx):
 //     x_0 = 0;  x_m = x_{m-1} + (2/3) D^{-1} (r - (alpha I - dt L_u) x_{m-1}),  m = 1..K
 // in ONE pass over the grid instead of K (the unfused path launches K 9-point
-// sweeps, each re-reading Psi, x and r: half of a configs[4] step).  A CTA of
+// sweeps, each re-reading Psi, x and r: half of a configs[4] step).  Two
+// forms: warp strips of column pairs (k_ara_sp2d, further down: the default
+// for even nx >= 64) and, for the other grids, CTA strips (k_ara_chain): a CTA of
 // 256 threads owns a strip of 256 columns (halo K-1 on each side: 258-2K
 // columns out) and slides along y through a band of rows, one column per
 // thread.  Sweep m runs two rows behind sweep m-1, so everything a step reads
